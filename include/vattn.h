@@ -1,0 +1,225 @@
+/*
+ * vattn.h — C ABI of the B200-native vAttention hot path (libvattn.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point returns a vattn_status
+ * (0 = OK).  On failure vattn_last_error() returns a message for the calling thread.
+ *
+ * Reference interface each group replaces (paths under /root/reference/pkg/src/kvsim/):
+ *   vattn_create / vattn_destroy      KVCacheManager.__init__            manager.py:85-130
+ *   vattn_alloc_reqid                 KVCacheManager.alloc_reqid         manager.py:163-178
+ *   vattn_free_reqid                  KVCacheManager.free_reqid          manager.py:180-190
+ *   vattn_step                        KVCacheManager.step                manager.py:255-296
+ *   vattn_plan_overlap / _plan_fetch  KVCacheManager.plan_overlap        manager.py:298-311
+ *   vattn_execute_plan                KVCacheManager.execute_plan        manager.py:313-333
+ *   vattn_eager_prepare               KVCacheManager.eager_prepare       manager.py:335-361
+ *   vattn_reclaim                     KVCacheManager.reclaim             manager.py:363-372
+ *   vattn_reclaim_until               KVCacheManager._reclaim_until      manager.py:238-251
+ *   vattn_bg_submit / vattn_bg_wait   _VattentionRuntime.background      simulator.py:199-203
+ *                                     (execute_plan -> eager_prepare -> reclaim, on a real thread)
+ *   vattn_slot_state / vattn_counters / vattn_api_stats / vattn_buffer_mappings / vattn_events
+ *                                     introspection read by the reference tests: RequestSlot
+ *                                     manager.py:66-75, PhysicalPool vmm.py:102-127,
+ *                                     VmmDevice.calls/ledger_us vmm.py:172-173,
+ *                                     VirtualKVBuffer.mappings vmm.py:141-147
+ *   vattn_buffer_base                 Table 3 `init` "returns a list of KV cache tensors"
+ *                                     (PAPER.md:434-437); the VA of buffer i never moves
+ *   vattn_kv_append / vattn_decode / vattn_prefill
+ *                                     no reference code; semantics of
+ *                                     flash_attn_with_kvcache as used by PAPER.md:511
+ *
+ * Error codes map 1:1 onto the reference exceptions (manager.py:28-33, vmm.py:26-47).
+ */
+#ifndef VATTN_H_
+#define VATTN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum vattn_status {
+  VATTN_OK = 0,
+  VATTN_BATCH_FULL = 1,        /* BatchFullError      manager.py:28 */
+  VATTN_DOUBLE_FREE = 2,       /* DoubleFreeError     manager.py:32 */
+  VATTN_VALUE_ERROR = 3,       /* ValueError          manager.py:86,100-109,265-272 */
+  VATTN_POOL_EXHAUSTED = 4,    /* PoolExhaustedError  vmm.py:34 */
+  VATTN_MAPPING_ERROR = 5,     /* MappingError        vmm.py:38 */
+  VATTN_ALIGNMENT_ERROR = 6,   /* AlignmentError      vmm.py:30 */
+  VATTN_INVALID_FREE = 7,      /* InvalidFreeError    vmm.py:42 */
+  VATTN_LATENCY_CONFIG = 8,    /* LatencyConfigError  vmm.py:46 */
+  VATTN_CUDA_ERROR = 9,        /* driver / runtime failure */
+  VATTN_UNSUPPORTED = 10,      /* shape / layout the kernels do not cover */
+  VATTN_BAD_STATE = 11         /* misuse (e.g. bg_wait without submit) */
+} vattn_status;
+
+typedef enum vattn_backend {
+  VATTN_BACKEND_SHADOW = 0,    /* bookkeeping only (no device); used by CPU parity tests */
+  VATTN_BACKEND_CUDA = 1       /* real cuMemAddressReserve/cuMemCreate/cuMemMap/cuMemSetAccess */
+} vattn_backend;
+
+typedef struct vattn_latency_entry {
+  const char* api;             /* e.g. "cuMemMap" (vmm.py:55-68 names) */
+  int64_t page_group_bytes;
+  double us;
+} vattn_latency_entry;
+
+typedef struct vattn_config {
+  /* ModelGeometry (geometry.py:64-117) */
+  int32_t n_layers;
+  int32_t kv_heads_total;
+  int32_t head_dim;
+  int32_t bytes_per_elem;
+  int32_t tp_degree;
+  int32_t n_q_heads_total;     /* build addition; 0 = kv_heads_total */
+  int64_t max_context;
+  int64_t max_batch;
+  /* ManagerConfig (manager.py:42-63) */
+  int64_t page_group_size;
+  int64_t pool_bytes;
+  double reclaim_threshold;
+  double pre_create_fraction;
+  int64_t eager_groups;
+  int32_t sliced;
+  /* build additions */
+  int32_t backend;             /* vattn_backend */
+  int32_t device;              /* CUDA ordinal for VATTN_BACKEND_CUDA */
+  int32_t release_physical;    /* 1: cuMemRelease on unmap; 0: recycle the 2 MiB handle */
+  int32_t log_events;          /* 1: keep the (op, buffer, offset) log for vattn_events */
+  int32_t batch_set_access;    /* 1: coalesce cuMemSetAccess over contiguous page runs */
+  const vattn_latency_entry* latency;  /* NULL = Table 2 defaults (vmm.py:55-68) */
+  int32_t n_latency;
+} vattn_config;
+
+typedef struct vattn_t vattn_t;
+
+typedef struct vattn_step_result {
+  int32_t ok;                  /* StepResult.ok (manager.py:78-81) */
+  double sync_us;              /* StepResult.sync_us: modelled Table-2 µs */
+  double wall_us;              /* measured host wall time of this call (driver calls incl.) */
+  double bg_wait_us;           /* time spent joining an outstanding background window */
+} vattn_step_result;
+
+typedef struct vattn_counters {
+  int64_t created, mapped, precreated, total_mapped_bytes;
+  int64_t capacity, page_group_size;
+  int64_t buffer_count, groups_per_slot, slot_stride, buffer_size;
+  int64_t per_buffer_token_bytes, max_batch, max_context;
+  int64_t eager_slot;          /* -1 = None */
+  int64_t next_handle_id;
+  double init_us, charged_us;
+  /* measured (real backend) */
+  int64_t real_maps, real_unmaps, real_set_access_calls, real_creates, real_releases;
+  double real_map_wall_us, real_unmap_wall_us, real_create_wall_us, real_set_access_wall_us;
+  double init_wall_us;
+} vattn_counters;
+
+typedef struct vattn_bg_result {
+  double plan_us, eager_us, reclaim_us;   /* modelled µs per component */
+  int64_t reclaimed_groups;
+  double bg_wall_us;                      /* wall time the background thread worked */
+  double waited_us;                       /* how long vattn_bg_wait blocked */
+} vattn_bg_result;
+
+/* background job flags, executed in this order (simulator.py:199-203) */
+#define VATTN_BG_EXECUTE_PLAN 1u
+#define VATTN_BG_EAGER 2u
+#define VATTN_BG_RECLAIM 4u
+
+/* ---- lifecycle --------------------------------------------------------------------- */
+const char* vattn_last_error(void);
+int32_t vattn_abi_version(void);
+vattn_status vattn_create(const vattn_config* cfg, vattn_t** out);
+vattn_status vattn_destroy(vattn_t* h);
+
+/* ---- Table 3 API + §6.1 optimisations ---------------------------------------------- */
+vattn_status vattn_alloc_reqid(vattn_t* h, int32_t* req_id);
+vattn_status vattn_free_reqid(vattn_t* h, int32_t req_id);
+vattn_status vattn_step(vattn_t* h, const int64_t* seq_lens, int32_t n, vattn_step_result* out);
+vattn_status vattn_plan_overlap(vattn_t* h, const int64_t* next_seq_lens, int32_t n,
+                                int64_t* n_entries);
+vattn_status vattn_plan_fetch(vattn_t* h, int64_t* triples, int64_t cap_entries);
+vattn_status vattn_execute_plan(vattn_t* h, const int64_t* triples, int64_t n_entries,
+                                double* us);
+vattn_status vattn_eager_prepare(vattn_t* h, int64_t k_groups /* <0: config */, double* us);
+vattn_status vattn_reclaim(vattn_t* h, int64_t* freed, double* us);
+vattn_status vattn_reclaim_until(vattn_t* h, int64_t target_available_bytes, int64_t* freed,
+                                 double* us);
+/* background thread: triples == NULL reuses the last vattn_plan_overlap result */
+vattn_status vattn_bg_submit(vattn_t* h, const int64_t* triples, int64_t n_entries,
+                             uint32_t flags, int64_t eager_k);
+vattn_status vattn_bg_wait(vattn_t* h, vattn_bg_result* out);
+/* unmap fence: record "the KV cache may be read by work queued on `stream` so far" */
+vattn_status vattn_mark_use(vattn_t* h, void* stream);
+
+/* ---- introspection ------------------------------------------------------------------ */
+vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out);
+/* 5 int64 per slot: active, context_len, mapped_groups, phase(0 inactive,1 prefill,2 decode),
+ * freed_seq */
+vattn_status vattn_slot_state(vattn_t* h, int64_t* out, int64_t cap_slots);
+int32_t vattn_api_count(void);
+const char* vattn_api_name(int32_t i);
+/* calls[i] and ledger_us[i] per API i (vattn_api_name order) + first-charge order */
+vattn_status vattn_api_stats(vattn_t* h, int64_t* calls, double* ledger_us, int32_t* order,
+                             int32_t* n_order);
+vattn_status vattn_buffer_mappings(vattn_t* h, int32_t buffer_id, int64_t* offsets,
+                                   int64_t* handle_ids, int64_t cap, int64_t* n);
+/* drain the event log: triples (0=map|1=unmap, buffer_id, offset) */
+vattn_status vattn_events(vattn_t* h, int64_t* triples, int64_t cap_entries, int64_t* n);
+vattn_status vattn_buffer_base(vattn_t* h, int32_t buffer_id, uint64_t* dptr);
+
+/* ---- kernels (bf16 K/V/Q/O; layouts in DESIGN.md §3) --------------------------------- */
+/* Write k_new/v_new [batch, n_new, Hkv, D] at rows cache_seqlens[b] + i of slot
+ * cache_batch_idx[b] (NULL = identity) of layer `layer`.  Device int32 arrays. */
+vattn_status vattn_kv_append(vattn_t* h, int32_t layer, const void* k_new, const void* v_new,
+                             int32_t batch, int32_t n_new, const int32_t* cache_seqlens,
+                             const int32_t* cache_batch_idx, void* stream);
+/* o[b, :, :] = softmax(q[b] K[slot, :seqlen]ᵀ · scale) V ; q/o [batch, Hq, D]. */
+vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, int32_t batch,
+                          const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                          float scale, int32_t num_splits /* 0 = auto */, void* stream);
+/* causal (bottom-right) prefill of q [n_q, Hq, D] against slot rows [0, kv_len). */
+vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
+                           int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
+                           void* stream);
+
+/* ---- standalone kernels (no manager; caller-owned device memory) ------------------------ */
+typedef struct vattn_cache_desc {
+  const void* k_base;          /* token-major [slots, slot_tokens, Hkv, D] with slot stride */
+  const void* v_base;
+  int64_t slot_stride_bytes;
+  int64_t token_stride_bytes;  /* 0 = Hkv*D*2 (per-layer buffers); N*Hkv*D*2 when layer-sliced */
+  int32_t slot_tokens;         /* rows addressable per slot (>= every seqlen) */
+  int32_t n_slots;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+} vattn_cache_desc;
+
+vattn_status vattn_kv_append_raw(const vattn_cache_desc* c, const void* k_new, const void* v_new,
+                                 int32_t batch, int32_t n_new, const int32_t* cache_seqlens,
+                                 const int32_t* cache_batch_idx, void* stream);
+vattn_status vattn_decode_raw(const vattn_cache_desc* c, const void* q, void* out,
+                              int32_t batch, int32_t n_q_heads, const int32_t* cache_seqlens,
+                              const int32_t* cache_batch_idx, float scale, int32_t num_splits,
+                              void* workspace, int64_t workspace_bytes, void* stream);
+vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
+                               int32_t n_q_heads, int32_t req_slot, int32_t kv_len, float scale,
+                               int32_t causal, void* stream);
+/* Paged-layout comparison kernel (PagedAttention block table; PAPER.md:602 block sizes):
+ * pools [num_blocks, block_size, Hkv, D], block_table [batch, max_blocks] int32. */
+vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,
+                                int32_t num_blocks, int32_t block_size, int32_t n_kv_heads,
+                                int32_t head_dim, const int32_t* block_table,
+                                int32_t max_blocks_per_seq, void* out, int32_t batch,
+                                int32_t n_q_heads, const int32_t* seqlens, float scale,
+                                int32_t num_splits, void* workspace, int64_t workspace_bytes,
+                                void* stream);
+/* split count the auto heuristic picks for `batch` rows x Hkv heads at max_seqlen tokens */
+int32_t vattn_decode_num_splits(int32_t batch, int32_t n_kv_heads, int32_t max_seqlen);
+int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t n_q_heads, int32_t head_dim,
+                                     int32_t num_splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VATTN_H_ */

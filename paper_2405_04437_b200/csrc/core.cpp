@@ -1,0 +1,1313 @@
+// vAttention allocator core: policy state machine, driver bookkeeping shadow, real CUDA VMM
+// backend and the background mapping thread, exported through the C ABI in include/vattn.h.
+//
+// The policy is the reference KVCacheManager (/root/reference/pkg/src/kvsim/manager.py) and
+// its mock driver VmmDevice (vmm.py); each method below cites the lines it reproduces.  The
+// shadow (counters, handle ids, per-API call counts, modelled Table-2 µs) is always kept, so
+// the reference's state is reproducible bit for bit; with VATTN_BACKEND_CUDA every shadow
+// map/unmap/create/release is also issued to the real driver at 2 MiB granularity.
+
+#include <cuda.h>
+#include <cuda_runtime_api.h>
+
+#include <algorithm>
+#include <cmath>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "internal.h"
+#include "vattn.h"
+
+namespace vattn {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+// ------------------------------------------------------------------------------ driver
+static Driver g_drv;
+static bool g_drv_loaded = false;
+static std::mutex g_drv_mu;
+
+template <typename F>
+static void load_sym(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  cudaError_t e = cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q);
+  if (e != cudaSuccess || p == nullptr || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    throw Fail(VATTN_CUDA_ERROR, std::string("driver entry point unavailable: ") + name);
+  }
+  *fn = reinterpret_cast<F>(p);
+}
+
+const Driver& driver() {
+  std::lock_guard<std::mutex> lk(g_drv_mu);
+  if (!g_drv_loaded) {
+    load_sym("cuMemAddressReserve", &g_drv.MemAddressReserve);
+    load_sym("cuMemAddressFree", &g_drv.MemAddressFree);
+    load_sym("cuMemCreate", &g_drv.MemCreate);
+    load_sym("cuMemRelease", &g_drv.MemRelease);
+    load_sym("cuMemMap", &g_drv.MemMap);
+    load_sym("cuMemUnmap", &g_drv.MemUnmap);
+    load_sym("cuMemSetAccess", &g_drv.MemSetAccess);
+    load_sym("cuMemGetAllocationGranularity", &g_drv.MemGetAllocationGranularity);
+    load_sym("cuCtxGetCurrent", &g_drv.CtxGetCurrent);
+    load_sym("cuCtxSetCurrent", &g_drv.CtxSetCurrent);
+    load_sym("cuDevicePrimaryCtxRetain", &g_drv.DevicePrimaryCtxRetain);
+    load_sym("cuDeviceGet", &g_drv.DeviceGet);
+    load_sym("cuGetErrorString", &g_drv.GetErrorString);
+    load_sym("cuTensorMapEncodeTiled", &g_drv.TensorMapEncodeTiled);
+    g_drv_loaded = true;
+  }
+  return g_drv;
+}
+
+void check_cu(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = "?";
+  if (g_drv_loaded && g_drv.GetErrorString) g_drv.GetErrorString(r, &s);
+  throw Fail(VATTN_CUDA_ERROR, std::string(what) + ": CUresult " + std::to_string(int(r)) + " " + s);
+}
+
+void check_rt(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  throw Fail(VATTN_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static double now_us() {
+  using namespace std::chrono;
+  return duration<double, std::micro>(steady_clock::now().time_since_epoch()).count();
+}
+
+// CPython >= 3.12 `sum()` of floats (Neumaier compensated summation).  The reference totals
+// its ledger with sum() (vmm.py:191-195, :301-302), so the modelled µs are reproduced bit for
+// bit only with the same algorithm.
+struct PySum {
+  double s = 0.0, c = 0.0;
+  void add(double x) {
+    const double t = s + x;
+    if (std::fabs(s) >= std::fabs(x)) c += (s - t) + x;
+    else c += (x - t) + s;
+    s = t;
+  }
+  double value() const { return (c != 0.0 && std::isfinite(c)) ? s + c : s; }
+};
+
+// ------------------------------------------------------------------------------ latency model
+// Table 2 of the paper as encoded in vmm.py:55-68.
+enum Api {
+  A_vMemReserve, A_cuMemAddressReserve, A_vMemCreate, A_cuMemCreate, A_vMemMap, A_cuMemMap,
+  A_cuMemSetAccess, A_cuMemUnmap, A_vMemRelease, A_cuMemRelease, A_vMemFree, A_cuMemAddressFree,
+  A_COUNT
+};
+static const char* kApiNames[A_COUNT] = {
+    "vMemReserve", "cuMemAddressReserve", "vMemCreate", "cuMemCreate", "vMemMap", "cuMemMap",
+    "cuMemSetAccess", "cuMemUnmap", "vMemRelease", "cuMemRelease", "vMemFree",
+    "cuMemAddressFree"};
+
+struct LatencyTable {
+  std::vector<std::pair<int64_t, double>> rows[A_COUNT];
+  void set(int api, int64_t size, double us) {
+    for (auto& r : rows[api])
+      if (r.first == size) { r.second = us; return; }
+    rows[api].push_back({size, us});
+  }
+  double get(int api, int64_t size) const {
+    for (auto& r : rows[api])
+      if (r.first == size) return r.second;
+    throw Fail(VATTN_LATENCY_CONFIG, std::string("no latency configured for (") + kApiNames[api] +
+                                         ", " + std::to_string(size) + ")");
+  }
+  static LatencyTable table2() {
+    LatencyTable t;
+    const int64_t K64 = 65536, K128 = 131072, K256 = 262144, M2 = 2097152;
+    t.set(A_vMemReserve, K64, 18); t.set(A_vMemReserve, K128, 17); t.set(A_vMemReserve, K256, 16);
+    t.set(A_cuMemAddressReserve, M2, 2);
+    t.set(A_vMemCreate, K64, 1.7); t.set(A_vMemCreate, K128, 2); t.set(A_vMemCreate, K256, 2.1);
+    t.set(A_cuMemCreate, M2, 29);
+    t.set(A_vMemMap, K64, 8); t.set(A_vMemMap, K128, 8.5); t.set(A_vMemMap, K256, 9);
+    t.set(A_cuMemMap, M2, 2);
+    t.set(A_cuMemSetAccess, M2, 38);
+    t.set(A_cuMemUnmap, M2, 34);
+    t.set(A_vMemRelease, K64, 2); t.set(A_vMemRelease, K128, 3); t.set(A_vMemRelease, K256, 4);
+    t.set(A_cuMemRelease, M2, 23);
+    t.set(A_vMemFree, K64, 35); t.set(A_vMemFree, K128, 35); t.set(A_vMemFree, K256, 35);
+    t.set(A_cuMemAddressFree, M2, 1);
+    return t;
+  }
+};
+
+static int api_index(const char* name) {
+  for (int i = 0; i < A_COUNT; ++i)
+    if (std::strcmp(name, kApiNames[i]) == 0) return i;
+  return -1;
+}
+
+// ------------------------------------------------------------------------------ manager
+enum Phase : int64_t { INACTIVE = 0, PREFILL = 1, DECODE = 2 };
+
+struct Slot {  // manager.py:66-75
+  bool active = false;
+  int64_t context_len = 0;
+  int64_t mapped_groups = 0;
+  Phase phase = INACTIVE;
+  int64_t freed_seq = 0;
+};
+
+struct Handle {  // vmm.py:130-138 plus the real driver handle
+  bool mapped = false;
+  int32_t buf = -1;
+  int64_t off = -1;
+  CUmemGenericAllocationHandle real = 0;
+};
+
+struct BgJob {
+  std::vector<int64_t> plan;
+  uint32_t flags = 0;
+  int64_t eager_k = -1;
+};
+
+class Manager {
+ public:
+  explicit Manager(const vattn_config& c);
+  ~Manager();
+
+  // Table 3 + §6.1 API (all called from the control thread; they join the bg window first)
+  int32_t alloc_reqid();
+  void free_reqid(int32_t rid);
+  bool step(const int64_t* seq, int32_t n, double* sync_us);
+  int64_t plan_overlap(const int64_t* next, int32_t n);
+  double execute_plan(const int64_t* trip, int64_t n);
+  double eager_prepare(int64_t k);
+  std::pair<int64_t, double> reclaim();
+  std::pair<int64_t, double> reclaim_until(int64_t target);
+
+  // background thread
+  void bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t eager_k);
+  void bg_wait(vattn_bg_result* out);
+  double join_bg();
+
+  void mark_use(cudaStream_t st);
+  void begin_call() { fenced_ = false; }
+  void end_call() { flush_access(); }
+
+  // introspection
+  void counters(vattn_counters* o) const;
+  void slot_state(int64_t* out) const;
+  void api_stats(int64_t* calls, double* ledger, int32_t* order, int32_t* n_order) const;
+  int64_t buffer_mappings(int32_t b, int64_t* offs, int64_t* hids, int64_t cap) const;
+  int64_t drain_events(int64_t* out, int64_t cap);
+  uint64_t buffer_base(int32_t b) const;
+  const std::vector<int64_t>& last_plan() const { return last_plan_; }
+  CacheView layer_view(int32_t layer) const;
+  bool real() const { return backend_ == VATTN_BACKEND_CUDA; }
+  int64_t max_batch() const { return (int64_t)slots_.size(); }
+  int32_t hq_local() const { return hq_local_; }
+
+  KernelState* ks = nullptr;
+
+ private:
+  // ---- shadow driver (vmm.py:150-302) ----
+  double bill(const std::vector<int>& apis, int64_t count = 1);
+  double unit_cost(const std::vector<int>& apis) const;
+  int64_t available() const { return capacity_ - mapped_ * t_; }   // vmm.py:124-127
+  int64_t free_bytes() const { return capacity_ - created_ * t_; }   // vmm.py:118-121
+  int64_t new_handle_id();
+  int64_t dev_create();                      // vmm.py:213-225
+  double dev_precreate(int64_t count);       // vmm.py:227-239
+  int64_t dev_take_precreated();             // vmm.py:245-253
+  double dev_map(int32_t b, int64_t off, int64_t hid);   // vmm.py:255-283
+  double dev_unmap_release(int32_t b, int64_t off);       // vmm.py:285-297
+  double charged_total() const;
+
+  // ---- real driver ----
+  CUmemGenericAllocationHandle real_create();
+  void real_release(CUmemGenericAllocationHandle hnd);
+  void real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle hnd);
+  void real_unmap(int32_t b, int64_t off);
+  void flush_access();
+  void fence_unmap();
+
+  // ---- policy (manager.py) ----
+  int64_t groups_required(int64_t seq) const;
+  int64_t slot_offset(int64_t rid, int64_t g) const { return rid * slot_stride_ + g * t_; }
+  int64_t reclaim_floor() const { return (int64_t)(reclaim_threshold_ * (double)pool_bytes_); }
+  int32_t best_inactive() const;
+  std::pair<int64_t, double> acquire_handle();
+  double map_group(int64_t rid, int64_t g);
+  double release_top_group(int64_t rid);
+  std::vector<int32_t> reclaim_victims() const;
+  void bg_loop();
+
+  // config / geometry
+  int32_t backend_;
+  int64_t t_, pool_bytes_, capacity_;
+  double reclaim_threshold_;
+  int64_t eager_groups_;
+  bool sliced_;
+  int64_t max_context_;
+  int32_t n_layers_, hkv_local_, hq_local_, head_dim_, elem_bytes_;
+  int64_t buffer_count_, per_buffer_token_bytes_, groups_per_slot_, slot_stride_, buffer_size_;
+  bool release_physical_, log_events_, batch_access_;
+  LatencyTable lat_;
+  std::vector<int> api_reserve_, api_create_, api_map_, api_release_;
+
+  // shadow state
+  int64_t created_ = 0, mapped_ = 0, precreated_ = 0, total_mapped_bytes_ = 0, next_hid_ = 0;
+  std::vector<std::unordered_map<int64_t, int64_t>> buf_maps_;
+  std::unordered_map<int64_t, Handle> handles_;
+  int64_t calls_[A_COUNT] = {};
+  double ledger_[A_COUNT] = {};
+  bool ledger_seen_[A_COUNT] = {};
+  std::vector<int32_t> ledger_order_;
+  std::vector<int64_t> events_;
+  std::vector<Slot> slots_;
+  int64_t eager_slot_ = -1;
+  int64_t freed_counter_ = 0;
+  std::deque<int64_t> handle_cache_;  // manager.py:130 rollback leftovers
+  std::vector<int64_t> last_plan_;
+
+  double init_us_ = 0.0, init_wall_us_ = 0.0;
+
+  // real backend state
+  CUdevice cu_dev_ = 0;
+  CUcontext ctx_ = nullptr;
+  std::vector<CUdeviceptr> va_;
+  std::vector<CUmemGenericAllocationHandle> real_precreated_, real_recycle_;
+  CUmemAllocationProp prop_{};
+  CUmemAccessDesc access_{};
+  std::vector<int64_t> run_begin_, run_end_;  // pending cuMemSetAccess page runs per buffer
+  cudaEvent_t use_event_ = nullptr;
+  bool use_recorded_ = false;
+  bool fenced_ = false;
+  // measured real-driver statistics
+  int64_t real_maps_ = 0, real_unmaps_ = 0, real_access_ = 0, real_creates_ = 0,
+          real_releases_ = 0;
+  double real_map_us_ = 0, real_unmap_us_ = 0, real_create_us_ = 0, real_access_us_ = 0;
+
+  // background thread
+  std::thread bg_thread_;
+  std::mutex bg_mu_;
+  std::condition_variable bg_cv_;
+  bool bg_has_job_ = false, bg_busy_ = false, bg_stop_ = false, bg_result_pending_ = false;
+  BgJob bg_job_;
+  vattn_bg_result bg_res_{};
+  vattn_status bg_status_ = VATTN_OK;
+  std::string bg_error_;
+};
+
+// ---- construction (manager.py:85-130) --------------------------------------------------
+Manager::Manager(const vattn_config& c) {
+  if (c.reclaim_threshold < 0.0 || c.reclaim_threshold > 1.0)
+    throw Fail(VATTN_VALUE_ERROR, "reclaim_threshold must be in [0, 1]");
+  if (c.pre_create_fraction < 0.0 || c.pre_create_fraction > 1.0)
+    throw Fail(VATTN_VALUE_ERROR, "pre_create_fraction must be in [0, 1]");
+  if (c.eager_groups < 0) throw Fail(VATTN_VALUE_ERROR, "eager_groups must be >= 0");
+  if (c.n_layers < 1 || c.kv_heads_total < 1 || c.head_dim < 1 || c.bytes_per_elem < 1 ||
+      c.tp_degree < 1)
+    throw Fail(VATTN_VALUE_ERROR, "geometry fields must be >= 1");
+  if (c.kv_heads_total % c.tp_degree != 0)
+    throw Fail(VATTN_VALUE_ERROR, "kv_heads_total must be divisible by tp_degree");
+  if (c.max_context < 0) throw Fail(VATTN_VALUE_ERROR, "max_context must be >= 0");
+  if (c.max_batch < 1) throw Fail(VATTN_VALUE_ERROR, "geometry.max_batch must be >= 1 to serve requests");
+  if (c.page_group_size < 1) throw Fail(VATTN_VALUE_ERROR, "page_group_size must be >= 1");
+  if (c.pool_bytes < 0) throw Fail(VATTN_VALUE_ERROR, "capacity must be >= 0");
+
+  backend_ = c.backend;
+  t_ = c.page_group_size;
+  pool_bytes_ = capacity_ = c.pool_bytes;
+  reclaim_threshold_ = c.reclaim_threshold;
+  eager_groups_ = c.eager_groups;
+  sliced_ = c.sliced != 0;
+  max_context_ = c.max_context;
+  n_layers_ = c.n_layers;
+  hkv_local_ = c.kv_heads_total / c.tp_degree;
+  int32_t hq_total = c.n_q_heads_total > 0 ? c.n_q_heads_total : c.kv_heads_total;
+  if (hq_total % c.tp_degree != 0 || hq_total % c.kv_heads_total != 0)
+    throw Fail(VATTN_VALUE_ERROR, "n_q_heads_total must be a multiple of kv_heads_total and tp");
+  hq_local_ = hq_total / c.tp_degree;
+  head_dim_ = c.head_dim;
+  elem_bytes_ = c.bytes_per_elem;
+  release_physical_ = c.release_physical != 0;
+  log_events_ = c.log_events != 0;
+  batch_access_ = c.batch_set_access != 0;
+
+  lat_ = LatencyTable::table2();
+  if (c.latency && c.n_latency > 0) {
+    lat_ = LatencyTable{};
+    for (int i = 0; i < c.n_latency; ++i) {
+      int a = api_index(c.latency[i].api);
+      if (a < 0) continue;  // unknown names are kept out of the model, as LatencyModel does
+      if (c.latency[i].us < 0) throw Fail(VATTN_VALUE_ERROR, "negative latency");
+      lat_.set(a, c.latency[i].page_group_bytes, c.latency[i].us);
+    }
+  }
+  const bool large = t_ == 2097152;  // vmm.py:178-182
+  api_reserve_ = {large ? A_cuMemAddressReserve : A_vMemReserve};
+  api_create_ = {large ? A_cuMemCreate : A_vMemCreate};
+  if (large) api_map_ = {A_cuMemMap, A_cuMemSetAccess}; else api_map_ = {A_vMemMap};
+  if (large) api_release_ = {A_cuMemUnmap, A_cuMemRelease}; else api_release_ = {A_vMemRelease};
+
+  const int64_t token_layer_bytes = (int64_t)hkv_local_ * head_dim_ * elem_bytes_;
+  if (sliced_) {  // manager.py:93-99
+    buffer_count_ = 2;
+    per_buffer_token_bytes_ = (int64_t)n_layers_ * token_layer_bytes;
+  } else {
+    buffer_count_ = 2 * (int64_t)n_layers_;
+    per_buffer_token_bytes_ = token_layer_bytes;
+  }
+  if (t_ < per_buffer_token_bytes_)
+    throw Fail(VATTN_VALUE_ERROR, "page-group size smaller than one token's cache in this layout");
+  if (pool_bytes_ < buffer_count_ * t_)
+    throw Fail(VATTN_VALUE_ERROR, "pool cannot back one page-group in each buffer");
+  groups_per_slot_ = (max_context_ * per_buffer_token_bytes_ + t_ - 1) / t_;  // :111-115
+  slot_stride_ = groups_per_slot_ * t_;
+  buffer_size_ = c.max_batch * slot_stride_;
+
+  const double t0 = now_us();
+  if (real()) {
+    if (t_ != 2097152)
+      throw Fail(VATTN_UNSUPPORTED, "the stock-driver backend maps 2 MiB page-groups only");
+    const Driver& d = driver();
+    check_rt(cudaSetDevice(c.device), "cudaSetDevice");
+    check_rt(cudaFree(nullptr), "cudaFree(0) context init");
+    check_cu(d.DeviceGet(&cu_dev_, c.device), "cuDeviceGet");
+    check_cu(d.CtxGetCurrent(&ctx_), "cuCtxGetCurrent");
+    if (!ctx_) {
+      check_cu(d.DevicePrimaryCtxRetain(&ctx_, cu_dev_), "cuDevicePrimaryCtxRetain");
+      check_cu(d.CtxSetCurrent(ctx_), "cuCtxSetCurrent");
+    }
+    prop_.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop_.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop_.location.id = c.device;
+    size_t gran = 0;
+    check_cu(d.MemGetAllocationGranularity(&gran, &prop_, CU_MEM_ALLOC_GRANULARITY_MINIMUM),
+             "cuMemGetAllocationGranularity");
+    if ((int64_t)gran > t_ || t_ % (int64_t)gran != 0)
+      throw Fail(VATTN_UNSUPPORTED, "page-group size is not a multiple of the driver granularity");
+    access_.location = prop_.location;
+    access_.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    check_rt(cudaEventCreateWithFlags(&use_event_, cudaEventDisableTiming), "cudaEventCreate");
+  }
+
+  buf_maps_.resize(buffer_count_);
+  run_begin_.assign(buffer_count_, -1);
+  run_end_.assign(buffer_count_, -1);
+  for (int64_t i = 0; i < buffer_count_; ++i) {  // :119-122 — reserve(max_batch * slot_stride)
+    if (buffer_size_ % t_ != 0) throw Fail(VATTN_ALIGNMENT_ERROR, "buffer size misaligned");
+    if (real()) {
+      CUdeviceptr p = 0;
+      check_cu(driver().MemAddressReserve(&p, (size_t)buffer_size_, (size_t)t_, 0, 0),
+               "cuMemAddressReserve");
+      va_.push_back(p);
+    }
+    bill(api_reserve_);
+  }
+  init_us_ = 0.0;
+  init_us_ += charged_total();
+  const int64_t pre = (int64_t)(c.pre_create_fraction * (double)c.pool_bytes) / t_;  // :124-125
+  init_us_ += dev_precreate(pre);
+  slots_.resize(c.max_batch);
+  init_wall_us_ = now_us() - t0;
+
+  bg_thread_ = std::thread([this] { bg_loop(); });
+}
+
+Manager::~Manager() {
+  {
+    std::unique_lock<std::mutex> lk(bg_mu_);
+    bg_cv_.wait(lk, [&] { return !bg_busy_; });
+    bg_stop_ = true;
+  }
+  bg_cv_.notify_all();
+  if (bg_thread_.joinable()) bg_thread_.join();
+  if (!real()) return;
+  const Driver& d = driver();
+  d.CtxSetCurrent(ctx_);
+  cudaDeviceSynchronize();
+  for (int32_t b = 0; b < (int32_t)buf_maps_.size(); ++b)
+    for (auto& kv : buf_maps_[b]) d.MemUnmap(va_[b] + kv.first, (size_t)t_);
+  for (auto& kv : handles_)
+    if (kv.second.real) d.MemRelease(kv.second.real);
+  for (auto h : real_precreated_) d.MemRelease(h);
+  for (auto h : real_recycle_) d.MemRelease(h);
+  for (size_t b = 0; b < va_.size(); ++b) d.MemAddressFree(va_[b], (size_t)buffer_size_);
+  if (use_event_) cudaEventDestroy(use_event_);
+}
+
+// ---- shadow driver ------------------------------------------------------------------------
+// vmm.py:186-195: each API charged count times; a composite charge sums from integer 0.
+double Manager::bill(const std::vector<int>& apis, int64_t count) {
+  PySum total;
+  for (int a : apis) {
+    const double us = lat_.get(a, t_) * (double)count;
+    if (!ledger_seen_[a]) { ledger_seen_[a] = true; ledger_order_.push_back(a); }
+    ledger_[a] = ledger_[a] + us;
+    calls_[a] += count;
+    total.add(us);
+  }
+  return total.value();
+}
+
+double Manager::unit_cost(const std::vector<int>& apis) const {  // manager.py:201-203
+  PySum total;
+  for (int a : apis) total.add(lat_.get(a, t_));
+  return total.value();
+}
+
+double Manager::charged_total() const {  // vmm.py:301-302 sum(ledger_us.values())
+  PySum s;
+  for (int32_t a : ledger_order_) s.add(ledger_[a]);
+  return s.value();
+}
+
+int64_t Manager::new_handle_id() {
+  const int64_t id = next_hid_++;
+  handles_.emplace(id, Handle{});
+  return id;
+}
+
+int64_t Manager::dev_create() {
+  if (free_bytes() < t_) throw Fail(VATTN_POOL_EXHAUSTED, "pool exhausted");
+  CUmemGenericAllocationHandle r = real() ? real_create() : 0;
+  const int64_t id = new_handle_id();
+  handles_[id].real = r;
+  created_ += 1;
+  bill(api_create_);
+  return id;
+}
+
+double Manager::dev_precreate(int64_t count) {
+  if (count < 0) throw Fail(VATTN_VALUE_ERROR, "count must be >= 0");
+  if (free_bytes() < count * t_) throw Fail(VATTN_POOL_EXHAUSTED, "cannot pre-create page-groups");
+  if (real()) {
+    real_precreated_.reserve((size_t)count);
+    for (int64_t i = 0; i < count; ++i) {
+      CUmemGenericAllocationHandle h = 0;
+      const double t0 = now_us();
+      check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
+      real_create_us_ += now_us() - t0;
+      real_creates_ += 1;
+      real_precreated_.push_back(h);
+    }
+  }
+  created_ += count;
+  precreated_ += count;
+  return count ? bill(api_create_, count) : 0.0;
+}
+
+int64_t Manager::dev_take_precreated() {
+  if (precreated_ < 1) throw Fail(VATTN_POOL_EXHAUSTED, "no pre-created handles available");
+  precreated_ -= 1;
+  const int64_t id = new_handle_id();
+  if (real()) {
+    handles_[id].real = real_precreated_.back();
+    real_precreated_.pop_back();
+  }
+  return id;
+}
+
+double Manager::dev_map(int32_t b, int64_t off, int64_t hid) {
+  auto it = handles_.find(hid);
+  if (it == handles_.end()) throw Fail(VATTN_MAPPING_ERROR, "handle released");
+  Handle& h = it->second;
+  if (h.mapped) throw Fail(VATTN_MAPPING_ERROR, "handle already mapped");
+  if (off % t_ != 0) throw Fail(VATTN_ALIGNMENT_ERROR, "offset not aligned");
+  if (off < 0 || off + t_ > buffer_size_) throw Fail(VATTN_MAPPING_ERROR, "offset out of range");
+  if (buf_maps_[b].count(off)) throw Fail(VATTN_MAPPING_ERROR, "offset already backed");
+  if (real()) real_map(b, off, h.real);
+  h.mapped = true;
+  h.buf = b;
+  h.off = off;
+  buf_maps_[b][off] = hid;
+  mapped_ += 1;
+  total_mapped_bytes_ += t_;
+  if (log_events_) { events_.push_back(0); events_.push_back(b); events_.push_back(off); }
+  return bill(api_map_);
+}
+
+double Manager::dev_unmap_release(int32_t b, int64_t off) {
+  auto it = buf_maps_[b].find(off);
+  if (it == buf_maps_[b].end()) throw Fail(VATTN_INVALID_FREE, "no mapping at offset");
+  const int64_t hid = it->second;
+  Handle h = handles_[hid];
+  if (real()) {
+    real_unmap(b, off);
+    real_release(h.real);
+  }
+  buf_maps_[b].erase(it);
+  handles_.erase(hid);
+  mapped_ -= 1;
+  created_ -= 1;  // capacity returns to the pool, not the pre-created reserve (vmm.py:295-296)
+  if (log_events_) { events_.push_back(1); events_.push_back(b); events_.push_back(off); }
+  return bill(api_release_);
+}
+
+// ---- real driver ----------------------------------------------------------------------------
+CUmemGenericAllocationHandle Manager::real_create() {
+  if (!real_recycle_.empty()) {  // a 2 MiB handle whose shadow was released earlier
+    auto h = real_recycle_.back();
+    real_recycle_.pop_back();
+    return h;
+  }
+  CUmemGenericAllocationHandle h = 0;
+  const double t0 = now_us();
+  check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
+  real_create_us_ += now_us() - t0;
+  real_creates_ += 1;
+  return h;
+}
+
+void Manager::real_release(CUmemGenericAllocationHandle h) {
+  if (!release_physical_) { real_recycle_.push_back(h); return; }
+  check_cu(driver().MemRelease(h), "cuMemRelease");
+  real_releases_ += 1;
+}
+
+void Manager::real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle h) {
+  const Driver& d = driver();
+  const double t0 = now_us();
+  check_cu(d.MemMap(va_[b] + off, (size_t)t_, 0, h, 0), "cuMemMap");
+  real_map_us_ += now_us() - t0;
+  real_maps_ += 1;
+  if (!batch_access_) {
+    const double t1 = now_us();
+    check_cu(d.MemSetAccess(va_[b] + off, (size_t)t_, &access_, 1), "cuMemSetAccess");
+    real_access_us_ += now_us() - t1;
+    real_access_ += 1;
+    return;
+  }
+  // coalesce contiguous pages of the same buffer into one cuMemSetAccess call
+  if (run_begin_[b] >= 0 && run_end_[b] == off) { run_end_[b] = off + t_; return; }
+  if (run_begin_[b] >= 0) {
+    const double t1 = now_us();
+    check_cu(d.MemSetAccess(va_[b] + run_begin_[b], (size_t)(run_end_[b] - run_begin_[b]), &access_, 1),
+             "cuMemSetAccess");
+    real_access_us_ += now_us() - t1;
+    real_access_ += 1;
+  }
+  run_begin_[b] = off;
+  run_end_[b] = off + t_;
+}
+
+void Manager::flush_access() {
+  if (!real() || !batch_access_) return;
+  const Driver& d = driver();
+  for (size_t b = 0; b < run_begin_.size(); ++b) {
+    if (run_begin_[b] < 0) continue;
+    const double t1 = now_us();
+    check_cu(d.MemSetAccess(va_[b] + run_begin_[b], (size_t)(run_end_[b] - run_begin_[b]), &access_, 1),
+             "cuMemSetAccess");
+    real_access_us_ += now_us() - t1;
+    real_access_ += 1;
+    run_begin_[b] = run_end_[b] = -1;
+  }
+}
+
+void Manager::fence_unmap() {
+  // Never unmap a page that queued kernels may still read (SURVEY §7 hard part 3).
+  if (fenced_) return;
+  flush_access();
+  if (use_recorded_) check_rt(cudaEventSynchronize(use_event_), "cudaEventSynchronize(unmap fence)");
+  fenced_ = true;
+}
+
+void Manager::real_unmap(int32_t b, int64_t off) {
+  fence_unmap();
+  const double t0 = now_us();
+  check_cu(driver().MemUnmap(va_[b] + off, (size_t)t_), "cuMemUnmap");
+  real_unmap_us_ += now_us() - t0;
+  real_unmaps_ += 1;
+}
+
+void Manager::mark_use(cudaStream_t st) {
+  if (!real()) return;
+  check_rt(cudaEventRecord(use_event_, st), "cudaEventRecord(use)");
+  use_recorded_ = true;
+}
+
+// ---- policy ------------------------------------------------------------------------------------
+int64_t Manager::groups_required(int64_t seq) const {  // manager.py:134-135, geometry.py:177-183
+  return (seq * per_buffer_token_bytes_ + t_ - 1) / t_;
+}
+
+int32_t Manager::best_inactive() const {  // max over inactive of (mapped_groups, -req_id)
+  int32_t best = -1;
+  for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+    if (slots_[r].active) continue;
+    if (best < 0 || slots_[r].mapped_groups > slots_[best].mapped_groups) best = r;
+  }
+  return best;
+}
+
+int32_t Manager::alloc_reqid() {  // manager.py:163-178
+  int32_t rid;
+  if (eager_slot_ >= 0 && !slots_[eager_slot_].active) {
+    rid = (int32_t)eager_slot_;
+    eager_slot_ = -1;
+  } else {
+    rid = best_inactive();
+    if (rid < 0)
+      throw Fail(VATTN_BATCH_FULL, "all " + std::to_string(slots_.size()) + " request slots active");
+  }
+  Slot& s = slots_[rid];
+  s.active = true;
+  s.context_len = 0;
+  s.phase = PREFILL;
+  return rid;
+}
+
+void Manager::free_reqid(int32_t rid) {  // manager.py:180-190 — no driver calls
+  if (rid < 0 || rid >= (int32_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "req_id out of range");
+  Slot& s = slots_[rid];
+  if (!s.active) throw Fail(VATTN_DOUBLE_FREE, "slot " + std::to_string(rid) + " is not active");
+  s.active = false;
+  s.context_len = 0;
+  s.phase = INACTIVE;
+  freed_counter_ += 1;
+  s.freed_seq = freed_counter_;
+}
+
+std::pair<int64_t, double> Manager::acquire_handle() {  // manager.py:194-204
+  if (!handle_cache_.empty()) {
+    const int64_t h = handle_cache_.front();
+    handle_cache_.pop_front();
+    return {h, 0.0};
+  }
+  if (precreated_ > 0) return {dev_take_precreated(), 0.0};
+  const int64_t h = dev_create();
+  return {h, unit_cost(api_create_)};
+}
+
+double Manager::map_group(int64_t rid, int64_t g) {  // manager.py:206-220, all-or-nothing
+  std::vector<int64_t> got;
+  got.reserve((size_t)buffer_count_);
+  double us = 0.0;
+  try {
+    for (int64_t i = 0; i < buffer_count_; ++i) {
+      auto hc = acquire_handle();
+      got.push_back(hc.first);
+      us += hc.second;
+    }
+  } catch (const Fail& f) {
+    if (f.code != VATTN_POOL_EXHAUSTED) throw;
+    for (int64_t h : got) handle_cache_.push_back(h);
+    throw;
+  }
+  const int64_t off = slot_offset(rid, g);
+  for (int64_t b = 0; b < buffer_count_; ++b) us += dev_map((int32_t)b, off, got[b]);
+  return us;
+}
+
+double Manager::release_top_group(int64_t rid) {  // manager.py:222-230
+  Slot& s = slots_[rid];
+  const int64_t g = s.mapped_groups - 1;
+  const int64_t off = slot_offset(rid, g);
+  double us = 0.0;
+  for (int64_t b = 0; b < buffer_count_; ++b) us += dev_unmap_release((int32_t)b, off);
+  s.mapped_groups = g;
+  return us;
+}
+
+std::vector<int32_t> Manager::reclaim_victims() const {  // manager.py:232-236
+  std::vector<int32_t> v;
+  for (int32_t r = 0; r < (int32_t)slots_.size(); ++r)
+    if (!slots_[r].active && slots_[r].mapped_groups > 0) v.push_back(r);
+  std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) {
+    const bool ea = a == eager_slot_, eb = b == eager_slot_;
+    if (ea != eb) return !ea;  // eager slot harvested last
+    if (slots_[a].freed_seq != slots_[b].freed_seq) return slots_[a].freed_seq < slots_[b].freed_seq;
+    return a < b;
+  });
+  return v;
+}
+
+std::pair<int64_t, double> Manager::reclaim_until(int64_t target) {  // manager.py:238-251
+  int64_t freed = 0;
+  double us = 0.0;
+  for (int32_t r : reclaim_victims()) {
+    Slot& s = slots_[r];
+    while (s.mapped_groups > 0 && available() < target) {
+      us += release_top_group(r);
+      freed += 1;
+    }
+    if (s.mapped_groups == 0 && eager_slot_ == r) eager_slot_ = -1;
+    if (available() >= target) break;
+  }
+  return {freed, us};
+}
+
+bool Manager::step(const int64_t* seq, int32_t n, double* sync_out) {  // manager.py:255-296
+  if (n != (int32_t)slots_.size())
+    throw Fail(VATTN_VALUE_ERROR, "expected " + std::to_string(slots_.size()) + " sequence lengths, got " +
+                                      std::to_string(n));
+  for (int32_t r = 0; r < n; ++r) {
+    if (!slots_[r].active && seq[r] != 0)
+      throw Fail(VATTN_VALUE_ERROR, "inactive slot " + std::to_string(r) + " has nonzero length");
+    if (seq[r] < 0 || seq[r] > max_context_)
+      throw Fail(VATTN_VALUE_ERROR, "slot " + std::to_string(r) + " length outside [0, max_context]");
+  }
+  double sync_us = 0.0;
+  for (int32_t r = 0; r < n; ++r) {
+    Slot& s = slots_[r];
+    if (!s.active) continue;
+    const int64_t required = groups_required(seq[r]);
+    if (s.phase == PREFILL)
+      while (s.mapped_groups > required) sync_us += release_top_group(r);
+    while (s.mapped_groups < required) {
+      try {
+        sync_us += map_group(r, s.mapped_groups);
+      } catch (const Fail& f) {
+        if (f.code != VATTN_POOL_EXHAUSTED) throw;
+        auto fr = reclaim_until(buffer_count_ * t_);
+        sync_us += fr.second;
+        if (fr.first == 0) { *sync_out = sync_us; return false; }
+        continue;
+      }
+      s.mapped_groups += 1;
+    }
+    s.context_len = seq[r];
+    s.phase = DECODE;
+  }
+  *sync_out = sync_us;
+  return true;
+}
+
+int64_t Manager::plan_overlap(const int64_t* next, int32_t n) {  // manager.py:298-311
+  if (n != (int32_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "plan length mismatch");
+  last_plan_.clear();
+  for (int32_t r = 0; r < n; ++r) {
+    const Slot& s = slots_[r];
+    if (!s.active) continue;
+    if (next[r] < 0) throw Fail(VATTN_VALUE_ERROR, "negative length");
+    const int64_t req = std::min(groups_required(next[r]), groups_per_slot_);
+    for (int64_t g = s.mapped_groups; g < req; ++g)
+      for (int64_t b = 0; b < buffer_count_; ++b) {
+        last_plan_.push_back(r);
+        last_plan_.push_back(b);
+        last_plan_.push_back(slot_offset(r, g));
+      }
+  }
+  return (int64_t)last_plan_.size() / 3;
+}
+
+double Manager::execute_plan(const int64_t* trip, int64_t n) {  // manager.py:313-333
+  double us = 0.0;
+  std::unordered_set<int64_t> done;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t rid = trip[3 * i], off = trip[3 * i + 2];
+    if (rid < 0 || rid >= (int64_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "plan req_id out of range");
+    Slot& s = slots_[rid];
+    const int64_t rel = off - rid * slot_stride_;
+    // Python floor division
+    const int64_t g = rel >= 0 ? rel / t_ : -((-rel + t_ - 1) / t_);
+    const int64_t key = rid * (groups_per_slot_ + 1) + g;
+    if ((g >= 0 && done.count(key)) || g < s.mapped_groups) continue;
+    if (g >= groups_per_slot_) continue;
+    while (s.mapped_groups <= g) {  // grow strictly in order; the mapped prefix stays contiguous
+      try {
+        us += map_group(rid, s.mapped_groups);
+      } catch (const Fail& f) {
+        if (f.code != VATTN_POOL_EXHAUSTED) throw;
+        return us;
+      }
+      s.mapped_groups += 1;
+    }
+    done.insert(key);
+  }
+  return us;
+}
+
+double Manager::eager_prepare(int64_t k) {  // manager.py:335-361
+  if (k < 0) k = eager_groups_;
+  if (k <= 0) return 0.0;
+  k = std::min(k, groups_per_slot_);
+  if (eager_slot_ >= 0 && slots_[eager_slot_].mapped_groups >= k) return 0.0;
+  const int32_t rid = best_inactive();
+  if (rid < 0) return 0.0;
+  eager_slot_ = rid;
+  Slot& s = slots_[rid];
+  double us = 0.0;
+  const int64_t group_bytes = buffer_count_ * t_;
+  while (s.mapped_groups < k) {
+    if (available() - group_bytes < reclaim_floor()) break;
+    try {
+      us += map_group(rid, s.mapped_groups);
+    } catch (const Fail& f) {
+      if (f.code != VATTN_POOL_EXHAUSTED) throw;
+      break;
+    }
+    s.mapped_groups += 1;
+  }
+  return us;
+}
+
+std::pair<int64_t, double> Manager::reclaim() {  // manager.py:363-372
+  const int64_t floor = reclaim_floor();
+  if (available() >= floor) return {0, 0.0};
+  return reclaim_until(floor);
+}
+
+// ---- background thread (simulator.py:199-203 on a real thread) ----------------------------
+void Manager::bg_loop() {
+  bool ctx_set = false;
+  for (;;) {
+    BgJob job;
+    {
+      std::unique_lock<std::mutex> lk(bg_mu_);
+      bg_cv_.wait(lk, [&] { return bg_has_job_ || bg_stop_; });
+      if (bg_stop_ && !bg_has_job_) return;
+      job = std::move(bg_job_);
+      bg_has_job_ = false;
+    }
+    vattn_bg_result res{};
+    vattn_status st = VATTN_OK;
+    std::string err;
+    const double t0 = now_us();
+    try {
+      if (real() && !ctx_set) {
+        check_cu(driver().CtxSetCurrent(ctx_), "cuCtxSetCurrent(bg)");
+        ctx_set = true;
+      }
+      fenced_ = false;
+      if (job.flags & VATTN_BG_EXECUTE_PLAN)
+        res.plan_us = execute_plan(job.plan.data(), (int64_t)job.plan.size() / 3);
+      if (job.flags & VATTN_BG_EAGER) res.eager_us = eager_prepare(job.eager_k);
+      if (job.flags & VATTN_BG_RECLAIM) {
+        auto r = reclaim();
+        res.reclaimed_groups = r.first;
+        res.reclaim_us = r.second;
+      }
+      flush_access();
+    } catch (const Fail& f) {
+      st = f.code;
+      err = f.what();
+    } catch (const std::exception& e) {
+      st = VATTN_BAD_STATE;
+      err = e.what();
+    }
+    res.bg_wall_us = now_us() - t0;
+    {
+      std::lock_guard<std::mutex> lk(bg_mu_);
+      bg_res_ = res;
+      bg_status_ = st;
+      bg_error_ = err;
+      bg_busy_ = false;
+      bg_result_pending_ = true;
+    }
+    bg_cv_.notify_all();
+  }
+}
+
+double Manager::join_bg() {
+  std::unique_lock<std::mutex> lk(bg_mu_);
+  if (!bg_busy_) return 0.0;
+  const double t0 = now_us();
+  bg_cv_.wait(lk, [&] { return !bg_busy_; });
+  return now_us() - t0;
+}
+
+void Manager::bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t eager_k) {
+  join_bg();
+  std::lock_guard<std::mutex> lk(bg_mu_);
+  bg_job_ = BgJob{};
+  if (trip) bg_job_.plan.assign(trip, trip + 3 * n);
+  else bg_job_.plan = last_plan_;
+  bg_job_.flags = flags;
+  bg_job_.eager_k = eager_k;
+  bg_has_job_ = true;
+  bg_busy_ = true;
+  bg_result_pending_ = false;
+  bg_cv_.notify_all();
+}
+
+void Manager::bg_wait(vattn_bg_result* out) {
+  std::unique_lock<std::mutex> lk(bg_mu_);
+  const double t0 = now_us();
+  bg_cv_.wait(lk, [&] { return !bg_busy_; });
+  const double waited = now_us() - t0;
+  if (!bg_result_pending_) throw Fail(VATTN_BAD_STATE, "vattn_bg_wait without a submitted job");
+  bg_result_pending_ = false;
+  if (out) { *out = bg_res_; out->waited_us = waited; }
+  if (bg_status_ != VATTN_OK) throw Fail(bg_status_, "background job failed: " + bg_error_);
+}
+
+// ---- introspection ------------------------------------------------------------------------------
+void Manager::counters(vattn_counters* o) const {
+  std::memset(o, 0, sizeof(*o));
+  o->created = created_;
+  o->mapped = mapped_;
+  o->precreated = precreated_;
+  o->total_mapped_bytes = total_mapped_bytes_;
+  o->capacity = capacity_;
+  o->page_group_size = t_;
+  o->buffer_count = buffer_count_;
+  o->groups_per_slot = groups_per_slot_;
+  o->slot_stride = slot_stride_;
+  o->buffer_size = buffer_size_;
+  o->per_buffer_token_bytes = per_buffer_token_bytes_;
+  o->max_batch = (int64_t)slots_.size();
+  o->max_context = max_context_;
+  o->eager_slot = eager_slot_;
+  o->next_handle_id = next_hid_;
+  o->init_us = init_us_;
+  o->charged_us = charged_total();
+  o->real_maps = real_maps_;
+  o->real_unmaps = real_unmaps_;
+  o->real_set_access_calls = real_access_;
+  o->real_creates = real_creates_;
+  o->real_releases = real_releases_;
+  o->real_map_wall_us = real_map_us_;
+  o->real_unmap_wall_us = real_unmap_us_;
+  o->real_create_wall_us = real_create_us_;
+  o->real_set_access_wall_us = real_access_us_;
+  o->init_wall_us = init_wall_us_;
+}
+
+void Manager::slot_state(int64_t* out) const {
+  for (size_t r = 0; r < slots_.size(); ++r) {
+    out[5 * r + 0] = slots_[r].active ? 1 : 0;
+    out[5 * r + 1] = slots_[r].context_len;
+    out[5 * r + 2] = slots_[r].mapped_groups;
+    out[5 * r + 3] = (int64_t)slots_[r].phase;
+    out[5 * r + 4] = slots_[r].freed_seq;
+  }
+}
+
+void Manager::api_stats(int64_t* calls, double* ledger, int32_t* order, int32_t* n_order) const {
+  for (int a = 0; a < A_COUNT; ++a) {
+    if (calls) calls[a] = calls_[a];
+    if (ledger) ledger[a] = ledger_[a];
+  }
+  if (order)
+    for (size_t i = 0; i < ledger_order_.size(); ++i) order[i] = ledger_order_[i];
+  if (n_order) *n_order = (int32_t)ledger_order_.size();
+}
+
+int64_t Manager::buffer_mappings(int32_t b, int64_t* offs, int64_t* hids, int64_t cap) const {
+  if (b < 0 || b >= (int32_t)buf_maps_.size()) throw Fail(VATTN_VALUE_ERROR, "buffer id out of range");
+  std::vector<std::pair<int64_t, int64_t>> v(buf_maps_[b].begin(), buf_maps_[b].end());
+  std::sort(v.begin(), v.end());
+  for (int64_t i = 0; i < (int64_t)v.size() && i < cap; ++i) {
+    if (offs) offs[i] = v[i].first;
+    if (hids) hids[i] = v[i].second;
+  }
+  return (int64_t)v.size();
+}
+
+int64_t Manager::drain_events(int64_t* out, int64_t cap) {
+  const int64_t n = (int64_t)events_.size() / 3;
+  if (out == nullptr) return n;
+  const int64_t k = std::min(n, cap);
+  std::copy(events_.begin(), events_.begin() + 3 * k, out);
+  events_.erase(events_.begin(), events_.begin() + 3 * k);
+  return k;
+}
+
+uint64_t Manager::buffer_base(int32_t b) const {
+  if (b < 0 || b >= (int32_t)buffer_count_) throw Fail(VATTN_VALUE_ERROR, "buffer id out of range");
+  if (!real()) throw Fail(VATTN_BAD_STATE, "shadow backend has no device buffers");
+  return (uint64_t)va_[b];
+}
+
+CacheView Manager::layer_view(int32_t layer) const {
+  if (!real()) throw Fail(VATTN_BAD_STATE, "kernels need the CUDA backend");
+  if (layer < 0 || layer >= n_layers_) throw Fail(VATTN_VALUE_ERROR, "layer out of range");
+  if (elem_bytes_ != 2) throw Fail(VATTN_UNSUPPORTED, "kernels compute on bf16 caches");
+  CacheView v;
+  const int64_t row = (int64_t)hkv_local_ * head_dim_ * elem_bytes_;
+  if (sliced_) {  // [B, L, N, H, D]: layer l sits at l*row inside each token's N*row bytes
+    v.k_base = va_[0] + (uint64_t)layer * row;
+    v.v_base = va_[1] + (uint64_t)layer * row;
+    v.token_stride = (int64_t)n_layers_ * row;
+  } else {  // buffer id 2*layer + {0: K, 1: V}
+    v.k_base = va_[2 * layer];
+    v.v_base = va_[2 * layer + 1];
+    v.token_stride = row;
+  }
+  v.slot_stride = slot_stride_;
+  v.slot_tokens = (int32_t)max_context_;
+  v.n_slots = (int32_t)slots_.size();
+  v.hkv = hkv_local_;
+  v.d = head_dim_;
+  return v;
+}
+
+CacheView view_from_desc(const vattn_cache_desc* c) {
+  if (!c) throw Fail(VATTN_VALUE_ERROR, "null cache descriptor");
+  CacheView v;
+  v.k_base = (uint64_t)c->k_base;
+  v.v_base = (uint64_t)c->v_base;
+  v.slot_stride = c->slot_stride_bytes;
+  v.token_stride = c->token_stride_bytes ? c->token_stride_bytes : (int64_t)c->n_kv_heads * c->head_dim * 2;
+  v.slot_tokens = c->slot_tokens;
+  v.n_slots = c->n_slots;
+  v.hkv = c->n_kv_heads;
+  v.d = c->head_dim;
+  return v;
+}
+
+}  // namespace vattn
+
+// ================================================================================ C ABI
+using vattn::Fail;
+using vattn::Manager;
+
+struct vattn_t {
+  Manager* m = nullptr;
+  void* workspace = nullptr;
+  int64_t workspace_bytes = 0;
+};
+
+template <typename F>
+static vattn_status guard(F&& f) {
+  try {
+    f();
+    return VATTN_OK;
+  } catch (const Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    vattn::set_last_error("out of host memory");
+    return VATTN_BAD_STATE;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
+}
+
+template <typename F>
+static vattn_status api_call(vattn_t* h, F&& f) {
+  if (!h || !h->m) {
+    vattn::set_last_error("null handle");
+    return VATTN_BAD_STATE;
+  }
+  return guard([&] {
+    h->m->join_bg();
+    h->m->begin_call();
+    try {
+      f(*h->m);
+    } catch (...) {
+      try { h->m->end_call(); } catch (...) {}
+      throw;
+    }
+    h->m->end_call();
+  });
+}
+
+extern "C" {
+
+const char* vattn_last_error(void) { return vattn::g_last_error.c_str(); }
+int32_t vattn_abi_version(void) { return 1; }
+
+vattn_status vattn_create(const vattn_config* cfg, vattn_t** out) {
+  return guard([&] {
+    if (!cfg || !out) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    auto h = std::make_unique<vattn_t>();
+    h->m = new Manager(*cfg);
+    h->m->ks = vattn::kernel_state_new();
+    *out = h.release();
+  });
+}
+
+vattn_status vattn_destroy(vattn_t* h) {
+  if (!h) return VATTN_OK;
+  return guard([&] {
+    if (h->m) {
+      if (h->m->ks) vattn::kernel_state_free(h->m->ks);
+      delete h->m;
+    }
+    if (h->workspace) cudaFree(h->workspace);
+    delete h;
+  });
+}
+
+vattn_status vattn_alloc_reqid(vattn_t* h, int32_t* rid) {
+  return api_call(h, [&](Manager& m) { *rid = m.alloc_reqid(); });
+}
+
+vattn_status vattn_free_reqid(vattn_t* h, int32_t rid) {
+  return api_call(h, [&](Manager& m) { m.free_reqid(rid); });
+}
+
+vattn_status vattn_step(vattn_t* h, const int64_t* seq, int32_t n, vattn_step_result* out) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    const double t0 = vattn::now_us();
+    const double waited = h->m->join_bg();
+    h->m->begin_call();
+    double us = 0.0;
+    bool ok;
+    try {
+      ok = h->m->step(seq, n, &us);
+    } catch (...) {
+      try { h->m->end_call(); } catch (...) {}
+      throw;
+    }
+    h->m->end_call();
+    if (out) {
+      out->ok = ok ? 1 : 0;
+      out->sync_us = us;
+      out->bg_wait_us = waited;
+      out->wall_us = vattn::now_us() - t0;
+    }
+  });
+}
+
+vattn_status vattn_plan_overlap(vattn_t* h, const int64_t* next, int32_t n, int64_t* n_entries) {
+  return api_call(h, [&](Manager& m) {
+    const int64_t k = m.plan_overlap(next, n);
+    if (n_entries) *n_entries = k;
+  });
+}
+
+vattn_status vattn_plan_fetch(vattn_t* h, int64_t* trip, int64_t cap) {
+  return api_call(h, [&](Manager& m) {
+    const auto& p = m.last_plan();
+    const int64_t k = std::min<int64_t>(cap, (int64_t)p.size() / 3);
+    std::copy(p.begin(), p.begin() + 3 * k, trip);
+  });
+}
+
+vattn_status vattn_execute_plan(vattn_t* h, const int64_t* trip, int64_t n, double* us) {
+  return api_call(h, [&](Manager& m) {
+    const double u = m.execute_plan(trip, n);
+    if (us) *us = u;
+  });
+}
+
+vattn_status vattn_eager_prepare(vattn_t* h, int64_t k, double* us) {
+  return api_call(h, [&](Manager& m) {
+    const double u = m.eager_prepare(k);
+    if (us) *us = u;
+  });
+}
+
+vattn_status vattn_reclaim(vattn_t* h, int64_t* freed, double* us) {
+  return api_call(h, [&](Manager& m) {
+    auto r = m.reclaim();
+    if (freed) *freed = r.first;
+    if (us) *us = r.second;
+  });
+}
+
+vattn_status vattn_reclaim_until(vattn_t* h, int64_t target, int64_t* freed, double* us) {
+  return api_call(h, [&](Manager& m) {
+    auto r = m.reclaim_until(target);
+    if (freed) *freed = r.first;
+    if (us) *us = r.second;
+  });
+}
+
+vattn_status vattn_bg_submit(vattn_t* h, const int64_t* trip, int64_t n, uint32_t flags,
+                             int64_t eager_k) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->bg_submit(trip, n, flags, eager_k); });
+}
+
+vattn_status vattn_bg_wait(vattn_t* h, vattn_bg_result* out) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->bg_wait(out); });
+}
+
+vattn_status vattn_mark_use(vattn_t* h, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->mark_use((cudaStream_t)stream); });
+}
+
+vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out) {
+  return api_call(h, [&](Manager& m) { m.counters(out); });
+}
+
+vattn_status vattn_slot_state(vattn_t* h, int64_t* out, int64_t cap) {
+  return api_call(h, [&](Manager& m) {
+    if (cap < m.max_batch()) throw Fail(VATTN_VALUE_ERROR, "slot buffer too small");
+    m.slot_state(out);
+  });
+}
+
+int32_t vattn_api_count(void) { return vattn::A_COUNT; }
+const char* vattn_api_name(int32_t i) {
+  return (i >= 0 && i < vattn::A_COUNT) ? vattn::kApiNames[i] : "";
+}
+
+vattn_status vattn_api_stats(vattn_t* h, int64_t* calls, double* ledger, int32_t* order,
+                             int32_t* n_order) {
+  return api_call(h, [&](Manager& m) { m.api_stats(calls, ledger, order, n_order); });
+}
+
+vattn_status vattn_buffer_mappings(vattn_t* h, int32_t b, int64_t* offs, int64_t* hids,
+                                   int64_t cap, int64_t* n) {
+  return api_call(h, [&](Manager& m) {
+    const int64_t k = m.buffer_mappings(b, offs, hids, cap);
+    if (n) *n = k;
+  });
+}
+
+vattn_status vattn_events(vattn_t* h, int64_t* trip, int64_t cap, int64_t* n) {
+  return api_call(h, [&](Manager& m) {
+    const int64_t k = m.drain_events(trip, cap);
+    if (n) *n = k;
+  });
+}
+
+vattn_status vattn_buffer_base(vattn_t* h, int32_t b, uint64_t* dptr) {
+  return api_call(h, [&](Manager& m) { *dptr = m.buffer_base(b); });
+}
+
+// ---- handle-based kernel entry points ------------------------------------------------------
+vattn_status vattn_kv_append(vattn_t* h, int32_t layer, const void* k_new, const void* v_new,
+                             int32_t batch, int32_t n_new, const int32_t* seqlens,
+                             const int32_t* batch_idx, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    const vattn::CacheView v = h->m->layer_view(layer);
+    vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
+                            (cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
+vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, int32_t batch,
+                          const int32_t* seqlens, const int32_t* batch_idx, float scale,
+                          int32_t num_splits, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    const vattn::CacheView v = h->m->layer_view(layer);
+    const int hq = h->m->hq_local();
+    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
+    if (need > h->workspace_bytes) {
+      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
+      h->workspace = nullptr;
+      h->workspace_bytes = 0;
+      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
+      h->workspace_bytes = need;
+    }
+    vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, seqlens, batch_idx, scale,
+                         num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
+vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
+                           int32_t slot, int32_t kv_len, float scale, int32_t causal,
+                           void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    const vattn::CacheView v = h->m->layer_view(layer);
+    vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
+                          causal != 0, (cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Internal interfaces shared by the allocator core (core.cpp) and the kernels (kernels.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime_api.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "vattn.h"
+
+namespace vattn {
+
+// Internal failure carrying a vattn_status; converted to a return code at the C ABI edge.
+struct Fail : std::runtime_error {
+  vattn_status code;
+  Fail(vattn_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+// Driver API resolved at runtime through cudaGetDriverEntryPoint, so libvattn.so has no link
+// dependency on libcuda (it loads on a CPU-only host for the shadow backend and ABI tests).
+struct Driver {
+  CUresult (*MemAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*MemAddressFree)(CUdeviceptr, size_t);
+  CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                        unsigned long long);
+  CUresult (*MemRelease)(CUmemGenericAllocationHandle);
+  CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle,
+                     unsigned long long);
+  CUresult (*MemUnmap)(CUdeviceptr, size_t);
+  CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*MemGetAllocationGranularity)(size_t*, const CUmemAllocationProp*,
+                                          CUmemAllocationGranularity_flags);
+  CUresult (*CtxGetCurrent)(CUcontext*);
+  CUresult (*CtxSetCurrent)(CUcontext);
+  CUresult (*DevicePrimaryCtxRetain)(CUcontext*, CUdevice);
+  CUresult (*DeviceGet)(CUdevice*, int);
+  CUresult (*GetErrorString)(CUresult, const char**);
+  CUresult (*TensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+};
+
+// Loads the entry points on first use; throws Fail(VATTN_CUDA_ERROR) when no driver exists.
+const Driver& driver();
+void check_cu(CUresult r, const char* what);
+void check_rt(cudaError_t e, const char* what);
+
+// Geometry of one layer's K and V caches as the kernels see them: token-major rows of
+// Hkv*D bf16 with an arbitrary token stride (per-layer or layer-sliced buffers) and a fixed
+// per-slot stride (slot i starts at i * slot_stride; manager.py:137-138).
+struct CacheView {
+  uint64_t k_base = 0, v_base = 0;
+  int64_t slot_stride = 0;
+  int64_t token_stride = 0;
+  int32_t slot_tokens = 0;
+  int32_t n_slots = 0;
+  int32_t hkv = 0;
+  int32_t d = 0;
+};
+
+CacheView view_from_desc(const vattn_cache_desc* c);
+
+// Kernel-side per-handle state (tensor-map cache, split-K workspace); defined in kernels.cu.
+struct KernelState;
+KernelState* kernel_state_new();
+void kernel_state_free(KernelState*);
+
+// Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
+void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,
+                      const void* v_new, int batch, int n_new, const int32_t* seqlens,
+                      const int32_t* batch_idx, cudaStream_t st);
+void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
+                   int batch, int hq, const int32_t* seqlens, const int32_t* batch_idx,
+                   float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st);
+void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
+                    int n_q, int hq, int slot, int kv_len, float scale, bool causal,
+                    cudaStream_t st);
+
+}  // namespace vattn

@@ -1,0 +1,597 @@
+// sm_100a kernels of the vAttention hot path: KV append, TMA-fed split-K GQA decode attention
+// (contiguous virtual cache and paged comparison variant), split combine.  The tcgen05 prefill
+// kernel lives in prefill.cu.
+//
+// Cache layout: per layer a K and a V region, token-major rows of Hkv*D bf16;
+// slot i starts at i*slot_stride (manager.py:137-138 `slot_offset`), token p of a slot at
+// p*token_stride.  No block table: the kernels address the virtual tensor directly.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "internal.h"
+#include "ptx.cuh"
+#include "vattn.h"
+
+namespace vattn {
+
+// ------------------------------------------------------------------------------ KV append
+// One 16-byte chunk per thread-iteration; rows are contiguous in both source and destination
+// so warps issue fully coalesced 128-bit loads and stores.
+struct AppendParams {
+  const uint4* k_src;
+  const uint4* v_src;
+  char* k_dst;
+  char* v_dst;
+  const int32_t* seqlens;
+  const int32_t* batch_idx;
+  int64_t slot_stride, token_stride;
+  int32_t n_new, chunks_per_row;
+  int64_t total_chunks;  // batch * n_new * chunks_per_row
+};
+
+__global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < p.total_chunks; c += stride) {
+    const int64_t row = c / p.chunks_per_row;
+    const int32_t within = (int32_t)(c - row * p.chunks_per_row);
+    const int32_t b = (int32_t)(row / p.n_new);
+    const int32_t i = (int32_t)(row - (int64_t)b * p.n_new);
+    const int32_t slot = p.batch_idx ? __ldg(p.batch_idx + b) : b;
+    const int64_t pos = (int64_t)__ldg(p.seqlens + b) + i;
+    const int64_t dst = (int64_t)slot * p.slot_stride + pos * p.token_stride + (int64_t)within * 16;
+    uint4 kv, vv;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(kv.x), "=r"(kv.y), "=r"(kv.z), "=r"(kv.w)
+                 : "l"(p.k_src + c));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
+                 : "l"(p.v_src + c));
+    *reinterpret_cast<uint4*>(p.k_dst + dst) = kv;
+    *reinterpret_cast<uint4*>(p.v_dst + dst) = vv;
+  }
+}
+
+// ------------------------------------------------------------------------------ decode
+constexpr int kTile = 64;        // tokens per pipeline stage
+constexpr int kConsumerWarps = 4;  // each owns 16 tokens of a tile
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + one TMA producer warp
+
+struct DecodeParams {
+  const __nv_bfloat16* q;     // [batch, hq, D]
+  __nv_bfloat16* out;         // [batch, hq, D]
+  float* part_o;              // [batch, hq, splits, D]  (split mode)
+  float* part_lse;            // [batch, hq, splits]     log2 domain
+  const int32_t* seqlens;
+  const int32_t* batch_idx;   // contiguous: cache slot of row b (nullptr = b)
+  const int32_t* block_table; // paged: [batch, max_blocks]
+  int32_t max_blocks, block_size, box_tokens;
+  int32_t hq, group, num_splits;
+  float scale_log2;
+};
+
+template <int D, int STAGES>
+struct DecodeSmem {
+  static constexpr int kHalfBytes = kTile * 128;             // 64 tokens x 64 dims x bf16
+  static constexpr int kTileBytes = (D / 64) * kHalfBytes;   // one of K or V
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kQStride = D + 8;                     // bf16 elements, conflict-free ldmatrix
+  static constexpr int kQBytes = 16 * kQStride * 2;
+  static constexpr int kRedBytes = kConsumerWarps * 16 * 2 * 4;
+  static constexpr int kBarOff = STAGES * kStageBytes + kQBytes + kRedBytes;
+  static constexpr int kBytes = kBarOff + 2 * STAGES * 8 + 1024;  // + alignment slack
+};
+
+template <int D, int STAGES, bool PAGED>
+__global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                          const __grid_constant__ CUtensorMap vmap,
+                                                          DecodeParams p) {
+  using L = DecodeSmem<D, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * L::kStageBytes);
+  float* red = reinterpret_cast<float*>(smem + STAGES * L::kStageBytes + L::kQBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + STAGES;
+
+  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int seqlen = __ldg(p.seqlens + b);
+  const int n_tiles_all = (seqlen + kTile - 1) / kTile;
+  const int tps = (n_tiles_all + p.num_splits - 1) / p.num_splits;
+  const int tile_begin = split * tps;
+  const int n_tiles = max(0, min(n_tiles_all, tile_begin + tps) - tile_begin);
+  const int slot = (!PAGED && p.batch_idx) ? __ldg(p.batch_idx + b) : b;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ===== TMA producer =====
+    if (lane == 0 && n_tiles > 0) {
+      ptx::prefetch_tmap(&kmap);
+      ptx::prefetch_tmap(&vmap);
+      for (int it = 0; it < n_tiles; ++it) {
+        const int st = it % STAGES;
+        if (it >= STAGES) ptx::mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        uint8_t* ks = smem + st * L::kStageBytes;
+        uint8_t* vs = ks + L::kTileBytes;
+        ptx::mbar_arrive_expect_tx(&full[st], L::kStageBytes);
+        const int tok0 = (tile_begin + it) * kTile;
+        if constexpr (!PAGED) {
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h) {
+            ptx::tma_load_4d(ks + h * L::kHalfBytes, &kmap, &full[st], h * 64, kvh, tok0, slot);
+            ptx::tma_load_4d(vs + h * L::kHalfBytes, &vmap, &full[st], h * 64, kvh, tok0, slot);
+          }
+        } else {
+          const int last_blk = (seqlen - 1) / p.block_size;
+          for (int sub = 0; sub < kTile / p.box_tokens; ++sub) {
+            const int tok = tok0 + sub * p.box_tokens;
+            const int bi = min(tok / p.block_size, last_blk);  // rows past seqlen are masked
+            const int blk = __ldg(p.block_table + (int64_t)b * p.max_blocks + bi);
+            const int within = tok % p.block_size;
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h) {
+              ptx::tma_load_4d(ks + h * L::kHalfBytes + sub * p.box_tokens * 128, &kmap, &full[st],
+                               h * 64, kvh, within, blk);
+              ptx::tma_load_4d(vs + h * L::kHalfBytes + sub * p.box_tokens * 128, &vmap, &full[st],
+                               h * 64, kvh, within, blk);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers: 4 warps x 16 tokens of every tile =====
+  // Q rows of this GQA group -> smem (rows >= group are zero padding of the m16 tile)
+  for (int i = threadIdx.x; i < 16 * (D / 8); i += kConsumerWarps * 32) {
+    const int r = i / (D / 8), c = i % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < p.group)
+      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.hq + kvh * p.group + r) * D + c * 8);
+    *reinterpret_cast<uint4*>(qs + r * L::kQStride + c * 8) = v;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  uint32_t qa[D / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    const int r = ((lane >> 3) & 1) * 8 + (lane & 7);
+    const int c = kk * 16 + (lane >> 4) * 8;
+    ptx::ldsm_x4(ptx::smem_u32(qs + r * L::kQStride + c), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+  }
+
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  for (int it = 0; it < n_tiles; ++it) {
+    const int st = it % STAGES;
+    ptx::mbar_wait(&full[st], (it / STAGES) & 1);
+    const uint32_t ks = ptx::smem_u32(smem + st * L::kStageBytes);
+    const uint32_t vs = ks + L::kTileBytes;
+    const int my_tok0 = (tile_begin + it) * kTile + warp * 16;
+    const int valid = min(16, seqlen - my_tok0);
+    if (valid > 0) {
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int row = warp * 16 + ((lane >> 4) << 3) + (lane & 7);
+        const int chunk = ((kk & 3) << 1) + ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ptx::ldsm_x4(ptx::swz128(ks + (kk >> 2) * L::kHalfBytes, row, chunk), b0, b1, b2, b3);
+        ptx::mma_bf16_16816(s[0], qa[kk], b0, b1);
+        ptx::mma_bf16_16816(s[1], qa[kk], b2, b3);
+      }
+      // scale into the log2 domain and mask tokens past seqlen
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = j * 8 + 2 * t4 + (e & 1);
+          s[j][e] = col < valid ? s[j][e] * p.scale_log2 : -INFINITY;
+        }
+      float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+      float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float c0 = ptx::fast_exp2(m0 - mn0), c1 = ptx::fast_exp2(m1 - mn1);  // m=-inf -> 0
+      m0 = mn0;
+      m1 = mn1;
+      float p_[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        p_[j][0] = ptx::fast_exp2(s[j][0] - mn0);
+        p_[j][1] = ptx::fast_exp2(s[j][1] - mn0);
+        p_[j][2] = ptx::fast_exp2(s[j][2] - mn1);
+        p_[j][3] = ptx::fast_exp2(s[j][3] - mn1);
+      }
+      l0 = l0 * c0 + (p_[0][0] + p_[0][1] + p_[1][0] + p_[1][1]);
+      l1 = l1 * c1 + (p_[0][2] + p_[0][3] + p_[1][2] + p_[1][3]);
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= c0; o[n][1] *= c0;
+        o[n][2] *= c1; o[n][3] *= c1;
+      }
+      if (valid < 16) {
+        // rows past seqlen may hold stale bytes of a reused physical page: 0 * NaN must not
+        // reach the accumulator, so zero them (they are the last rows this CTA reads).
+        for (int i = lane; i < (16 - valid) * (D / 8); i += 32) {
+          const int r = warp * 16 + valid + i / (D / 8);
+          const int c = i % (D / 8);
+          const uint32_t a = ptx::swz128(vs + (c >> 3) * L::kHalfBytes, r, c & 7);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(0u));
+        }
+        __syncwarp();
+      }
+      uint32_t pa[4];
+      pa[0] = ptx::pack_bf16(p_[0][0], p_[0][1]);
+      pa[1] = ptx::pack_bf16(p_[0][2], p_[0][3]);
+      pa[2] = ptx::pack_bf16(p_[1][0], p_[1][1]);
+      pa[3] = ptx::pack_bf16(p_[1][2], p_[1][3]);
+#pragma unroll
+      for (int nd = 0; nd < D / 16; ++nd) {
+        const int row = warp * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
+        const int chunk = ((nd & 3) << 1) + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ptx::ldsm_x4_t(ptx::swz128(vs + (nd >> 2) * L::kHalfBytes, row, chunk), b0, b1, b2, b3);
+        ptx::mma_bf16_16816(o[2 * nd], pa, b0, b1);
+        ptx::mma_bf16_16816(o[2 * nd + 1], pa, b2, b3);
+      }
+      if (valid < 16) ptx::fence_proxy_async();
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[st]);
+  }
+
+  // ===== merge the 4 warps' (m, l, O) and write =====
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  float* red_m = red;
+  float* red_l = red + kConsumerWarps * 16;
+  if (t4 == 0) {
+    red_m[warp * 16 + g] = m0;
+    red_m[warp * 16 + g + 8] = m1;
+    red_l[warp * 16 + g] = l0;
+    red_l[warp * 16 + g + 8] = l1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  float M0 = -INFINITY, M1 = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    M0 = fmaxf(M0, red_m[w * 16 + g]);
+    M1 = fmaxf(M1, red_m[w * 16 + g + 8]);
+  }
+  const float sc0 = (M0 == -INFINITY) ? 0.f : ptx::fast_exp2(m0 - M0);
+  const float sc1 = (M1 == -INFINITY) ? 0.f : ptx::fast_exp2(m1 - M1);
+  // every stage has been consumed: reuse the pipeline smem as [warp][16][D] fp32 scratch
+  float* scratch = reinterpret_cast<float*>(smem);
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    const int c = n * 8 + 2 * t4;
+    float* r0 = scratch + (warp * 16 + g) * D + c;
+    float* r1 = scratch + (warp * 16 + g + 8) * D + c;
+    r0[0] = o[n][0] * sc0;
+    r0[1] = o[n][1] * sc0;
+    r1[0] = o[n][2] * sc1;
+    r1[1] = o[n][3] * sc1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  for (int i = threadIdx.x; i < p.group * D; i += kConsumerWarps * 32) {
+    const int r = i / D, c = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, red_m[w * 16 + r]);
+    float lsum = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float mw = red_m[w * 16 + r];
+      const float f = (M == -INFINITY) ? 0.f : ptx::fast_exp2(mw - M);
+      lsum += red_l[w * 16 + r] * f;
+      acc += scratch[(w * 16 + r) * D + c];
+    }
+    const float val = lsum > 0.f ? acc / lsum : 0.f;
+    const int head = kvh * p.group + r;
+    if (p.num_splits == 1) {
+      p.out[((int64_t)b * p.hq + head) * D + c] = __float2bfloat16(val);
+    } else {
+      const int64_t row = ((int64_t)b * p.hq + head) * p.num_splits + split;
+      p.part_o[row * D + c] = val;
+      if (c == 0) p.part_lse[row] = lsum > 0.f ? M + log2f(lsum) : -INFINITY;
+    }
+  }
+}
+
+// merge split partials with log-sum-exp weights (log2 domain)
+template <int D>
+__global__ void __launch_bounds__(128) decode_combine_kernel(const float* __restrict__ part_o,
+                                                             const float* __restrict__ part_lse,
+                                                             __nv_bfloat16* __restrict__ out,
+                                                             int rows, int num_splits) {
+  const int row = blockIdx.x * (blockDim.x / (D / 4)) + threadIdx.x / (D / 4);
+  const int c4 = threadIdx.x % (D / 4);
+  if (row >= rows) return;
+  const float* lse = part_lse + (int64_t)row * num_splits;
+  float M = -INFINITY;
+  for (int s = 0; s < num_splits; ++s) M = fmaxf(M, lse[s]);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float wsum = 0.f;
+  if (M != -INFINITY) {
+    for (int s = 0; s < num_splits; ++s) {
+      const float w = exp2f(lse[s] - M);
+      if (w == 0.f) continue;
+      const float4 v = *reinterpret_cast<const float4*>(part_o + ((int64_t)row * num_splits + s) * D + c4 * 4);
+      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+      wsum += w;
+    }
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(out + (int64_t)row * D + c4 * 4) = pk;
+}
+
+// ------------------------------------------------------------------------------ host side
+struct KernelState {
+  std::mutex mu;
+  std::map<std::tuple<uint64_t, int64_t, int64_t, int, int, int, int, int>, CUtensorMap> maps;
+};
+KernelState* kernel_state_new() { return new KernelState(); }
+void kernel_state_free(KernelState* s) { delete s; }
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    check_rt(cudaGetDevice(&dev), "cudaGetDevice");
+    check_rt(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  }
+  return g_num_sms;
+}
+
+// 4-D bf16 map over (D, Hkv, tokens, slots|blocks), 128B swizzle, box (64, 1, box_tokens, 1).
+static CUtensorMap make_kv_map(uint64_t base, int d, int hkv, int64_t token_stride, int tokens,
+                               int64_t outer_stride, int outer, int box_tokens) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)hkv, (cuuint64_t)tokens, (cuuint64_t)outer};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)token_stride, (cuuint64_t)outer_stride};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)box_tokens, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  check_cu(driver().TensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                                         reinterpret_cast<void*>(base), dims, strides, box, estr,
+                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled");
+  return m;
+}
+
+static CUtensorMap cached_map(KernelState* ks, uint64_t base, int d, int hkv, int64_t token_stride,
+                              int tokens, int64_t outer_stride, int outer, int box_tokens) {
+  if (!ks) return make_kv_map(base, d, hkv, token_stride, tokens, outer_stride, outer, box_tokens);
+  auto key = std::make_tuple(base, token_stride, outer_stride, tokens, outer, hkv, d, box_tokens);
+  std::lock_guard<std::mutex> lk(ks->mu);
+  auto it = ks->maps.find(key);
+  if (it != ks->maps.end()) return it->second;
+  CUtensorMap m = make_kv_map(base, d, hkv, token_stride, tokens, outer_stride, outer, box_tokens);
+  ks->maps.emplace(key, m);
+  return m;
+}
+
+static void check_view(const CacheView& v) {
+  if (v.d != 64 && v.d != 128) throw Fail(VATTN_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (v.token_stride % 16 || v.slot_stride % 16 || (v.k_base | v.v_base) % 16)
+    throw Fail(VATTN_UNSUPPORTED, "cache rows must be 16-byte aligned");
+}
+
+void launch_kv_append(KernelState*, int, const CacheView& v, const void* k_new, const void* v_new,
+                      int batch, int n_new, const int32_t* seqlens, const int32_t* batch_idx,
+                      cudaStream_t st) {
+  check_view(v);
+  if (batch <= 0 || n_new <= 0) return;
+  const int64_t row_bytes = (int64_t)v.hkv * v.d * 2;
+  AppendParams p;
+  p.k_src = reinterpret_cast<const uint4*>(k_new);
+  p.v_src = reinterpret_cast<const uint4*>(v_new);
+  p.k_dst = reinterpret_cast<char*>(v.k_base);
+  p.v_dst = reinterpret_cast<char*>(v.v_base);
+  p.seqlens = seqlens;
+  p.batch_idx = batch_idx;
+  p.slot_stride = v.slot_stride;
+  p.token_stride = v.token_stride;
+  p.n_new = n_new;
+  p.chunks_per_row = (int32_t)(row_bytes / 16);
+  p.total_chunks = (int64_t)batch * n_new * p.chunks_per_row;
+  const int threads = 256;
+  const int64_t want = (p.total_chunks + threads - 1) / threads;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
+  kv_append_kernel<<<blocks, threads, 0, st>>>(p);
+  check_rt(cudaGetLastError(), "kv_append launch");
+}
+
+constexpr int kMaxSplits = 64;
+
+static int auto_splits(int units, int max_len) {
+  const int tiles = std::max(1, (max_len + kTile - 1) / kTile);
+  const int target = num_sms() * 2;  // two resident CTAs per SM
+  int s = (target + units - 1) / units;
+  s = std::min(s, std::max(1, tiles / 4));  // keep >= 4 tiles (256 tokens) per split
+  return std::max(1, std::min(s, kMaxSplits));
+}
+
+template <int D, int STAGES, bool PAGED>
+static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParams p, int batch,
+                       int hkv, cudaStream_t st) {
+  using L = DecodeSmem<D, STAGES>;
+  auto kern = decode_kernel<D, STAGES, PAGED>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    check_rt(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes),
+             "decode smem attribute");
+    attr_done = true;
+  }
+  dim3 grid(p.num_splits, hkv, batch);
+  kern<<<grid, kThreads, L::kBytes, st>>>(km, vm, p);
+  check_rt(cudaGetLastError(), "decode launch");
+  if (p.num_splits > 1) {
+    const int rows = batch * p.hq;
+    const int per_block = 128 / (D / 4);
+    decode_combine_kernel<D><<<(rows + per_block - 1) / per_block, 128, 0, st>>>(
+        p.part_o, p.part_lse, p.out, rows, p.num_splits);
+    check_rt(cudaGetLastError(), "combine launch");
+  }
+}
+
+static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, int hkv, int hq,
+                          const void* q, void* out, int batch, const int32_t* seqlens,
+                          const int32_t* batch_idx, const int32_t* block_table, int max_blocks,
+                          int block_size, int box_tokens, float scale, int num_splits,
+                          int max_len, void* ws, int64_t ws_bytes, bool paged, cudaStream_t st) {
+  if (hq % hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
+  const int group = hq / hkv;
+  if (group > 16) throw Fail(VATTN_UNSUPPORTED, "GQA group larger than 16");
+  if (batch <= 0) return;
+  if (num_splits <= 0) num_splits = auto_splits(batch * hkv, max_len);
+  num_splits = std::min(num_splits, kMaxSplits);
+  DecodeParams p{};
+  p.q = reinterpret_cast<const __nv_bfloat16*>(q);
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.seqlens = seqlens;
+  p.batch_idx = batch_idx;
+  p.block_table = block_table;
+  p.max_blocks = max_blocks;
+  p.block_size = block_size;
+  p.box_tokens = box_tokens;
+  p.hq = hq;
+  p.group = group;
+  p.num_splits = num_splits;
+  if (scale <= 0.f) scale = 1.f / sqrtf((float)d);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  if (num_splits > 1) {
+    const int64_t need = vattn_decode_workspace_bytes(batch, hq, d, num_splits);
+    if (!ws || ws_bytes < need) throw Fail(VATTN_VALUE_ERROR, "decode workspace too small");
+    p.part_o = reinterpret_cast<float*>(ws);
+    p.part_lse = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                          (int64_t)batch * hq * num_splits * d * 4);
+  }
+  if (d == 128) {
+    if (paged) run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
+    else run_decode<128, 4, false>(km, vm, p, batch, hkv, st);
+  } else {
+    if (paged) run_decode<64, 6, true>(km, vm, p, batch, hkv, st);
+    else run_decode<64, 6, false>(km, vm, p, batch, hkv, st);
+  }
+}
+
+void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void* out, int batch,
+                   int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
+                   int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  check_view(v);
+  const CUtensorMap km = cached_map(ks, v.k_base, v.d, v.hkv, v.token_stride, v.slot_tokens, v.slot_stride, v.n_slots, kTile);
+  const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, v.slot_tokens, v.slot_stride, v.n_slots, kTile);
+  decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
+                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st);
+}
+
+}  // namespace vattn
+
+// ================================================================================ C ABI
+using vattn::Fail;
+
+template <typename F>
+static vattn_status kguard(F&& f) {
+  try {
+    f();
+    return VATTN_OK;
+  } catch (const Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
+}
+
+extern "C" {
+
+int32_t vattn_decode_num_splits(int32_t batch, int32_t hkv, int32_t max_seqlen) {
+  try {
+    return vattn::auto_splits(batch * hkv, max_seqlen);
+  } catch (...) {
+    return 1;
+  }
+}
+
+int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t hq, int32_t d, int32_t num_splits) {
+  const int64_t s = num_splits > 0 ? num_splits : vattn::kMaxSplits;
+  return (int64_t)batch * hq * s * (d + 1) * 4;
+}
+
+vattn_status vattn_kv_append_raw(const vattn_cache_desc* c, const void* k_new, const void* v_new,
+                                 int32_t batch, int32_t n_new, const int32_t* seqlens,
+                                 const int32_t* batch_idx, void* stream) {
+  return kguard([&] {
+    vattn::launch_kv_append(nullptr, -1, vattn::view_from_desc(c), k_new, v_new, batch, n_new,
+                            seqlens, batch_idx, (cudaStream_t)stream);
+  });
+}
+
+vattn_status vattn_decode_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t batch,
+                              int32_t hq, const int32_t* seqlens, const int32_t* batch_idx,
+                              float scale, int32_t num_splits, void* ws, int64_t ws_bytes,
+                              void* stream) {
+  return kguard([&] {
+    const vattn::CacheView v = vattn::view_from_desc(c);
+    vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, seqlens, batch_idx, scale, num_splits,
+                         ws, ws_bytes, (cudaStream_t)stream);
+  });
+}
+
+vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,
+                                int32_t num_blocks, int32_t block_size, int32_t hkv, int32_t d,
+                                const int32_t* block_table, int32_t max_blocks, void* out,
+                                int32_t batch, int32_t hq, const int32_t* seqlens, float scale,
+                                int32_t num_splits, void* ws, int64_t ws_bytes, void* stream) {
+  return kguard([&] {
+    if (d != 64 && d != 128) throw Fail(VATTN_UNSUPPORTED, "head_dim must be 64 or 128");
+    if (block_size <= 0 || (block_size < vattn::kTile && vattn::kTile % block_size) ||
+        (block_size >= vattn::kTile && block_size % vattn::kTile))
+      throw Fail(VATTN_UNSUPPORTED, "block_size must divide 64 or be a multiple of 64");
+    const int box = std::min(block_size, vattn::kTile);
+    const int64_t row = (int64_t)hkv * d * 2;
+    const CUtensorMap km = vattn::make_kv_map((uint64_t)k_pool, d, hkv, row, block_size,
+                                              row * block_size, num_blocks, box);
+    const CUtensorMap vm = vattn::make_kv_map((uint64_t)v_pool, d, hkv, row, block_size,
+                                              row * block_size, num_blocks, box);
+    vattn::decode_common(km, vm, d, hkv, hq, q, out, batch, seqlens, nullptr, block_table,
+                         max_blocks, block_size, box, scale, num_splits, max_blocks * block_size,
+                         ws, ws_bytes, true, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"
