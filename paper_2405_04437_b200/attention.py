@@ -1,0 +1,187 @@
+"""Attention entry points over the virtual KV cache (torch tensors only at this edge).
+
+Semantics follow the paper's use of flash_attn_with_kvcache: q [B, Hq, D],
+`cache_seqlens[b]` cached rows of slot `cache_batch_idx[b]`, GQA head h -> KV head h // (Hq/Hkv),
+scale 1/sqrt(D) by default, bf16 in / fp32 accumulate / bf16 out.  Every op launches the sm_100a
+kernels in libvattn.so on the current torch stream; there is no Python or CPU fallback — a
+missing library or a non-CUDA tensor is an error.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _abi
+from ._abi import check, lib
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("attention ops take CUDA tensors (there is no CPU path)")
+
+
+def _i32(t, name):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.int32 or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA int32 tensor")
+    return t.contiguous()
+
+
+def _bf16(t, name):
+    if t.dtype != torch.bfloat16:
+        raise ValueError(f"{name} must be bfloat16")
+    return t.contiguous()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+# ------------------------------------------------------------------ manager-backed ops
+def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None):
+    """Write k_new/v_new [B, T, Hkv, D] (or [B, Hkv, D] for one token) at rows
+    cache_seqlens[b] .. +T of slot cache_batch_idx[b].  The rows must be backed (call
+    mgr.step with the grown lengths first)."""
+    _need_cuda(k_new, v_new)
+    if k_new.dim() == 3:
+        k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
+    k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    check(lib().vattn_kv_append(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
+                                _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
+
+
+def decode_attention(mgr, layer: int, q, cache_seqlens, cache_batch_idx=None, softmax_scale=None,
+                     out=None, num_splits: int = 0, stream=None):
+    """o[b] = softmax(q[b] K[slot, :seqlen]ᵀ·scale) V[slot, :seqlen] for q [B, Hq, D]."""
+    _need_cuda(q)
+    q = _bf16(q, "q")
+    if out is None:
+        out = torch.empty_like(q)
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    check(lib().vattn_decode(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], _ptr(seq), _ptr(idx),
+                             float(scale), int(num_splits), C.c_void_p(_stream(stream))))
+    return out
+
+
+def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None, causal=True,
+                      softmax_scale=None, out=None, stream=None):
+    """Causal (bottom-right aligned) attention of q [S, Hq, D] over rows [0, kv_len) of slot
+    req_id (default kv_len = S, i.e. the prompt just appended)."""
+    _need_cuda(q)
+    q = _bf16(q, "q")
+    if out is None:
+        out = torch.empty_like(q)
+    kv_len = q.shape[0] if kv_len is None else kv_len
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    check(lib().vattn_prefill(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
+                              float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
+    return out
+
+
+# ------------------------------------------------------------------ standalone ops
+def cache_desc(k_cache, v_cache) -> _abi.CacheDesc:
+    """Descriptor of caller-owned token-major caches [slots, tokens, Hkv, D] (any slot/token
+    strides, rows contiguous)."""
+    _need_cuda(k_cache, v_cache)
+    if k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
+        raise ValueError("caches must be bfloat16")
+    if k_cache.shape != v_cache.shape or k_cache.stride() != v_cache.stride():
+        raise ValueError("K and V caches must share shape and strides")
+    n, L, h, d = k_cache.shape
+    if k_cache.stride(3) != 1 or k_cache.stride(2) != d:
+        raise ValueError("each token row [Hkv, D] must be contiguous")
+    desc = _abi.CacheDesc()
+    desc.k_base, desc.v_base = k_cache.data_ptr(), v_cache.data_ptr()
+    desc.slot_stride_bytes = k_cache.stride(0) * 2
+    desc.token_stride_bytes = k_cache.stride(1) * 2
+    desc.slot_tokens, desc.n_slots, desc.n_kv_heads, desc.head_dim = L, n, h, d
+    return desc
+
+
+def kv_append_raw(k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None):
+    desc = cache_desc(k_cache, v_cache)
+    if k_new.dim() == 3:
+        k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
+    k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    check(lib().vattn_kv_append_raw(C.byref(desc), _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
+                                    _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(device, nbytes):
+    ws = _ws_cache.get(device)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _ws_cache[device] = ws
+    return ws
+
+
+def decode_attention_raw(q, k_cache, v_cache, cache_seqlens, cache_batch_idx=None, softmax_scale=None,
+                         out=None, num_splits: int = 0, stream=None):
+    desc = cache_desc(k_cache, v_cache)
+    q = _bf16(q, "q")
+    out = torch.empty_like(q) if out is None else out
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    b, hq, d = q.shape
+    nbytes = lib().vattn_decode_workspace_bytes(b, hq, d, 0)
+    ws = _workspace(q.device, nbytes)
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_decode_raw(C.byref(desc), _ptr(q), _ptr(out), b, hq, _ptr(seq), _ptr(idx), float(scale),
+                                 int(num_splits), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return out
+
+
+def decode_attention_paged(q, k_pool, v_pool, block_table, seqlens, softmax_scale=None, out=None,
+                           num_splits: int = 0, stream=None):
+    """PagedAttention-layout comparison kernel: pools [num_blocks, block_size, Hkv, D],
+    block_table [B, max_blocks] int32 (PAPER.md:602 block sizes 16 / 256)."""
+    _need_cuda(q, k_pool, v_pool)
+    q = _bf16(q, "q")
+    k_pool, v_pool = _bf16(k_pool, "k_pool"), _bf16(v_pool, "v_pool")
+    out = torch.empty_like(q) if out is None else out
+    bt = _i32(block_table, "block_table")
+    seq = _i32(seqlens, "seqlens")
+    b, hq, d = q.shape
+    nb, bs, hkv, _ = k_pool.shape
+    nbytes = lib().vattn_decode_workspace_bytes(b, hq, d, 0)
+    ws = _workspace(q.device, nbytes)
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_decode_paged(_ptr(q), _ptr(k_pool), _ptr(v_pool), nb, bs, hkv, d, _ptr(bt), bt.shape[1],
+                                   _ptr(out), b, hq, _ptr(seq), float(scale), int(num_splits), _ptr(ws),
+                                   ws.numel(), C.c_void_p(_stream(stream))))
+    return out
+
+
+def decode_num_splits(batch: int, n_kv_heads: int, max_seqlen: int) -> int:
+    return lib().vattn_decode_num_splits(batch, n_kv_heads, max_seqlen)
+
+
+def prefill_attention_raw(q, k_cache, v_cache, req_slot: int, kv_len: int, causal=True,
+                          softmax_scale=None, out=None, stream=None):
+    desc = cache_desc(k_cache, v_cache)
+    q = _bf16(q, "q")
+    out = torch.empty_like(q) if out is None else out
+    n_q, hq, d = q.shape
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_prefill_raw(C.byref(desc), _ptr(q), _ptr(out), n_q, hq, int(req_slot), int(kv_len),
+                                  float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
+    return out

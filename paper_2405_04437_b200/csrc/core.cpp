@@ -11,6 +11,7 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <chrono>
 #include <condition_variable>
@@ -287,7 +288,7 @@ class Manager {
   CUmemAccessDesc access_{};
   std::vector<int64_t> run_begin_, run_end_;  // pending cuMemSetAccess page runs per buffer
   cudaEvent_t use_event_ = nullptr;
-  bool use_recorded_ = false;
+  std::atomic<bool> use_recorded_{false};
   bool fenced_ = false;
   // measured real-driver statistics
   int64_t real_maps_ = 0, real_unmaps_ = 0, real_access_ = 0, real_creates_ = 0,

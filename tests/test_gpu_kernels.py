@@ -1,0 +1,130 @@
+"""GPU parity of the sm_100a kernels against the fp32 CPU oracle (oracle/attention.py).
+
+Tolerance (north_star): bf16 inputs, fp32 accumulation, max relative error
+max|o - o_ref| / max|o_ref| <= 2e-2.  KV append is byte work: bit-exact.
+"""
+
+import pytest
+import torch
+
+from oracle.attention import decode_ref, kv_append_ref, max_rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    return torch.device("cuda")
+
+
+def _rand(shape, gen, scale=1.0):
+    return (torch.randn(shape, generator=gen) * scale).to(torch.bfloat16)
+
+
+def _mk_cache(slots, L, hkv, d, gen, fill_nan=False):
+    k = _rand((slots, L, hkv, d), gen)
+    v = _rand((slots, L, hkv, d), gen)
+    return k, v
+
+
+DECODE_CASES = [
+    # B, Hq, Hkv, D, seqlens, idx permutation?, splits
+    (2, 8, 2, 64, [128, 512], False, 0),                       # config 1 (tiny)
+    (2, 8, 2, 64, [128, 512], False, 3),
+    (6, 32, 8, 128, [1, 63, 64, 65, 1000, 4096], True, 0),     # L8 shape, ragged
+    (6, 32, 8, 128, [1, 63, 64, 65, 1000, 4096], False, 1),
+    (6, 32, 8, 128, [1, 63, 64, 65, 1000, 4096], False, 5),
+    (3, 56, 8, 128, [8192, 777, 4097], True, 0),                # Y34 group of 7
+    (2, 32, 4, 128, [2048, 31], False, 0),                      # Y6 group of 8
+    (3, 7, 1, 128, [300, 0, 129], False, 2),                    # Y34/8 shard: 1 KV head, empty row
+    (4, 16, 1, 64, [64, 65, 127, 1], True, 0),                  # group of 16
+]
+
+
+@pytest.mark.parametrize("case", DECODE_CASES, ids=[str(i) for i in range(len(DECODE_CASES))])
+def test_decode_raw_matches_oracle(case):
+    from paper_2405_04437_b200.attention import decode_attention_raw
+
+    dev = _cuda()
+    B, hq, hkv, d, lens, perm, splits = case
+    gen = torch.Generator().manual_seed(0)
+    L = max(max(lens), 1)
+    L = (L + 63) // 64 * 64
+    slots = B + 2
+    k, v = _mk_cache(slots, L, hkv, d, gen)
+    q = _rand((B, hq, d), gen)
+    idx = torch.randperm(slots, generator=gen)[:B].to(torch.int32) if perm else torch.arange(B, dtype=torch.int32)
+    seq = torch.tensor(lens, dtype=torch.int32)
+    ref = decode_ref(q, k, v, seq, idx)
+    out = decode_attention_raw(q.to(dev), k.to(dev), v.to(dev), seq.to(dev), idx.to(dev), num_splits=splits)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    err = max_rel_err(out.cpu(), ref)
+    assert err <= TOL, err
+    for b, n in enumerate(lens):
+        if n == 0:
+            assert out[b].abs().max().item() == 0.0
+
+
+def test_decode_ignores_stale_rows_past_seqlen():
+    """Rows past seqlen inside the last tile may hold NaN/Inf left in a reused physical page."""
+    from paper_2405_04437_b200.attention import decode_attention_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(1)
+    B, hq, hkv, d, L = 3, 32, 8, 128, 256
+    k, v = _mk_cache(B, L, hkv, d, gen)
+    lens = [5, 100, 191]
+    for b, n in enumerate(lens):
+        k[b, n:] = float("nan")
+        v[b, n:] = float("inf")
+    q = _rand((B, hq, d), gen)
+    seq = torch.tensor(lens, dtype=torch.int32)
+    ref = decode_ref(q, k, v, seq)
+    for splits in (1, 2):
+        out = decode_attention_raw(q.to(dev), k.to(dev), v.to(dev), seq.to(dev), num_splits=splits)
+        assert torch.isfinite(out.float()).all()
+        assert max_rel_err(out.cpu(), ref) <= TOL
+
+
+@pytest.mark.parametrize("block_size", [16, 64, 256])
+def test_decode_paged_matches_oracle(block_size):
+    from paper_2405_04437_b200.attention import decode_attention_paged
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(2)
+    B, hq, hkv, d = 5, 32, 8, 128
+    lens = [1, 300, 1024, 17, 2049]
+    maxb = (max(lens) + block_size - 1) // block_size
+    nblocks = B * maxb + 3
+    kp, vp = _mk_cache(nblocks, block_size, hkv, d, gen)
+    perm = torch.randperm(nblocks, generator=gen)[: B * maxb].view(B, maxb).to(torch.int32)
+    # gather the oracle's contiguous view of each sequence
+    kc = kp[perm.long()].reshape(B, maxb * block_size, hkv, d)
+    vc = vp[perm.long()].reshape(B, maxb * block_size, hkv, d)
+    q = _rand((B, hq, d), gen)
+    seq = torch.tensor(lens, dtype=torch.int32)
+    ref = decode_ref(q, kc, vc, seq)
+    out = decode_attention_paged(q.to(dev), kp.to(dev), vp.to(dev), perm.to(dev), seq.to(dev))
+    assert max_rel_err(out.cpu(), ref) <= TOL
+
+
+def test_kv_append_raw_bit_exact():
+    from paper_2405_04437_b200.attention import kv_append_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(3)
+    slots, L, hkv, d = 5, 300, 8, 128
+    k, v = _mk_cache(slots, L, hkv, d, gen)
+    for B, T in ((4, 1), (2, 37), (1, 256)):
+        kn = _rand((B, T, hkv, d), gen)
+        vn = _rand((B, T, hkv, d), gen)
+        seq = torch.randint(0, L - T, (B,), generator=gen, dtype=torch.int32)
+        idx = torch.randperm(slots, generator=gen)[:B].to(torch.int32)
+        kr, vr = kv_append_ref(k, v, kn, vn, seq, idx)
+        kd, vd = k.to(dev), v.to(dev)
+        kv_append_raw(kd, vd, kn.to(dev), vn.to(dev), seq.to(dev), idx.to(dev))
+        assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)
+        k, v = kr, vr

@@ -1,0 +1,127 @@
+"""GPU: the allocator with the real CUDA VMM backend (cuMemAddressReserve / cuMemCreate /
+cuMemMap / cuMemSetAccess at 2 MiB) — bookkeeping parity against the reference recordings,
+and the kernels running on the resulting virtual tensors."""
+
+import pytest
+import torch
+
+from allocator_replay import CoreAdapter, load_fixtures, replay
+from oracle.attention import decode_ref, max_rel_err
+
+pytestmark = pytest.mark.gpu
+
+MB2 = 2 * 1024 * 1024
+GPU_FIXTURES = [f for f in load_fixtures()
+                if f["config"]["page_group_size"] == MB2 and f["config"]["pool_bytes"] <= 8 * 1024 ** 3]
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+@pytest.mark.parametrize("fixture", GPU_FIXTURES, ids=[f["name"] for f in GPU_FIXTURES])
+def test_cuda_backend_bookkeeping_matches_reference(fixture):
+    _cuda()
+    a = CoreAdapter(fixture, backend="cuda")
+    try:
+        replay(fixture, a)
+        st = a.m.driver_stats()
+        # every shadow map was a real cuMemMap (+ coalesced cuMemSetAccess)
+        assert st["real_maps"] == a.m.vmm.calls.get("cuMemMap", 0)
+        assert st["real_unmaps"] == a.m.vmm.calls.get("cuMemUnmap", 0)
+    finally:
+        a.close()
+
+
+def test_tiny_config_end_to_end():
+    """BASELINE config 1: 1 layer, 8 Q / 2 KV heads, D 64, batch 2, contexts 128-512, 2 MiB."""
+    _cuda()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention, kv_append
+    from paper_2405_04437_b200.geometry import tiny
+
+    dev = torch.device("cuda")
+    g = tiny()
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * 1024 * 1024))
+    r0, r1 = mgr.alloc_reqid(), mgr.alloc_reqid()
+    lens = [0, 0]
+    lens[r0], lens[r1] = 128, 512
+    assert mgr.step(lens).ok
+    assert mgr.vmm.pool.mapped == 2 * 2      # 1 group per slot x 2 buffers
+    gen = torch.Generator().manual_seed(0)
+    for rid in (r0, r1):
+        n = lens[rid]
+        kn = torch.randn(1, n, 2, 64, generator=gen).to(torch.bfloat16)
+        vn = torch.randn(1, n, 2, 64, generator=gen).to(torch.bfloat16)
+        kv_append(mgr, 0, kn.to(dev), vn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                  torch.tensor([rid], dtype=torch.int32, device=dev))
+    torch.cuda.synchronize()
+    kc, vc = mgr.k_cache(0), mgr.v_cache(0)
+    q = torch.randn(2, 8, 64, generator=gen).to(torch.bfloat16)
+    seq = torch.tensor([lens[r0], lens[r1]], dtype=torch.int32)
+    idx = torch.tensor([r0, r1], dtype=torch.int32)
+    k_host = torch.zeros(2, 512, 2, 64, dtype=torch.bfloat16)
+    v_host = torch.zeros_like(k_host)
+    for rid in (r0, r1):
+        k_host[rid, : lens[rid]] = kc[rid, : lens[rid]].cpu()
+        v_host[rid, : lens[rid]] = vc[rid, : lens[rid]].cpu()
+    ref = decode_ref(q, k_host, v_host, seq, idx)
+    out = decode_attention(mgr, 0, q.to(dev), seq.to(dev), idx.to(dev))
+    torch.cuda.synchronize()
+    assert max_rel_err(out.cpu(), ref) <= 2e-2
+    mgr.close()
+
+
+def test_decode_through_manager_l8_shape_with_growth():
+    """L8 geometry (reduced batch/layers): decode steps cross a 1024-token page boundary; the
+    background thread maps the next page during the previous step's kernels."""
+    _cuda()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention, kv_append
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=256 * MB2))
+    rids = [mgr.alloc_reqid() for _ in range(3)]
+    lens = [0] * 4
+    for i, r in enumerate(rids):
+        lens[r] = 1020 + i
+    assert mgr.step(lens).ok
+    gen = torch.Generator().manual_seed(5)
+    host_k = {l: torch.zeros(4, 4096, 8, 128, dtype=torch.bfloat16) for l in range(2)}
+    host_v = {l: torch.zeros(4, 4096, 8, 128, dtype=torch.bfloat16) for l in range(2)}
+    for layer in range(2):
+        for r in rids:
+            kn = torch.randn(1, lens[r], 8, 128, generator=gen).to(torch.bfloat16)
+            vn = torch.randn(1, lens[r], 8, 128, generator=gen).to(torch.bfloat16)
+            host_k[layer][r, : lens[r]] = kn[0]
+            host_v[layer][r, : lens[r]] = vn[0]
+            kv_append(mgr, layer, kn.to(dev), vn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                      torch.tensor([r], dtype=torch.int32, device=dev))
+    idx = torch.tensor(rids, dtype=torch.int32)
+    for it in range(8):
+        nxt = list(lens)
+        for r in rids:
+            nxt[r] += 1
+        plan = mgr.plan_overlap(nxt)
+        mgr.bg_submit(plan)                    # maps crossing pages while we append+decode
+        res = mgr.step(nxt)                    # joins the window; nothing left to map
+        assert res.ok and res.sync_us == 0.0
+        seq_before = torch.tensor([lens[r] for r in rids], dtype=torch.int32)
+        seq_after = seq_before + 1
+        for layer in range(2):
+            kn = torch.randn(3, 8, 128, generator=gen).to(torch.bfloat16)
+            vn = torch.randn(3, 8, 128, generator=gen).to(torch.bfloat16)
+            for j, r in enumerate(rids):
+                host_k[layer][r, lens[r]] = kn[j]
+                host_v[layer][r, lens[r]] = vn[j]
+            kv_append(mgr, layer, kn.to(dev), vn.to(dev), seq_before.to(dev), idx.to(dev))
+            q = torch.randn(3, 32, 128, generator=gen).to(torch.bfloat16)
+            out = decode_attention(mgr, layer, q.to(dev), seq_after.to(dev), idx.to(dev))
+            ref = decode_ref(q, host_k[layer], host_v[layer], seq_after, idx)
+            torch.cuda.synchronize()
+            assert max_rel_err(out.cpu(), ref) <= 2e-2, (it, layer)
+        lens = nxt
+    assert mgr.slots[rids[-1]].mapped_groups == 2     # 1022+8 tokens crossed 1024
+    mgr.close()
