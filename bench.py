@@ -1,0 +1,459 @@
+"""Benchmark of the vAttention hot path on B200 (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload l8_decode|y34_decode|y6_prefill]
+
+Default workload = BASELINE config 2 (Llama-3-8B-shaped decode: 32 layers, 32 Q / 8 KV heads,
+D 128, batch 64, context 4K, bf16, 2 MiB pages).  One step = one decode iteration of the whole
+KV cache: allocator `step` (+ the background thread mapping the next iteration's pages), then
+per layer KV-append of the new token and split-K decode attention over it.  `value` is decode
+tokens/s with inputs resident in HBM; `e2e` is the same through the public API with the inputs
+copied H2D from pinned host memory and the outputs read back D2H every step.
+
+Multi-GPU (torchrun, one process per GPU): KV heads are sharded (geometry.with_tp(N)); every
+rank runs an independent allocator + kernels over its heads, no data-path collective; the whole
+job's tokens/s = B / (max-over-ranks step time).  Total work is fixed -> "strong" scaling.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MB2 = 2 * 1024 * 1024
+GIB = 1024 ** 3
+
+
+# ----------------------------------------------------------------------------- utilities
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- workloads
+def decode_geometry(workload: str, world: int):
+    from paper_2405_04437_b200.geometry import llama3_8b, yi_34b
+
+    if workload == "l8_decode":
+        g = llama3_8b(max_context=8192, max_batch=64)
+        ctx = 4096
+        name = "llama-3-8b decode b64 ctx4096 (32 layers)"
+    elif workload == "y34_decode":
+        # Yi-34B at G=1 does not fit (60 layers x 4 GiB); per-layer throughput on 8 layers
+        g = yi_34b(max_context=8448, max_batch=128)
+        g = g.__class__(**{**g.to_dict(), "n_layers": 8})
+        ctx = 8192
+        name = "yi-34b decode b128 ctx8192 (8 of 60 layers timed)"
+    else:
+        raise ValueError(workload)
+    return g.with_tp(world), ctx, name
+
+
+def bench_decode(args, world, rank, local):
+    import torch
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention, decode_num_splits, kv_append
+
+    dev = torch.device("cuda", local)
+    g, ctx, wname = decode_geometry(args.workload, world)
+    B, N = g.max_batch, g.n_layers
+    hkv, hq, d = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim
+    steps, warm = args.steps, args.warmup
+    # pool: every slot at ctx + the steps we run, + one group per buffer of slack
+    groups = math.ceil((ctx + steps + warm + 1) * g.per_token_layer_bytes / MB2)
+    pool = (groups + 1) * 2 * N * B * MB2
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool, eager_groups=0,
+                                          reclaim_threshold=0.0), backend="cuda", device=local)
+    t0 = time.perf_counter()
+    rids = [mgr.alloc_reqid() for _ in range(B)]
+    seq = [0] * B
+    for r in rids:
+        seq[r] = ctx
+    res0 = mgr.step(seq)
+    assert res0.ok
+    prefill_map_s = time.perf_counter() - t0
+    # synthetic K/V history: fill each layer's cache rows [0, ctx) (prefill-style append)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    zeros = torch.zeros(B, dtype=torch.int32, device=dev)
+    idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+    chunk = 512
+    for layer in range(N):
+        for c0 in range(0, ctx, chunk):
+            kn = torch.randn(B, chunk, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+            vn = torch.randn(B, chunk, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+            kv_append(mgr, layer, kn, vn, zeros + c0, idx)
+    torch.cuda.synchronize()
+    # per-step inputs (resident): q, new k/v per layer
+    q = torch.randn(N, B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    kn = torch.randn(N, B, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    vn = torch.randn(N, B, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    out = torch.empty(N, B, hq, d, device=dev, dtype=torch.bfloat16)
+    pos = torch.full((B,), ctx, dtype=torch.int32, device=dev)     # row the new token goes to
+    stream = torch.cuda.current_stream()
+
+    state = {"seq": list(seq), "pos": pos}
+    splits = decode_num_splits(B, hkv, ctx + 1)
+
+    def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out):
+        nxt = list(state["seq"])
+        for r in rids:
+            nxt[r] += 1
+        t_h = time.perf_counter()
+        r = mgr.step(nxt)                       # joins the bg window, maps any shortfall
+        exposed = time.perf_counter() - t_h
+        assert r.ok
+        p = state["pos"]
+        seqlen = p + 1
+        for layer in range(N):
+            kv_append(mgr, layer, kn_[layer], vn_[layer], p, idx)
+            if dec_events is not None:
+                dec_events[layer][0].record(stream)
+            decode_attention(mgr, layer, q_[layer], seqlen, idx, out=out_[layer], num_splits=splits)
+            if dec_events is not None:
+                dec_events[layer][1].record(stream)
+        p.add_(1)
+        state["seq"] = nxt
+        nn = list(nxt)
+        for rr in rids:
+            nn[rr] += 1
+        mgr.plan_overlap(nn)
+        mgr.bg_submit()                         # next iteration's maps run during these kernels
+        return exposed
+
+    for _ in range(warm):
+        one_step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(N)] for _ in range(steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    exposed = []
+    s0.record(stream)
+    for i in range(steps):
+        exposed.append(one_step(ev[i]))
+    s1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms_total = s0.elapsed_time(s1)
+    dec_ms = [a.elapsed_time(b) for row in ev for a, b in row]
+    ms_step = max_over_ranks(ms_total / steps)
+    tokens_s = B / (ms_step / 1e3)
+    mean_ctx = ctx + warm + 1 + (steps - 1) / 2
+    dec_bytes = 2 * B * mean_ctx * hkv * d * 2 + 2 * B * hq * d * 2     # algorithmic, per launch
+    dec_us = statistics.mean(dec_ms) * 1e3
+    pk = peaks()
+    achieved = dec_bytes / (dec_us * 1e-6) / 1e9
+
+    # ---- e2e through the public API with host buffers (pinned) ----
+    qh = q.cpu().pin_memory()
+    knh, vnh = kn.cpu().pin_memory(), vn.cpu().pin_memory()
+    outh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    q_d, kn_d, vn_d = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn)
+    e2e_steps = max(3, min(steps, 20))
+
+    def e2e_step():
+        q_d.copy_(qh, non_blocking=True)
+        kn_d.copy_(knh, non_blocking=True)
+        vn_d.copy_(vnh, non_blocking=True)
+        one_step(None, q_d, kn_d, vn_d, out)
+        outh.copy_(out, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    s0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps)
+    h2d = qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2
+    d2h = outh.numel() * 2
+    st = mgr.driver_stats()
+    result = {
+        "metric": "decode_attn_tokens_per_s",
+        "value": tokens_s * 1.0,
+        "unit": "tokens/s",
+        "ms_per_step": ms_step,
+        "workload": wname,
+        "geometry": {"n_layers": N, "batch": B, "context": ctx, "hq": hq, "hkv": hkv, "d": d,
+                     "page_group": MB2},
+        "decode_kernel_us_mean": dec_us,
+        "decode_num_splits": splits,
+        "decode_hbm_gbs": achieved,
+        "decode_bytes_per_launch": dec_bytes,
+        "exposed_map_ms_per_iter": statistics.mean(exposed) * 1e3,
+        "exposed_map_ms_max": max(exposed) * 1e3,
+        "prefill_map_ms": prefill_map_s * 1e3,
+        "driver": {k: st[k] for k in ("real_maps", "real_set_access_calls", "real_map_wall_us",
+                                      "real_set_access_wall_us", "real_creates", "init_wall_us")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "kernel": "decode_kernel<128,4,false>", "peak_source": pk["source"]},
+        "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "clocks": clk,
+        "gpu_launches": steps * N * (2 + (1 if splits > 1 else 0)),
+    }
+    mgr.close()
+    return result
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+class CpuDecodeSample:
+    """Oracle port (fp32 torch on all host cores + the oracle allocator) on a bounded sample of
+    the decode step: `layers` of the geometry's layers are computed and scaled to the full step."""
+
+    def __init__(self, workload: str, world: int, layers: int = 1, batch_frac: int = 4):
+        import torch
+
+        from oracle.allocator import Geometry, OracleManager
+
+        g, ctx, _ = decode_geometry(workload, world)
+        self.g, self.ctx, self.layers = g, ctx, layers
+        self.cores = host_cores()
+        torch.set_num_threads(self.cores)
+        hkv, hq, d = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim
+        self.rows = max(1, g.max_batch // batch_frac)     # batch rows computed per sampled layer
+        B = self.rows
+        gen = torch.Generator().manual_seed(0)
+        self.k = torch.randn(B, ctx + 1, hkv, d, generator=gen, dtype=torch.bfloat16)
+        self.v = torch.randn(B, ctx + 1, hkv, d, generator=gen, dtype=torch.bfloat16)
+        self.q = torch.randn(B, hq, d, generator=gen, dtype=torch.bfloat16)
+        self.seq = torch.full((B,), ctx + 1, dtype=torch.int32)
+        B = g.max_batch
+        og = Geometry(g.n_layers, g.kv_heads_total, g.head_dim, g.bytes_per_elem, g.max_context, B,
+                      g.tp_degree)
+        pool = (g.max_context * g.per_token_layer_bytes // MB2 + 2) * 2 * g.n_layers * B * MB2
+        self.om = OracleManager(og, MB2, pool_bytes=pool)
+        self.rids = [self.om.alloc_reqid() for _ in range(B)]
+        self.sl = [0] * B
+        for r in self.rids:
+            self.sl[r] = ctx
+        self.om.step(self.sl)
+
+    def step(self) -> float:
+        """Seconds for one full decode iteration (sampled layers scaled to all layers)."""
+        from oracle.attention import decode_ref
+
+        t0 = time.perf_counter()
+        for r in self.rids:
+            self.sl[r] = min(self.sl[r] + 1, self.g.max_context)
+        self.om.step(self.sl)
+        t_alloc = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for _ in range(self.layers):
+            decode_ref(self.q, self.k, self.v, self.seq)
+        t_layer = (time.perf_counter() - t0) / self.layers * (self.g.max_batch / self.rows)
+        return t_alloc + t_layer * self.g.n_layers
+
+    def describe(self) -> str:
+        g = self.g
+        return (f"{self.layers} of {g.n_layers} layers x {self.rows} of {g.max_batch} batch rows per step "
+                f"(ctx={self.ctx + 1}, "
+                f"Hq={g.q_heads_per_worker}, Hkv={g.kv_heads_per_worker}, D={g.head_dim}; fp32 torch "
+                f"restatement oracle/attention.py on {self.cores} threads) scaled to the full step"
+                f" + oracle allocator step (1 thread); cpu: {cpu_model()}")
+
+
+def cpu_baseline(workload: str, world: int, steps: int = 2):
+    s = CpuDecodeSample(workload, world)
+    s.step()
+    t = statistics.mean(s.step() for _ in range(steps))
+    return {"value": s.g.max_batch / t, "unit": "tokens/s", "cores": s.cores, "kind": "port",
+            "sample": s.describe(), "ms_per_step": t * 1e3}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference path's CPU implementation (the oracle port, since the
+    reference itself is a hardware-free Python simulator with no attention code) on host cores."""
+    if rank != 0:
+        return None
+    s = CpuDecodeSample(args.workload, world)
+    for _ in range(args.warmup):
+        s.step()
+    times = [s.step() for _ in range(args.steps)]
+    ms = statistics.mean(times) * 1e3
+    _, _, wname = decode_geometry(args.workload, world)
+    val = s.g.max_batch / (ms / 1e3)
+    return {
+        "impl": "reference", "metric": "decode_attn_tokens_per_s", "value": val, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded randn K/V/Q)",
+        "config": {"workload": wname, "parallelism": f"tp{world}-kv-heads"},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": s.cores, "kind": "port",
+                         "sample": s.describe()},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ----------------------------------------------------------------------------- main
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["l8_decode", "y34_decode"], default="l8_decode")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return 0
+
+    res = bench_decode(args, world, rank, local)
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(args.workload, world)
+        line = {
+            "metric": res.pop("metric"), "value": res.pop("value"), "unit": res.pop("unit"),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res.pop("ms_per_step"), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn K/V/Q)",
+            "config": {"workload": res.pop("workload"), "parallelism": f"tp{world}-kv-heads",
+                       "l2": "inputs larger than L2 (1 GiB K+V per layer)", **res.pop("geometry")},
+            "roofline": res.pop("roofline"),
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": res.pop("e2e"), "clocks": res.pop("clocks"), "gpu_launches": res.pop("gpu_launches"),
+            **res,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
