@@ -14,6 +14,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <climits>
 #include <tuple>
 
 #include "internal.h"
@@ -512,8 +513,13 @@ void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void
                    int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
                    int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st) {
   check_view(v);
-  const CUtensorMap km = cached_map(ks, v.k_base, v.d, v.hkv, v.token_stride, v.slot_tokens, v.slot_stride, v.n_slots, kTile);
-  const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, v.slot_tokens, v.slot_stride, v.n_slots, kTile);
+  // Token extent = every row inside the slot stride, so a 64-row tile that starts below seqlen
+  // never takes TMA's out-of-bounds path (which faults on VMM-backed maps when the box
+  // straddles the token bound); those rows sit in the slot's last mapped page and are masked.
+  const int64_t rows = v.slot_stride / v.token_stride;
+  const int tokens = (int)std::max<int64_t>(v.slot_tokens, std::min<int64_t>(rows, INT32_MAX));
+  const CUtensorMap km = cached_map(ks, v.k_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
+  const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
   decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
                 scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st);
 }

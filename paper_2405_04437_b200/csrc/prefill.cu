@@ -1,15 +1,450 @@
-// tcgen05/TMEM causal prefill attention (placeholder until the tcgen05 kernel lands).
+// Causal prefill attention on 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// One CTA = one query head x 256 query rows, split into two 128-row tiles A and B that
+// ping-pong (FA4-style): while the softmax warpgroup of tile A turns S_A = Q_A·Kᵀ into P_A, the
+// tensor core works on tile B, and vice versa.  Everything that is a contraction runs on
+// tcgen05.mma with fp32 accumulators in TMEM:
+//   S_X(j)  = Q_X · K_jᵀ      A = Q (smem, K-major), B = K_j (smem, K-major), D = TMEM
+//   O_X    += P_X(j) · V_j    A = P (TMEM, bf16, aliased on S_X), B = V_j (smem, MN-major)
+// K/V tiles of 128 tokens are read straight out of the request's slot of the virtual KV cache
+// by TMA (4-D map over [D, Hkv, tokens, slots]; no block table).  The online softmax keeps one
+// query row per thread (TMEM lane), so row max / row sum need no shuffles; the O rescale is
+// lazy (only when the running max grows by more than 2^8).
+//
+// Warp roles (320 threads): warps 0-3 softmax A, 4-7 softmax B, 8 TMA producer, 9 MMA issuer
+// (+ TMEM allocator).  TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512) columns.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
 #include "internal.h"
+#include "ptx.cuh"
+#include "vattn.h"
 
 namespace vattn {
-void launch_prefill(KernelState*, int, const CacheView&, const void*, void*, int, int, int, int,
-                    float, bool, cudaStream_t) {
-  throw Fail(VATTN_UNSUPPORTED, "prefill kernel not built yet");
+namespace pf {
+
+constexpr int kBM = 128;           // query rows per tile
+constexpr int kBN = 128;           // keys per KV tile
+constexpr int kD = 128;            // head dim (Yi-6B / Llama / Yi-34B)
+constexpr int kStages = 2;         // K/V ring depth
+constexpr int kThreads = 320;
+constexpr int kHalf = kBN * 128;               // one 64-column half of a 128-row tile (16 KB)
+constexpr int kTileBytes = 2 * kHalf;          // 128 rows x 128 bf16 (32 KB)
+constexpr int kQOff = 0;                       // Q_A, Q_B
+constexpr int kKOff = 2 * kTileBytes;          // K stages
+constexpr int kVOff = kKOff + kStages * kTileBytes;
+constexpr int kBarOff = kVOff + kStages * kTileBytes;
+constexpr int kSmemBytes = kBarOff + 256 + 1024;
+constexpr float kRescaleThreshold = 8.0f;      // log2 domain: rescale O when max grows > 2^8
+
+struct Params {
+  __nv_bfloat16* out;      // [n_q, hq, D]
+  int n_q, hq, group, kv_len, slot, n_pairs;
+  int q_off;               // kv_len - n_q  (bottom-right causal alignment)
+  int causal;
+  float scale_log2;
+};
+
+// ---- tcgen05 wrappers -------------------------------------------------------------------
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SM100 UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (cute UMMA::SmemDescriptor)
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
+// instruction descriptor, kind::f16: bf16 x bf16 -> f32, M=128, N=128
+__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((kBN >> 3) << 17) |
+         ((kBM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   ptx::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+#define TMEM_LD32(taddr, r)                                                                            \
+  asm volatile(                                                                                        \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                       \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),           \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),    \
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),    \
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                            \
+      : "r"(taddr))
+
+#define TMEM_ST32(taddr, r)                                                                             \
+  asm volatile(                                                                                         \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),         \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),    \
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),  \
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) \
+      : "memory")
+
+#define TMEM_ST16(taddr, r)                                                                             \
+  asm volatile(                                                                                         \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
+      "%15,%16};" ::"r"(taddr),                                                                         \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])     \
+      : "memory")
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// number of KV tiles a query tile starting at row q0 needs
+__device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
+  if (q0 >= p.n_q) return 0;
+  int last_key = p.kv_len - 1;
+  if (p.causal) {
+    const int q_last = min(q0 + kBM, p.n_q) - 1;
+    last_key = min(last_key, q_last + p.q_off);
+  }
+  if (last_key < 0) return 0;
+  return last_key / kBN + 1;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+               const __grid_constant__ CUtensorMap vmap, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;            // [kStages]
+  uint64_t* v_full = bars + 3;            // [kStages]
+  uint64_t* kv_empty = bars + 5;          // [kStages]
+  uint64_t* s_full = bars + 7;            // [2] tiles A, B
+  uint64_t* p_full = bars + 9;            // [2]
+  uint64_t* o_final = bars + 11;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int pair = p.n_pairs - 1 - blockIdx.x;   // heaviest (latest) query rows first
+  const int head = blockIdx.y;
+  const int kvh = head / p.group;
+  const int q0A = pair * 2 * kBM, q0B = q0A + kBM;
+  const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
+  const int n_kv = max(nA, nB);
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&s_full[x], 1);
+      ptx::mbar_init(&p_full[x], kBM);
+      ptx::mbar_init(&o_final[x], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ===================== TMA producer =====================
+    if (lane == 0 && n_kv > 0) {
+      ptx::prefetch_tmap(&qmap);
+      ptx::prefetch_tmap(&kmap);
+      ptx::prefetch_tmap(&vmap);
+      ptx::mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ptx::tma_load_3d(smem + kQOff + h * kHalf, &qmap, q_full, h * 64, head, q0A);
+        ptx::tma_load_3d(smem + kQOff + kTileBytes + h * kHalf, &qmap, q_full, h * 64, head, q0B);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const int s = j % kStages;
+        if (j >= kStages) ptx::mbar_wait(&kv_empty[s], ((j / kStages) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(&k_full[s], kTileBytes);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          ptx::tma_load_3d(smem + kKOff + s * kTileBytes + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
+                           j * kBN);
+        ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          ptx::tma_load_3d(smem + kVOff + s * kTileBytes + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
+                           j * kBN);
+      }
+    }
+  } else if (warp == 9) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0 && n_kv > 0) {
+      const uint32_t id_qk = idesc(false), id_pv = idesc(true);
+      const uint32_t sbase = ptx::smem_u32(smem);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const int nX[2] = {nA, nB};
+      auto issue_s = [&](int x, int j) {   // S_x(j) = Q_x K_j^T
+        const int s = j % kStages;
+        const uint32_t qa = sbase + kQOff + x * kTileBytes;
+        const uint32_t kb = sbase + kKOff + s * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+          mma_ss(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
+        }
+        mma_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
+        const int s = j % kStages;
+        const uint32_t vb = sbase + kVOff + s * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
+      };
+      ptx::mbar_wait(q_full, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int s = j % kStages;
+        ptx::mbar_wait(&k_full[s], (j / kStages) & 1);
+        fence_after();
+        if (j == 0) {
+          for (int x = 0; x < 2; ++x)
+            if (nX[x] > 0) issue_s(x, 0);
+        }
+        ptx::mbar_wait(&v_full[s], (j / kStages) & 1);
+        fence_after();
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nX[x]) continue;
+          ptx::mbar_wait(&p_full[x], j & 1);
+          fence_after();
+          issue_pv(x, j);
+          if (j + 1 == nX[x]) {
+            mma_commit(&o_final[x]);
+          } else {
+            // S_x(j+1) needs K_{j+1}
+            const int s1 = (j + 1) % kStages;
+            ptx::mbar_wait(&k_full[s1], ((j + 1) / kStages) & 1);
+            fence_after();
+            issue_s(x, j + 1);
+          }
+        }
+        mma_commit(&kv_empty[s]);   // K_j / V_j fully consumed once these MMAs retire
+      }
+    }
+  } else {
+    // ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
+    const int x = warp / 4;
+    const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
+    const int q0 = x == 0 ? q0A : q0B;
+    const int n = x == 0 ? nA : nB;
+    const int qpos = q0 + row;
+    const uint32_t lane_base = tmem + (((warp % 4) * 32) << 16);
+    const uint32_t tS = lane_base + x * 128;
+    const uint32_t tO = lane_base + 256 + x * 128;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n; ++j) {
+      ptx::mbar_wait(&s_full[x], j & 1);
+      fence_after();
+      // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap)
+      const int k0 = j * kBN;
+      const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
+      const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        uint32_t r[32];
+        TMEM_LD32(tS + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float v = (c0 + c < lim) ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, v);
+        }
+      }
+      // lazy rescale: keep the stale max unless it grows by more than 2^8 (warp-uniform decision)
+      const bool grow = (m_run == -INFINITY) ? (mx > -INFINITY) : (mx > m_run + kRescaleThreshold);
+      if (__any_sync(0xffffffffu, grow)) {
+        const float m_new = fmaxf(m_run, mx);
+        const float f = (m_run == -INFINITY) ? 0.f : ptx::fast_exp2(m_run - m_new);
+        l_run *= f;
+        if (j > 0 && __any_sync(0xffffffffu, f != 1.f)) {
+          // O_x(j-1) is complete: S_x(j) was issued after PV_x(j-1) and has retired
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t o[32];
+            TMEM_LD32(tO + c0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            TMEM_ST32(tO + c0, o);
+          }
+          tmem_wait_st();
+        }
+        m_run = m_new;
+      }
+      // pass 2: P = exp2(S*scale - m) -> bf16 into TMEM over the S columns already consumed
+      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+      float lsum = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        uint32_t r[32], pk[16];
+        TMEM_LD32(tS + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float p0 = (c0 + c < lim) ? ptx::fast_exp2(fmaf(__uint_as_float(r[c]), p.scale_log2, neg_m)) : 0.f;
+          const float p1 = (c0 + c + 1 < lim) ? ptx::fast_exp2(fmaf(__uint_as_float(r[c + 1]), p.scale_log2, neg_m)) : 0.f;
+          lsum += p0 + p1;
+          pk[c / 2] = ptx::pack_bf16(p0, p1);
+        }
+        TMEM_ST16(tS + c0 / 2, pk);
+      }
+      l_run += lsum;
+      tmem_wait_st();
+      fence_before();
+      ptx::mbar_arrive(&p_full[x]);
+    }
+    // ---- epilogue: O / l -> bf16 -> global ----
+    if (n > 0) {
+      ptx::mbar_wait(&o_final[x], 0);
+      fence_after();
+    }
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * kD;
+    const bool live = qpos < p.n_q;
+#pragma unroll
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      uint32_t o[32];
+      if (n > 0) {
+        TMEM_LD32(tO + c0, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0u;
+      }
+      if (live) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          uint4 v;
+          v.x = ptx::pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
+          v.y = ptx::pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
+          v.z = ptx::pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
+          v.w = ptx::pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c0 + c) = v;
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+}  // namespace pf
+
+static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                            const cuuint32_t* box) {
+  CUtensorMap m;
+  const char* promo_env = getenv("VATTN_PF_L2PROMO");
+  const CUtensorMapL2promotion promo = (promo_env && promo_env[0] == '0') ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  check_cu(driver().TensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides,
+                                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                         CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled(prefill)");
+  return m;
+}
+
+void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* out, int n_q, int hq,
+                    int slot, int kv_len, float scale, bool causal, cudaStream_t st) {
+  if (v.d != pf::kD) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 128");
+  if (hq % v.hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
+  if (slot < 0 || slot >= v.n_slots) throw Fail(VATTN_VALUE_ERROR, "slot out of range");
+  if (kv_len < 0 || kv_len > v.slot_tokens) throw Fail(VATTN_VALUE_ERROR, "kv_len out of range");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) % 16)
+    throw Fail(VATTN_UNSUPPORTED, "q/out must be 16-byte aligned");
+  if (n_q <= 0) return;
+  // Per-call maps: the K/V token extent is exactly kv_len, so rows past it are zero-filled by
+  // TMA instead of being read from (possibly stale or unmapped) pages.
+  const int kvl = std::max(kv_len, 1);
+  cuuint64_t qd[3] = {(cuuint64_t)pf::kD, (cuuint64_t)hq, (cuuint64_t)n_q};
+  cuuint64_t qs[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)hq * pf::kD * 2};
+  cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
+  const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  // 3-D map rooted at the request's slot: [D, Hkv, kv_len] (the slot index is folded into the base)
+  cuuint64_t kd[3] = {(cuuint64_t)pf::kD, (cuuint64_t)v.hkv, (cuuint64_t)kvl};
+  cuuint64_t ks[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)v.token_stride};
+  cuuint32_t kb[3] = {64, 1, (cuuint32_t)pf::kBN};
+  const uint64_t slot_off = (uint64_t)slot * (uint64_t)v.slot_stride;
+  const CUtensorMap kmap = make_map(reinterpret_cast<void*>(v.k_base + slot_off), 3, kd, ks, kb);
+  const CUtensorMap vmap = make_map(reinterpret_cast<void*>(v.v_base + slot_off), 3, kd, ks, kb);
+  pf::Params p;
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.n_q = n_q;
+  p.hq = hq;
+  p.group = hq / v.hkv;
+  p.kv_len = kv_len;
+  p.slot = slot;
+  p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
+  p.q_off = kv_len - n_q;
+  p.causal = causal ? 1 : 0;
+  if (scale <= 0.f) scale = 1.f / sqrtf((float)pf::kD);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  static bool attr = false;
+  if (!attr) {
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  pf::kSmemBytes),
+             "prefill smem attribute");
+    attr = true;
+  }
+  dim3 grid(p.n_pairs, hq);
+  pf::prefill_kernel<<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  check_rt(cudaGetLastError(), "prefill launch");
+}
+
 }  // namespace vattn
 
-extern "C" vattn_status vattn_prefill_raw(const vattn_cache_desc*, const void*, void*, int32_t,
-                                          int32_t, int32_t, int32_t, float, int32_t, void*) {
-  vattn::set_last_error("prefill kernel not built yet");
-  return VATTN_UNSUPPORTED;
+extern "C" vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
+                                          int32_t hq, int32_t slot, int32_t kv_len, float scale,
+                                          int32_t causal, void* stream) {
+  try {
+    vattn::launch_prefill(nullptr, -1, vattn::view_from_desc(c), q, out, n_q, hq, slot, kv_len, scale,
+                          causal != 0, (cudaStream_t)stream);
+    return VATTN_OK;
+  } catch (const vattn::Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
 }
