@@ -125,6 +125,23 @@ typedef struct vattn_bg_result {
 #define VATTN_BG_EXECUTE_PLAN 1u
 #define VATTN_BG_EAGER 2u
 #define VATTN_BG_RECLAIM 4u
+/* execute_plan submitted ahead of the next admission: record per-slot credits so that
+ * alloc_reqid ranks slots as if the plan ran after it (reference order, simulator.py:395-418) */
+#define VATTN_BG_CREDIT 8u
+/* vattn_iteration_step: defer eager/reclaim past step onto the background thread when the
+ * result is provably identical */
+#define VATTN_ITER_DEFER 16u
+
+typedef struct vattn_iteration_result {
+  int32_t ok;                  /* step ok (preempt on 0) */
+  int32_t deferred;            /* eager/reclaim were queued behind step */
+  double sync_us;              /* modelled µs of step */
+  double eager_us, reclaim_us; /* modelled µs of eager/reclaim when run synchronously */
+  int64_t reclaimed_groups;
+  double bg_wait_us;           /* joining the previous background window */
+  double sync_bg_wall_us;      /* wall time of synchronous eager+reclaim */
+  double wall_us;              /* wall time of the whole call = exposed allocation time */
+} vattn_iteration_result;
 
 /* ---- lifecycle --------------------------------------------------------------------- */
 const char* vattn_last_error(void);
@@ -136,6 +153,11 @@ vattn_status vattn_destroy(vattn_t* h);
 vattn_status vattn_alloc_reqid(vattn_t* h, int32_t* req_id);
 vattn_status vattn_free_reqid(vattn_t* h, int32_t req_id);
 vattn_status vattn_step(vattn_t* h, const int64_t* seq_lens, int32_t n, vattn_step_result* out);
+/* One serving iteration's allocation work in the reference order (simulator.py:414-426):
+ * [join background] -> eager_prepare/reclaim per flags (sync, or deferred behind step when
+ * VATTN_ITER_DEFER and provably equivalent) -> step. */
+vattn_status vattn_iteration_step(vattn_t* h, const int64_t* seq_lens, int32_t n, uint32_t flags,
+                                  int64_t eager_k, vattn_iteration_result* out);
 vattn_status vattn_plan_overlap(vattn_t* h, const int64_t* next_seq_lens, int32_t n,
                                 int64_t* n_entries);
 vattn_status vattn_plan_fetch(vattn_t* h, int64_t* triples, int64_t cap_entries);
@@ -167,6 +189,11 @@ vattn_status vattn_buffer_mappings(vattn_t* h, int32_t buffer_id, int64_t* offse
 /* drain the event log: triples (0=map|1=unmap, buffer_id, offset) */
 vattn_status vattn_events(vattn_t* h, int64_t* triples, int64_t cap_entries, int64_t* n);
 vattn_status vattn_buffer_base(vattn_t* h, int32_t buffer_id, uint64_t* dptr);
+
+/* Table 2 analog measured on this device: mean µs per call at `page_bytes` (out[8]: reserve,
+ * create, map, set_access, unmap, release, address_free, set_access-per-page batched by `run`). */
+vattn_status vattn_vmm_microbench(int32_t device, int64_t page_bytes, int32_t n_pages, int32_t run,
+                                  double* out);
 
 /* ---- kernels (bf16 K/V/Q/O; layouts in DESIGN.md §3) --------------------------------- */
 /* Write k_new/v_new [batch, n_new, Hkv, D] at rows cache_seqlens[b] + i of slot

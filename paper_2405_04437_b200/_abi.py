@@ -66,7 +66,13 @@ class CacheDesc(C.Structure):
                 ("n_kv_heads", c_i32), ("head_dim", c_i32)]
 
 
-BG_EXECUTE_PLAN, BG_EAGER, BG_RECLAIM = 1, 2, 4
+class IterationResult(C.Structure):
+    _fields_ = [("ok", c_i32), ("deferred", c_i32), ("sync_us", c_f64), ("eager_us", c_f64),
+                ("reclaim_us", c_f64), ("reclaimed_groups", c_i64), ("bg_wait_us", c_f64),
+                ("sync_bg_wall_us", c_f64), ("wall_us", c_f64)]
+
+
+BG_EXECUTE_PLAN, BG_EAGER, BG_RECLAIM, BG_CREDIT, ITER_DEFER = 1, 2, 4, 8, 16
 
 # every symbol include/vattn.h declares, with its ctypes signature
 SIGNATURES = {
@@ -77,6 +83,7 @@ SIGNATURES = {
     "vattn_alloc_reqid": (c_i32, [c_vp, P_i32]),
     "vattn_free_reqid": (c_i32, [c_vp, c_i32]),
     "vattn_step": (c_i32, [c_vp, P_i64, c_i32, C.POINTER(StepResultC)]),
+    "vattn_iteration_step": (c_i32, [c_vp, P_i64, c_i32, c_u32, c_i64, C.POINTER(IterationResult)]),
     "vattn_plan_overlap": (c_i32, [c_vp, P_i64, c_i32, P_i64]),
     "vattn_plan_fetch": (c_i32, [c_vp, P_i64, c_i64]),
     "vattn_execute_plan": (c_i32, [c_vp, P_i64, c_i64, P_f64]),
@@ -104,6 +111,7 @@ SIGNATURES = {
                                   c_f32, c_i32, c_vp]),
     "vattn_decode_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp,
                                    c_i32, c_i32, c_vp, c_f32, c_i32, c_vp, c_i64, c_vp]),
+    "vattn_vmm_microbench": (c_i32, [c_i32, c_i64, c_i32, c_i32, C.POINTER(c_f64)]),
     "vattn_decode_num_splits": (c_i32, [c_i32, c_i32, c_i32]),
     "vattn_decode_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
 }

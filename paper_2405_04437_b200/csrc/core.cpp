@@ -175,6 +175,7 @@ struct BgJob {
   std::vector<int64_t> plan;
   uint32_t flags = 0;
   int64_t eager_k = -1;
+  uint64_t seq = 0;
 };
 
 class Manager {
@@ -195,7 +196,10 @@ class Manager {
   // background thread
   void bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t eager_k);
   void bg_wait(vattn_bg_result* out);
-  double join_bg();
+  double join_bg();                 // wait until every submitted job retired
+  double join_noncommuting();       // wait for queued eager/reclaim jobs only
+  bool deferral_safe(const int64_t* seq, int32_t n, int64_t eager_k) const;
+  void reset_credits() { std::fill(plan_credit_.begin(), plan_credit_.end(), 0); }
 
   void mark_use(cudaStream_t st);
   void begin_call() { fenced_ = false; }
@@ -299,11 +303,15 @@ class Manager {
   std::thread bg_thread_;
   std::mutex bg_mu_;
   std::condition_variable bg_cv_;
-  bool bg_has_job_ = false, bg_busy_ = false, bg_stop_ = false, bg_result_pending_ = false;
-  BgJob bg_job_;
-  vattn_bg_result bg_res_{};
+  std::deque<BgJob> bg_queue_;
+  uint64_t bg_submitted_ = 0, bg_completed_ = 0, bg_last_noncommuting_ = 0;
+  bool bg_stop_ = false;
+  vattn_bg_result bg_res_{};        // accumulated since the last bg_wait
   vattn_status bg_status_ = VATTN_OK;
   std::string bg_error_;
+  // groups mapped per slot by a plan executed ahead of the reference's position (credit mode)
+  std::vector<int64_t> plan_credit_;
+  bool credit_mode_ = false;
 };
 
 // ---- construction (manager.py:85-130) --------------------------------------------------
@@ -418,6 +426,7 @@ Manager::Manager(const vattn_config& c) {
   const int64_t pre = (int64_t)(c.pre_create_fraction * (double)c.pool_bytes) / t_;  // :124-125
   init_us_ += dev_precreate(pre);
   slots_.resize(c.max_batch);
+  plan_credit_.assign(c.max_batch, 0);
   init_wall_us_ = now_us() - t0;
 
   bg_thread_ = std::thread([this] { bg_loop(); });
@@ -426,7 +435,7 @@ Manager::Manager(const vattn_config& c) {
 Manager::~Manager() {
   {
     std::unique_lock<std::mutex> lk(bg_mu_);
-    bg_cv_.wait(lk, [&] { return !bg_busy_; });
+    bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
     bg_stop_ = true;
   }
   bg_cv_.notify_all();
@@ -650,13 +659,22 @@ int32_t Manager::best_inactive() const {  // max over inactive of (mapped_groups
   return best;
 }
 
+// alloc_reqid's choice as the reference makes it: admission precedes execute_plan
+// (simulator.py:395-418), so a plan executed early (during the previous iteration's compute)
+// must not influence which inactive slot is reused.  Credits undo its effect on the ranking.
+static inline int64_t ranked(const Slot& s, int64_t credit) { return s.mapped_groups - credit; }
+
 int32_t Manager::alloc_reqid() {  // manager.py:163-178
   int32_t rid;
   if (eager_slot_ >= 0 && !slots_[eager_slot_].active) {
     rid = (int32_t)eager_slot_;
     eager_slot_ = -1;
   } else {
-    rid = best_inactive();
+    rid = -1;
+    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+      if (slots_[r].active) continue;
+      if (rid < 0 || ranked(slots_[r], plan_credit_[r]) > ranked(slots_[rid], plan_credit_[rid])) rid = r;
+    }
     if (rid < 0)
       throw Fail(VATTN_BATCH_FULL, "all " + std::to_string(slots_.size()) + " request slots active");
   }
@@ -822,6 +840,7 @@ double Manager::execute_plan(const int64_t* trip, int64_t n) {  // manager.py:31
         return us;
       }
       s.mapped_groups += 1;
+      if (credit_mode_) plan_credit_[rid] += 1;
     }
     done.insert(key);
   }
@@ -859,16 +878,19 @@ std::pair<int64_t, double> Manager::reclaim() {  // manager.py:363-372
 }
 
 // ---- background thread (simulator.py:199-203 on a real thread) ----------------------------
+// A FIFO of jobs; each runs execute_plan -> eager_prepare -> reclaim per its flags.  API calls
+// join the queue before touching state, except free_reqid, which only waits for queued
+// eager/reclaim jobs (execute_plan never reads the fields free_reqid writes, and vice versa).
 void Manager::bg_loop() {
   bool ctx_set = false;
   for (;;) {
     BgJob job;
     {
       std::unique_lock<std::mutex> lk(bg_mu_);
-      bg_cv_.wait(lk, [&] { return bg_has_job_ || bg_stop_; });
-      if (bg_stop_ && !bg_has_job_) return;
-      job = std::move(bg_job_);
-      bg_has_job_ = false;
+      bg_cv_.wait(lk, [&] { return !bg_queue_.empty() || bg_stop_; });
+      if (bg_queue_.empty()) return;
+      job = std::move(bg_queue_.front());
+      bg_queue_.pop_front();
     }
     vattn_bg_result res{};
     vattn_status st = VATTN_OK;
@@ -880,8 +902,11 @@ void Manager::bg_loop() {
         ctx_set = true;
       }
       fenced_ = false;
-      if (job.flags & VATTN_BG_EXECUTE_PLAN)
+      if (job.flags & VATTN_BG_EXECUTE_PLAN) {
+        credit_mode_ = (job.flags & VATTN_BG_CREDIT) != 0;
         res.plan_us = execute_plan(job.plan.data(), (int64_t)job.plan.size() / 3);
+        credit_mode_ = false;
+      }
       if (job.flags & VATTN_BG_EAGER) res.eager_us = eager_prepare(job.eager_k);
       if (job.flags & VATTN_BG_RECLAIM) {
         auto r = reclaim();
@@ -899,11 +924,16 @@ void Manager::bg_loop() {
     res.bg_wall_us = now_us() - t0;
     {
       std::lock_guard<std::mutex> lk(bg_mu_);
-      bg_res_ = res;
-      bg_status_ = st;
-      bg_error_ = err;
-      bg_busy_ = false;
-      bg_result_pending_ = true;
+      bg_res_.plan_us += res.plan_us;
+      bg_res_.eager_us += res.eager_us;
+      bg_res_.reclaim_us += res.reclaim_us;
+      bg_res_.reclaimed_groups += res.reclaimed_groups;
+      bg_res_.bg_wall_us += res.bg_wall_us;
+      if (st != VATTN_OK && bg_status_ == VATTN_OK) {
+        bg_status_ = st;
+        bg_error_ = err;
+      }
+      bg_completed_ = job.seq;
     }
     bg_cv_.notify_all();
   }
@@ -911,35 +941,76 @@ void Manager::bg_loop() {
 
 double Manager::join_bg() {
   std::unique_lock<std::mutex> lk(bg_mu_);
-  if (!bg_busy_) return 0.0;
+  if (bg_completed_ == bg_submitted_) return 0.0;
   const double t0 = now_us();
-  bg_cv_.wait(lk, [&] { return !bg_busy_; });
+  bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
+  return now_us() - t0;
+}
+
+double Manager::join_noncommuting() {
+  std::unique_lock<std::mutex> lk(bg_mu_);
+  if (bg_completed_ >= bg_last_noncommuting_) return 0.0;
+  const double t0 = now_us();
+  bg_cv_.wait(lk, [&] { return bg_completed_ >= bg_last_noncommuting_; });
   return now_us() - t0;
 }
 
 void Manager::bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t eager_k) {
-  join_bg();
   std::lock_guard<std::mutex> lk(bg_mu_);
-  bg_job_ = BgJob{};
-  if (trip) bg_job_.plan.assign(trip, trip + 3 * n);
-  else bg_job_.plan = last_plan_;
-  bg_job_.flags = flags;
-  bg_job_.eager_k = eager_k;
-  bg_has_job_ = true;
-  bg_busy_ = true;
-  bg_result_pending_ = false;
+  BgJob job;
+  if (trip) job.plan.assign(trip, trip + 3 * n);
+  else if (flags & VATTN_BG_EXECUTE_PLAN) job.plan = last_plan_;
+  job.flags = flags;
+  job.eager_k = eager_k;
+  job.seq = ++bg_submitted_;
+  if (flags & (VATTN_BG_EAGER | VATTN_BG_RECLAIM)) bg_last_noncommuting_ = job.seq;
+  bg_queue_.push_back(std::move(job));
   bg_cv_.notify_all();
 }
 
 void Manager::bg_wait(vattn_bg_result* out) {
   std::unique_lock<std::mutex> lk(bg_mu_);
   const double t0 = now_us();
-  bg_cv_.wait(lk, [&] { return !bg_busy_; });
+  bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
   const double waited = now_us() - t0;
-  if (!bg_result_pending_) throw Fail(VATTN_BAD_STATE, "vattn_bg_wait without a submitted job");
-  bg_result_pending_ = false;
-  if (out) { *out = bg_res_; out->waited_us = waited; }
-  if (bg_status_ != VATTN_OK) throw Fail(bg_status_, "background job failed: " + bg_error_);
+  vattn_bg_result r = bg_res_;
+  r.waited_us = waited;
+  bg_res_ = vattn_bg_result{};
+  const vattn_status st = bg_status_;
+  const std::string err = bg_error_;
+  bg_status_ = VATTN_OK;
+  bg_error_.clear();
+  if (out) *out = r;
+  if (st != VATTN_OK) throw Fail(st, "background job failed: " + err);
+}
+
+// Deferring eager_prepare/reclaim past step (so they run during compute) yields the same state
+// as the reference order (eager -> reclaim -> step, simulator.py:414-426) when nothing can hit
+// the pool floor or run dry: with A = available bytes, E eager groups and S step groups still
+// to map, A - (E + S)·G >= floor keeps every eager floor check passing and reclaim a no-op in
+// both orders, and enough cached/pre-created handles keep the modelled create charges in place.
+bool Manager::deferral_safe(const int64_t* seq, int32_t n, int64_t eager_k) const {
+  if (n != (int32_t)slots_.size()) return false;
+  int64_t k = eager_k < 0 ? eager_groups_ : eager_k;
+  int64_t E = 0;
+  if (k > 0) {
+    k = std::min(k, groups_per_slot_);
+    const bool done = eager_slot_ >= 0 && slots_[eager_slot_].mapped_groups >= k;
+    if (!done) {
+      const int32_t x = best_inactive();
+      if (x >= 0) E = std::max<int64_t>(0, k - slots_[x].mapped_groups);
+    }
+  }
+  int64_t S = 0;
+  for (int32_t r = 0; r < n; ++r) {
+    if (!slots_[r].active) continue;
+    if (seq[r] < 0 || seq[r] > max_context_) return false;
+    S += std::max<int64_t>(0, groups_required(seq[r]) - slots_[r].mapped_groups);
+  }
+  const int64_t G = buffer_count_ * t_;
+  if (available() - (E + S) * G < reclaim_floor()) return false;
+  const int64_t free_handles = (int64_t)handle_cache_.size() + precreated_;
+  return free_handles >= (E + S) * buffer_count_;
 }
 
 // ---- introspection ------------------------------------------------------------------------------
@@ -1137,7 +1208,13 @@ vattn_status vattn_alloc_reqid(vattn_t* h, int32_t* rid) {
 }
 
 vattn_status vattn_free_reqid(vattn_t* h, int32_t rid) {
-  return api_call(h, [&](Manager& m) { m.free_reqid(rid); });
+  // free_reqid commutes with a queued execute_plan (disjoint fields), so it waits only for
+  // queued eager/reclaim jobs, which read `active` (manager.py:232-236, :347-349).
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    h->m->join_noncommuting();
+    h->m->free_reqid(rid);
+  });
 }
 
 vattn_status vattn_step(vattn_t* h, const int64_t* seq, int32_t n, vattn_step_result* out) {
@@ -1149,6 +1226,7 @@ vattn_status vattn_step(vattn_t* h, const int64_t* seq, int32_t n, vattn_step_re
     double us = 0.0;
     bool ok;
     try {
+      h->m->reset_credits();
       ok = h->m->step(seq, n, &us);
     } catch (...) {
       try { h->m->end_call(); } catch (...) {}
@@ -1161,6 +1239,46 @@ vattn_status vattn_step(vattn_t* h, const int64_t* seq, int32_t n, vattn_step_re
       out->bg_wait_us = waited;
       out->wall_us = vattn::now_us() - t0;
     }
+  });
+}
+
+vattn_status vattn_iteration_step(vattn_t* h, const int64_t* seq, int32_t n, uint32_t flags,
+                                  int64_t eager_k, vattn_iteration_result* out) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    Manager& m = *h->m;
+    const double t0 = vattn::now_us();
+    vattn_iteration_result r{};
+    r.bg_wait_us = m.join_bg();
+    m.begin_call();
+    try {
+      const bool want = (flags & (VATTN_BG_EAGER | VATTN_BG_RECLAIM)) != 0;
+      const bool defer = want && (flags & VATTN_ITER_DEFER) && m.deferral_safe(seq, n, eager_k);
+      if (want && !defer) {
+        const double t1 = vattn::now_us();
+        if (flags & VATTN_BG_EAGER) r.eager_us = m.eager_prepare(eager_k);
+        if (flags & VATTN_BG_RECLAIM) {
+          auto rc = m.reclaim();
+          r.reclaimed_groups = rc.first;
+          r.reclaim_us = rc.second;
+        }
+        r.sync_bg_wall_us = vattn::now_us() - t1;
+      }
+      m.reset_credits();
+      double us = 0.0;
+      r.ok = m.step(seq, n, &us) ? 1 : 0;
+      r.sync_us = us;
+      m.end_call();
+      if (defer) {
+        m.bg_submit(nullptr, 0, flags & (VATTN_BG_EAGER | VATTN_BG_RECLAIM), eager_k);
+        r.deferred = 1;
+      }
+    } catch (...) {
+      try { m.end_call(); } catch (...) {}
+      throw;
+    }
+    r.wall_us = vattn::now_us() - t0;
+    if (out) *out = r;
   });
 }
 
@@ -1308,6 +1426,59 @@ vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, 
     vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
                           causal != 0, (cudaStream_t)stream);
     h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
+
+// Table 2 analog on the real driver: mean µs per call of every cuMem* API at `page_bytes`,
+// plus cuMemSetAccess over runs of `run` contiguous pages (one call per run).
+// out[0..7] = reserve, create, map, set_access(1 page), unmap, release, address_free,
+//             set_access per page when batched over `run` pages.
+vattn_status vattn_vmm_microbench(int32_t device, int64_t page_bytes, int32_t n_pages, int32_t run,
+                                  double* out) {
+  return guard([&] {
+    using vattn::check_cu;
+    const vattn::Driver& d = vattn::driver();
+    vattn::check_rt(cudaSetDevice(device), "cudaSetDevice");
+    vattn::check_rt(cudaFree(nullptr), "context init");
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (n_pages < 1 || run < 1 || n_pages % run) throw Fail(VATTN_VALUE_ERROR, "n_pages must be a multiple of run");
+    const size_t pg = (size_t)page_bytes, total = pg * (size_t)n_pages;
+    std::vector<CUmemGenericAllocationHandle> h((size_t)n_pages);
+    double t0 = vattn::now_us();
+    CUdeviceptr va = 0;
+    check_cu(d.MemAddressReserve(&va, total, pg, 0, 0), "cuMemAddressReserve");
+    out[0] = vattn::now_us() - t0;
+    t0 = vattn::now_us();
+    for (auto& x : h) check_cu(d.MemCreate(&x, pg, &prop, 0), "cuMemCreate");
+    out[1] = (vattn::now_us() - t0) / n_pages;
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemMap(va + i * pg, pg, 0, h[i], 0), "cuMemMap");
+    out[2] = (vattn::now_us() - t0) / n_pages;
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemSetAccess(va + i * pg, pg, &acc, 1), "cuMemSetAccess");
+    out[3] = (vattn::now_us() - t0) / n_pages;
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemUnmap(va + i * pg, pg), "cuMemUnmap");
+    out[4] = (vattn::now_us() - t0) / n_pages;
+    // batched access: map again, one cuMemSetAccess per run of `run` pages
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemMap(va + i * pg, pg, 0, h[i], 0), "cuMemMap");
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; i += run) check_cu(d.MemSetAccess(va + i * pg, pg * run, &acc, 1), "cuMemSetAccess(run)");
+    out[7] = (vattn::now_us() - t0) / n_pages;
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemUnmap(va + i * pg, pg), "cuMemUnmap");
+    t0 = vattn::now_us();
+    for (auto& x : h) check_cu(d.MemRelease(x), "cuMemRelease");
+    out[5] = (vattn::now_us() - t0) / n_pages;
+    t0 = vattn::now_us();
+    check_cu(d.MemAddressFree(va, total), "cuMemAddressFree");
+    out[6] = vattn::now_us() - t0;
   });
 }
 

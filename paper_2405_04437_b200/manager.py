@@ -84,6 +84,19 @@ class BackgroundResult:
     waited_us: float
 
 
+@dataclass
+class IterationResult:
+    ok: bool
+    deferred: bool
+    sync_us: float
+    eager_us: float
+    reclaim_us: float
+    reclaimed_groups: int
+    bg_wait_us: float
+    sync_bg_wall_us: float
+    wall_us: float
+
+
 class _Pool:
     """PhysicalPool view (vmm.py:102-127)."""
 
@@ -350,16 +363,32 @@ class KVCacheManager:
 
     # -- the background mapping thread (§6.1.1/§6.1.2; simulator.py:199-203 order) ----------------
     def bg_submit(self, plan=None, *, execute_plan: bool = True, eager: bool = False,
-                  reclaim: bool = False, eager_k: int | None = None) -> None:
-        """Start execute_plan → eager_prepare → reclaim on the background thread.  Every other
-        call joins the window first, so state is never mutated concurrently."""
+                  reclaim: bool = False, eager_k: int | None = None, credit: bool = False) -> None:
+        """Queue execute_plan → eager_prepare → reclaim on the background thread.  Every other
+        call joins the queue first (free_reqid only waits for queued eager/reclaim), so state is
+        never mutated concurrently.  credit=True: the plan runs ahead of the next admission;
+        alloc_reqid then ranks slots as if it had run after (the reference's order)."""
         flags = ((_abi.BG_EXECUTE_PLAN if execute_plan else 0) | (_abi.BG_EAGER if eager else 0)
-                 | (_abi.BG_RECLAIM if reclaim else 0))
+                 | (_abi.BG_RECLAIM if reclaim else 0) | (_abi.BG_CREDIT if credit else 0))
         if plan is None or plan is self._last_plan:
             arr, n = None, 0
         else:
             arr, n = self._plan_array(plan), len(plan)
         check(lib().vattn_bg_submit(self._h, arr, n, flags, -1 if eager_k is None else int(eager_k)))
+
+    def iteration_step(self, seq_lens, *, eager: bool = True, reclaim: bool = True, defer: bool = True,
+                       eager_k: int | None = None) -> "IterationResult":
+        """One serving iteration's allocation work in the reference order (simulator.py:414-426):
+        join the background queue, eager_prepare + reclaim (deferred behind step onto the
+        background thread when provably equivalent), then step."""
+        buf = self._fill_seq(seq_lens)
+        flags = ((_abi.BG_EAGER if eager else 0) | (_abi.BG_RECLAIM if reclaim else 0)
+                 | (_abi.ITER_DEFER if defer else 0))
+        r = _abi.IterationResult()
+        check(lib().vattn_iteration_step(self._h, buf, self._n, flags, -1 if eager_k is None else int(eager_k),
+                                         C.byref(r)))
+        return IterationResult(bool(r.ok), bool(r.deferred), r.sync_us, r.eager_us, r.reclaim_us,
+                               r.reclaimed_groups, r.bg_wait_us, r.sync_bg_wall_us, r.wall_us)
 
     def bg_wait(self) -> BackgroundResult:
         r = _abi.BgResult()

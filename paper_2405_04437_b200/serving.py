@@ -1,0 +1,372 @@
+"""Algorithm-1 serving loop over the vAttention allocator.
+
+The event order is the reference simulator's (kvsim/simulator.py:333-504): admit arrivals ->
+background allocation work (overlapped mode: execute_plan -> eager_prepare -> reclaim) -> step
+(preempting the newest request on failure) -> compute -> plan the next iteration's decode growth
+-> retire finished requests.  Two clocks:
+
+* ``clock="model"`` advances time with the reference's linear IterationModel and the modelled
+  Table-2 latencies, so the per-iteration records equal ``kvsim.simulator.run`` exactly
+  (tests/test_serving_parity.py) while the allocator calls go through the C++ core;
+* ``clock="wall"`` runs the real sm_100a kernels per iteration (KV append + prefill attention
+  for new requests, KV append + decode attention for the batch) on the real cuMem* backend and
+  measures, per iteration, the host time the allocator keeps off the GPU ("exposed map ms").
+
+Overlapped mode runs the planned maps on the background thread *during* the iteration's
+kernels (submitted right after launch, with plan credits so admission ranks slots exactly as
+the reference does), and queues eager_prepare/reclaim behind step whenever that provably
+yields the same state (vattn_iteration_step, VATTN_ITER_DEFER).
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+from .errors import BatchFullError
+from .manager import KVCacheManager, ManagerConfig
+
+MB2 = 2 * 1024 * 1024
+
+
+class SimulationAborted(RuntimeError):
+    """No forward progress within the preemption cap (simulator.py:40-41)."""
+
+
+@dataclass(frozen=True)
+class IterationModel:
+    """Linear compute proxy of the reference (simulator.py:45-62); model clock only."""
+
+    c0_ms: float = 10.0
+    c1_ms_per_token: float = 0.0005
+
+    def compute_ms(self, tokens: int) -> float:
+        return self.c0_ms + self.c1_ms_per_token * tokens
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    end_ms: float
+    batch: int
+    prefills: int
+    tokens: int
+    compute_ms: float
+    sync_alloc_ms: float
+    stall_ms: float
+    cpu_ms: float
+    committed_bytes: int
+    used_bytes: int
+    alloc_bytes: int
+    preemptions: int
+    # measured (wall clock); zero under the model clock
+    exposed_ms: float = 0.0
+    kernel_ms: float = 0.0
+    bg_wall_ms: float = 0.0
+    deferred: int = 0
+
+    REF_FIELDS = ("iteration", "end_ms", "batch", "prefills", "tokens", "compute_ms", "sync_alloc_ms",
+                  "stall_ms", "cpu_ms", "committed_bytes", "used_bytes", "alloc_bytes", "preemptions")
+    CSV_FIELDS = REF_FIELDS + ("exposed_ms", "kernel_ms", "bg_wall_ms", "deferred")
+
+    def row(self, fields=CSV_FIELDS) -> list:
+        return [getattr(self, f) for f in fields]
+
+
+@dataclass
+class ServingMetrics:
+    iterations: list = field(default_factory=list)
+    completed_requests: int = 0
+    generated_tokens: int = 0
+    preemptions: int = 0
+    init_alloc_ms: float = 0.0
+    init_wall_ms: float = 0.0
+
+    @staticmethod
+    def _pct(values, q):
+        if not values:
+            return 0.0
+        v = sorted(values)
+        rank = -(-q * len(v) // 1)
+        return v[min(len(v), max(1, int(rank))) - 1]
+
+    def summary(self) -> dict:
+        """Same keys as SimMetrics.summary (simulator.py:118-141) + measured exposure."""
+        its = self.iterations
+        lat = [r.compute_ms + r.stall_ms + r.cpu_ms for r in its]
+        end = its[-1].end_ms if its else 0.0
+        n = len(its)
+        out = {
+            "iterations": n,
+            "max_batch": max((r.batch for r in its), default=0),
+            "completed_requests": self.completed_requests,
+            "generated_tokens": self.generated_tokens,
+            "tokens_per_s": self.generated_tokens / (end / 1000.0) if end > 0 else 0.0,
+            "sim_time_ms": end,
+            "p50_iteration_ms": self._pct(lat, 0.50),
+            "p99_iteration_ms": self._pct(lat, 0.99),
+            "stall_ms_total": sum(r.stall_ms for r in its),
+            "sync_alloc_ms_total": sum(r.sync_alloc_ms for r in its),
+            "cpu_ms_total": sum(r.cpu_ms for r in its),
+            "preemptions": self.preemptions,
+            "peak_committed_bytes": max((r.committed_bytes for r in its), default=0),
+            "peak_used_bytes": max((r.used_bytes for r in its), default=0),
+            "mean_waste_bytes": sum(r.committed_bytes - r.used_bytes for r in its) / n if n else 0.0,
+            "init_alloc_ms": self.init_alloc_ms,
+        }
+        ex = [r.exposed_ms for r in its]
+        out.update({
+            "exposed_map_ms_per_iter": sum(ex) / n if n else 0.0,
+            "exposed_map_ms_p99": self._pct(ex, 0.99),
+            "exposed_map_ms_max": max(ex, default=0.0),
+            "kernel_ms_total": sum(r.kernel_ms for r in its),
+            "init_wall_ms": self.init_wall_ms,
+        })
+        return out
+
+    def write_iterations_csv(self, path) -> None:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(IterationRecord.CSV_FIELDS)
+            for r in self.iterations:
+                w.writerow(r.row())
+
+    def write_summary_json(self, path) -> None:
+        with open(path, "w") as fh:
+            json.dump(self.summary(), fh, indent=2, sort_keys=True)
+            fh.write("\n")
+
+
+@dataclass
+class _Running:
+    record_index: int
+    prompt_tokens: int
+    decode_tokens: int
+    ctx: int
+    produced: int = 0
+    admit_order: int = 0
+
+
+class SyntheticModel:
+    """Attention-only model forward on the virtual KV cache: per layer KV-append of this
+    iteration's tokens, prefill attention for newly admitted requests and one batched decode
+    attention for the rest.  Inputs are seeded random bf16 (no weights: the hot path under test
+    is the KV cache and attention)."""
+
+    def __init__(self, mgr: KVCacheManager, geometry, max_prompt: int, seed: int = 0):
+        import torch
+
+        self.t = torch
+        self.mgr = mgr
+        g = geometry
+        self.layers = g.n_layers
+        self.hq, self.hkv, self.d = g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
+        self.dev = torch.device("cuda", mgr.device)
+        gen = torch.Generator(device=self.dev).manual_seed(seed)
+        B = g.max_batch
+        self.q_pf = torch.randn(max_prompt, self.hq, self.d, device=self.dev, generator=gen, dtype=torch.bfloat16)
+        self.k_pf = torch.randn(1, max_prompt, self.hkv, self.d, device=self.dev, generator=gen, dtype=torch.bfloat16)
+        self.v_pf = torch.randn_like(self.k_pf)
+        self.q_dec = torch.randn(B, self.hq, self.d, device=self.dev, generator=gen, dtype=torch.bfloat16)
+        self.k_dec = torch.randn(B, self.hkv, self.d, device=self.dev, generator=gen, dtype=torch.bfloat16)
+        self.v_dec = torch.randn_like(self.k_dec)
+        self.out_pf = torch.empty_like(self.q_pf)
+        self.out_dec = torch.empty_like(self.q_dec)
+        self.zero = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def forward(self, prefills, decodes) -> None:
+        """prefills: [(slot, prompt_len)]; decodes: [(slot, ctx)] (ctx includes the new token)."""
+        from .attention import decode_attention, kv_append, prefill_attention
+
+        t = self.t
+        for slot, n in prefills:
+            idx = t.tensor([slot], dtype=t.int32, device=self.dev)
+            for layer in range(self.layers):
+                kv_append(self.mgr, layer, self.k_pf[:, :n], self.v_pf[:, :n], self.zero, idx)
+                prefill_attention(self.mgr, layer, self.q_pf[:n], slot, kv_len=n, out=self.out_pf[:n])
+        if decodes:
+            B = len(decodes)
+            idx = t.tensor([s for s, _ in decodes], dtype=t.int32, device=self.dev)
+            after = t.tensor([c for _, c in decodes], dtype=t.int32, device=self.dev)
+            before = after - 1
+            for layer in range(self.layers):
+                kv_append(self.mgr, layer, self.k_dec[:B], self.v_dec[:B], before, idx)
+                decode_attention(self.mgr, layer, self.q_dec[:B], after, idx, out=self.out_dec[:B])
+
+
+def median_prompt_groups(records, geometry, page_group_size: int, sliced: bool = False) -> int:
+    """Default eager page-groups = groups covering the median prompt (simulator.py:507-520)."""
+    if not records:
+        return 0
+    prompts = sorted(r[1] for r in records)
+    median = prompts[(len(prompts) - 1) // 2]
+    tb = geometry.per_token_layer_bytes * (geometry.n_layers if sliced else 1)
+    return -(-median * tb // int(page_group_size))
+
+
+def load_trace_csv(path) -> list[tuple[int, int, int]]:
+    with open(path, newline="") as fh:
+        rd = csv.reader(fh)
+        next(rd)
+        return [(int(a), int(p), int(d)) for a, p, d in rd if a]
+
+
+def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
+        page_group_size: int = MB2, pool_bytes: int = 80 * 1024 ** 3, reclaim_threshold: float = 0.10,
+        eager_groups: int = 0, sliced: bool = False, pre_create_fraction: float = 1.0,
+        iteration_model: IterationModel | None = None, preemption_cap: int = 1000,
+        backend: str | None = None, defer: bool | None = None, observer=None,
+        max_iterations: int | None = None, model: SyntheticModel | None = None,
+        manager: KVCacheManager | None = None) -> ServingMetrics:
+    """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31)."""
+    if mode not in ("sync", "overlapped"):
+        raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
+    if clock not in ("model", "wall"):
+        raise ValueError(f"clock must be 'model' or 'wall', got {clock!r}")
+    for i, (_, p, d) in enumerate(records):
+        if p + d > geometry.max_context:
+            raise ValueError(f"trace record {i}: prompt+decode ({p}+{d}) exceeds max_context")
+    wall = clock == "wall"
+    if defer is None:
+        defer = wall               # model clock keeps the reference's exact call order
+    im = iteration_model or IterationModel()
+    mgr = manager or KVCacheManager(
+        geometry, ManagerConfig(page_group_size=int(page_group_size), pool_bytes=pool_bytes,
+                                reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
+                                sliced=sliced, pre_create_fraction=pre_create_fraction),
+        backend=backend or ("cuda" if wall else "shadow"))
+    if wall and model is None:
+        model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1)
+    if wall:
+        import torch
+
+    metrics = ServingMetrics(init_alloc_ms=mgr.init_us / 1000.0, init_wall_ms=mgr.init_wall_us / 1000.0)
+    token_bytes = 2 * geometry.n_layers * geometry.per_token_layer_bytes
+    pending: deque = deque(enumerate(records))
+    running: dict[int, _Running] = {}
+    seq_lens = [0] * geometry.max_batch
+    clock_us = 0
+    iteration = 0
+    admit_counter = 0
+    prev_compute_budget_us = 0.0
+    prev_alloc_cum = mgr.vmm.total_mapped_bytes
+    t_start = time.perf_counter()
+    overlapped = mode == "overlapped"
+
+    while pending or running:
+        if max_iterations is not None and iteration >= max_iterations:
+            break
+        t_it = time.perf_counter()
+        if wall:
+            clock_us = max(clock_us, int((t_it - t_start) * 1e6))
+        if not running and pending:
+            clock_us = max(clock_us, pending[0][1][0] * 1000)
+            if wall:      # idle: let real time catch up with the next arrival
+                gap = clock_us / 1e6 - (time.perf_counter() - t_start)
+                if gap > 0:
+                    time.sleep(gap)
+        # -- admit (Algorithm 1 lines 6-11) --
+        t_exp = time.perf_counter()
+        while pending and pending[0][1][0] * 1000 <= clock_us:
+            try:
+                rid = mgr.alloc_reqid()
+            except BatchFullError:
+                break
+            index, rec = pending.popleft()
+            running[rid] = _Running(index, rec[1], rec[2], ctx=rec[1], admit_order=admit_counter)
+            admit_counter += 1
+            seq_lens[rid] = rec[1]
+        if not running and pending:
+            raise SimulationAborted("no request can be admitted into an empty batch")
+        # -- background work + step (line 13) --
+        bg_us = 0.0
+        bg_wall_ms = 0.0
+        deferred = 0
+        if overlapped:
+            bgr = mgr.bg_wait()                  # the plan executed during the previous compute
+            bg_wall_ms = bgr.bg_wall_us / 1000.0
+            it_res = mgr.iteration_step(seq_lens, eager=True, reclaim=True, defer=defer)
+            bg_us = bgr.plan_us + bgr.eager_us + bgr.reclaim_us + it_res.eager_us + it_res.reclaim_us
+            ok, us = it_res.ok, it_res.sync_us
+            deferred = int(it_res.deferred)
+        else:
+            r = mgr.step(seq_lens)
+            ok, us = r.ok, r.sync_us
+        overflow_us = max(0.0, bg_us - prev_compute_budget_us)
+        sync_us = us
+        preempted_here = 0
+        while not ok:
+            if not running:
+                raise SimulationAborted("memory demand cannot be met with an empty batch")
+            victim = max(running, key=lambda r: running[r].admit_order)
+            state = running.pop(victim)
+            mgr.free_reqid(victim)
+            seq_lens[victim] = 0
+            pending.appendleft((state.record_index, records[state.record_index]))
+            preempted_here += 1
+            metrics.preemptions += 1
+            if metrics.preemptions > preemption_cap:
+                raise SimulationAborted(f"aborted after {metrics.preemptions} preemptions")
+            r = mgr.step(seq_lens)
+            ok = r.ok
+            sync_us += r.sync_us
+        exposed_ms = (time.perf_counter() - t_exp) * 1e3
+        if observer is not None:
+            observer(mgr, list(seq_lens), iteration)
+
+        batch = len(running)
+        tokens = sum(seq_lens[rid] for rid in running)
+        prefills = sum(1 for r in running.values() if r.produced == 0)
+        # quiescent-point counters (before this iteration's plan starts mapping in background)
+        alloc_cum = mgr.vmm.total_mapped_bytes
+        committed = mgr.committed_bytes()
+        # -- compute (line 14) + overlapped planning of the next iteration's maps --
+        kernel_ms = 0.0
+        if wall and batch:
+            t_k = time.perf_counter()
+            model.forward([(rid, seq_lens[rid]) for rid, r in running.items() if r.produced == 0],
+                          [(rid, seq_lens[rid]) for rid, r in running.items() if r.produced > 0])
+            mgr.mark_use()
+        if overlapped:
+            next_seq = list(seq_lens)
+            for rid in running:
+                next_seq[rid] = min(seq_lens[rid] + 1, geometry.max_context)
+            plan = mgr.plan_overlap(next_seq)
+            mgr.bg_submit(plan, credit=True)     # maps run on the bg thread during the kernels
+        if wall and batch:
+            torch.cuda.synchronize()
+            kernel_ms = (time.perf_counter() - t_k) * 1e3
+        compute_ms = (kernel_ms if wall else im.compute_ms(tokens)) if batch else 0.0
+        stall_us = (exposed_ms * 1000.0) if wall else (sync_us + overflow_us)
+        if wall:
+            clock_us = int((time.perf_counter() - t_start) * 1e6)
+        else:
+            clock_us += round(compute_ms * 1000) + round(stall_us)
+        metrics.iterations.append(IterationRecord(
+            iteration=iteration, end_ms=clock_us / 1000.0, batch=batch, prefills=prefills, tokens=tokens,
+            compute_ms=compute_ms, sync_alloc_ms=sync_us / 1000.0, stall_ms=stall_us / 1000.0, cpu_ms=0.0,
+            committed_bytes=committed, used_bytes=tokens * token_bytes, alloc_bytes=alloc_cum - prev_alloc_cum,
+            preemptions=preempted_here, exposed_ms=exposed_ms if wall else 0.0, kernel_ms=kernel_ms,
+            bg_wall_ms=bg_wall_ms, deferred=deferred))
+        prev_alloc_cum = alloc_cum
+        prev_compute_budget_us = compute_ms * 1000.0
+        # -- retire (lines 15-22) --
+        for rid in list(running):
+            st = running[rid]
+            st.produced += 1
+            if st.produced >= st.decode_tokens:
+                metrics.completed_requests += 1
+                metrics.generated_tokens += st.decode_tokens
+                mgr.free_reqid(rid)
+                seq_lens[rid] = 0
+                del running[rid]
+            else:
+                st.ctx += 1
+                seq_lens[rid] = st.ctx
+        iteration += 1
+    if overlapped:
+        mgr.bg_wait()
+    return metrics
