@@ -190,10 +190,16 @@ vattn_status vattn_buffer_mappings(vattn_t* h, int32_t buffer_id, int64_t* offse
 vattn_status vattn_events(vattn_t* h, int64_t* triples, int64_t cap_entries, int64_t* n);
 vattn_status vattn_buffer_base(vattn_t* h, int32_t buffer_id, uint64_t* dptr);
 
-/* Table 2 analog measured on this device: mean µs per call at `page_bytes` (out[8]: reserve,
- * create, map, set_access, unmap, release, address_free, set_access-per-page batched by `run`). */
+/* Table 2 analog measured on this device: mean µs per call at `page_bytes` (out[10]: reserve,
+ * create, map, set_access, unmap, release, address_free, set_access-per-page batched by `run`,
+ * map and set_access again on recycled (previously mapped) handles). */
 vattn_status vattn_vmm_microbench(int32_t device, int64_t page_bytes, int32_t n_pages, int32_t run,
                                   double* out);
+
+/* Probe: per-2MiB-slice map/set_access/unmap µs when slices come from one big physical handle
+ * (big_handle=1) or one handle each, with `extra_handles` other live allocations. */
+vattn_status vattn_vmm_slice_probe(int32_t device, int32_t n_pages, int32_t big_handle,
+                                   int32_t extra_handles, double* out);
 
 /* ---- kernels (bf16 K/V/Q/O; layouts in DESIGN.md §3) --------------------------------- */
 /* Write k_new/v_new [batch, n_new, Hkv, D] at rows cache_seqlens[b] + i of slot
@@ -241,6 +247,8 @@ vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v
                                 int32_t n_q_heads, const int32_t* seqlens, float scale,
                                 int32_t num_splits, void* workspace, int64_t workspace_bytes,
                                 void* stream);
+/* serving benchmark only: occupy `stream` for `ns` ns of device time (dense-layer compute proxy) */
+vattn_status vattn_compute_proxy(uint64_t ns, void* stream);
 /* split count the auto heuristic picks for `batch` rows x Hkv heads at max_seqlen tokens */
 int32_t vattn_decode_num_splits(int32_t batch, int32_t n_kv_heads, int32_t max_seqlen);
 int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t n_q_heads, int32_t head_dim,

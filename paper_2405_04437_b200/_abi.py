@@ -112,6 +112,8 @@ SIGNATURES = {
     "vattn_decode_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp,
                                    c_i32, c_i32, c_vp, c_f32, c_i32, c_vp, c_i64, c_vp]),
     "vattn_vmm_microbench": (c_i32, [c_i32, c_i64, c_i32, c_i32, C.POINTER(c_f64)]),
+    "vattn_vmm_slice_probe": (c_i32, [c_i32, c_i32, c_i32, c_i32, C.POINTER(c_f64)]),
+    "vattn_compute_proxy": (c_i32, [c_u64, c_vp]),
     "vattn_decode_num_splits": (c_i32, [c_i32, c_i32, c_i32]),
     "vattn_decode_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
 }

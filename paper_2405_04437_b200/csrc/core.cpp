@@ -1473,12 +1473,86 @@ vattn_status vattn_vmm_microbench(int32_t device, int64_t page_bytes, int32_t n_
     for (int i = 0; i < n_pages; i += run) check_cu(d.MemSetAccess(va + i * pg, pg * run, &acc, 1), "cuMemSetAccess(run)");
     out[7] = (vattn::now_us() - t0) / n_pages;
     for (int i = 0; i < n_pages; ++i) check_cu(d.MemUnmap(va + i * pg, pg), "cuMemUnmap");
+    // recycled handles: map the same physical pages again at shifted slots
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemMap(va + ((i + 1) % n_pages) * pg, pg, 0, h[i], 0), "cuMemMap(re)");
+    out[8] = (vattn::now_us() - t0) / n_pages;
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemSetAccess(va + i * pg, pg, &acc, 1), "cuMemSetAccess(re)");
+    out[9] = (vattn::now_us() - t0) / n_pages;
+    for (int i = 0; i < n_pages; ++i) check_cu(d.MemUnmap(va + i * pg, pg), "cuMemUnmap");
     t0 = vattn::now_us();
     for (auto& x : h) check_cu(d.MemRelease(x), "cuMemRelease");
     out[5] = (vattn::now_us() - t0) / n_pages;
     t0 = vattn::now_us();
     check_cu(d.MemAddressFree(va, total), "cuMemAddressFree");
     out[6] = vattn::now_us() - t0;
+  });
+}
+
+
+// Probe: map+SetAccess+unmap cost of `n_pages` 2 MiB slices when the physical memory comes
+// from one big handle (cuMemMap offset) vs one handle per slice, with `extra_handles` other
+// live allocations in the context.  out[0..2] = per-slice map, set_access, unmap µs.
+vattn_status vattn_vmm_slice_probe(int32_t device, int32_t n_pages, int32_t big_handle,
+                                   int32_t extra_handles, double* out) {
+  return guard([&] {
+    using vattn::check_cu;
+    const vattn::Driver& d = vattn::driver();
+    vattn::check_rt(cudaSetDevice(device), "cudaSetDevice");
+    vattn::check_rt(cudaFree(nullptr), "context init");
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    const size_t pg = 2u << 20;
+    // `extra_handles` other live 2 MiB allocations, mapped and accessible (a populated cache)
+    std::vector<CUmemGenericAllocationHandle> extra((size_t)extra_handles);
+    CUdeviceptr xva = 0;
+    if (extra_handles > 0) check_cu(d.MemAddressReserve(&xva, pg * extra_handles, pg, 0, 0), "reserve(extra)");
+    for (int i = 0; i < extra_handles; ++i) {
+      check_cu(d.MemCreate(&extra[i], pg, &prop, 0), "cuMemCreate(extra)");
+      check_cu(d.MemMap(xva + (size_t)i * pg, pg, 0, extra[i], 0), "cuMemMap(extra)");
+    }
+    if (extra_handles > 0) check_cu(d.MemSetAccess(xva, pg * extra_handles, &acc, 1), "cuMemSetAccess(extra)");
+    std::vector<CUmemGenericAllocationHandle> h;
+    if (big_handle) {
+      h.resize(1);
+      check_cu(d.MemCreate(&h[0], pg * n_pages, &prop, 0), "cuMemCreate(big)");
+    } else {
+      h.resize((size_t)n_pages);
+      for (auto& x : h) check_cu(d.MemCreate(&x, pg, &prop, 0), "cuMemCreate");
+    }
+    CUdeviceptr va = 0;
+    check_cu(d.MemAddressReserve(&va, pg * n_pages * 2, pg, 0, 0), "reserve");
+    double tm = 0, ta = 0, tu = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      double t0 = vattn::now_us();
+      for (int i = 0; i < n_pages; ++i) {
+        const CUdeviceptr p = va + (size_t)(2 * i + rep) * pg;   // non-contiguous slots
+        if (big_handle) check_cu(d.MemMap(p, pg, pg * i, h[0], 0), "cuMemMap(slice)");
+        else check_cu(d.MemMap(p, pg, 0, h[i], 0), "cuMemMap");
+      }
+      tm += vattn::now_us() - t0;
+      t0 = vattn::now_us();
+      for (int i = 0; i < n_pages; ++i)
+        check_cu(d.MemSetAccess(va + (size_t)(2 * i + rep) * pg, pg, &acc, 1), "cuMemSetAccess");
+      ta += vattn::now_us() - t0;
+      t0 = vattn::now_us();
+      for (int i = 0; i < n_pages; ++i) check_cu(d.MemUnmap(va + (size_t)(2 * i + rep) * pg, pg), "cuMemUnmap");
+      tu += vattn::now_us() - t0;
+    }
+    out[0] = tm / (2.0 * n_pages);
+    out[1] = ta / (2.0 * n_pages);
+    out[2] = tu / (2.0 * n_pages);
+    d.MemAddressFree(va, pg * n_pages * 2);
+    for (auto x : h) d.MemRelease(x);
+    for (int i = 0; i < extra_handles; ++i) d.MemUnmap(xva + (size_t)i * pg, pg);
+    for (auto x : extra) d.MemRelease(x);
+    if (extra_handles > 0) d.MemAddressFree(xva, pg * extra_handles);
   });
 }
 

@@ -357,6 +357,19 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
   *reinterpret_cast<uint2*>(out + (int64_t)row * D + c4 * 4) = pk;
 }
 
+// ------------------------------------------------------------------------------ compute proxy
+// Stands in for the non-attention part of a model iteration (GEMMs) in the serving benchmark:
+// holds the stream for `ns` nanoseconds of device time (globaltimer), calibrated by the caller
+// to the reference's IterationModel (simulator.py:45-62).  One warp; does not touch memory.
+__global__ void compute_proxy_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 // ------------------------------------------------------------------------------ host side
 struct KernelState {
   std::mutex mu;
@@ -544,6 +557,13 @@ static vattn_status kguard(F&& f) {
 }
 
 extern "C" {
+
+vattn_status vattn_compute_proxy(uint64_t ns, void* stream) {
+  return kguard([&] {
+    vattn::compute_proxy_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns);
+    vattn::check_rt(cudaGetLastError(), "compute proxy launch");
+  });
+}
 
 int32_t vattn_decode_num_splits(int32_t batch, int32_t hkv, int32_t max_seqlen) {
   try {

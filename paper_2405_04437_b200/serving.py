@@ -156,7 +156,8 @@ class SyntheticModel:
     attention for the rest.  Inputs are seeded random bf16 (no weights: the hot path under test
     is the KV cache and attention)."""
 
-    def __init__(self, mgr: KVCacheManager, geometry, max_prompt: int, seed: int = 0):
+    def __init__(self, mgr: KVCacheManager, geometry, max_prompt: int, seed: int = 0,
+                 dense_model: "IterationModel | None" = None):
         import torch
 
         self.t = torch
@@ -176,6 +177,7 @@ class SyntheticModel:
         self.out_pf = torch.empty_like(self.q_pf)
         self.out_dec = torch.empty_like(self.q_dec)
         self.zero = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.dense_model = dense_model
 
     def forward(self, prefills, decodes) -> None:
         """prefills: [(slot, prompt_len)]; decodes: [(slot, ctx)] (ctx includes the new token)."""
@@ -195,6 +197,14 @@ class SyntheticModel:
             for layer in range(self.layers):
                 kv_append(self.mgr, layer, self.k_dec[:B], self.v_dec[:B], before, idx)
                 decode_attention(self.mgr, layer, self.q_dec[:B], after, idx, out=self.out_dec[:B])
+        if self.dense_model is not None:
+            # the dense layers (QKV/O projections, MLP) of the iteration, as device time
+            import ctypes as C
+
+            from ._abi import check, lib
+            tokens = sum(n for _, n in prefills) + len(decodes)
+            ns = int(self.dense_model.compute_ms(tokens) * 1e6)
+            check(lib().vattn_compute_proxy(ns, C.c_void_p(t.cuda.current_stream().cuda_stream)))
 
 
 def median_prompt_groups(records, geometry, page_group_size: int, sliced: bool = False) -> int:
@@ -220,7 +230,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         iteration_model: IterationModel | None = None, preemption_cap: int = 1000,
         backend: str | None = None, defer: bool | None = None, observer=None,
         max_iterations: int | None = None, model: SyntheticModel | None = None,
-        manager: KVCacheManager | None = None) -> ServingMetrics:
+        manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31)."""
     if mode not in ("sync", "overlapped"):
         raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
@@ -239,7 +249,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
                                 sliced=sliced, pre_create_fraction=pre_create_fraction),
         backend=backend or ("cuda" if wall else "shadow"))
     if wall and model is None:
-        model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1)
+        model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1,
+                               dense_model=dense_proxy)
     if wall:
         import torch
 

@@ -1,0 +1,41 @@
+"""BASELINE config 5 on the GPU: Algorithm-1 serving loop with real kernels (wall clock).
+
+python tools/serving_trace.py --mode sync|overlapped --requests 128 [--out gpurun_out/serving]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+from paper_2405_04437_b200.geometry import llama3_8b  # noqa: E402
+from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run  # noqa: E402
+
+MB2 = 2 * 1024 * 1024
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="overlapped")
+ap.add_argument("--requests", type=int, default=128)
+ap.add_argument("--pool-gib", type=int, default=40)
+ap.add_argument("--no-defer", action="store_true")
+ap.add_argument("--out", default=None)
+ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel dense-layer time on the GPU")
+a = ap.parse_args()
+rows = load_trace_csv(Path("tests/golden/trace_config5.csv"))[: a.requests]
+g = llama3_8b(max_context=4096, max_batch=64)
+eager = median_prompt_groups(rows, g, MB2)
+m = run(rows, g, mode=a.mode, clock="wall", page_group_size=MB2, pool_bytes=a.pool_gib * 1024 ** 3,
+        eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
+        preemption_cap=100_000, defer=not a.no_defer,
+        dense_proxy=IterationModel() if a.dense_proxy else None)
+s = m.summary()
+s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
+          "dense_proxy": a.dense_proxy})
+print(json.dumps(s))
+if a.out:
+    Path(a.out).parent.mkdir(parents=True, exist_ok=True)
+    tag = a.mode + ("_dense" if a.dense_proxy else "")
+    m.write_iterations_csv(a.out + f"_{tag}.csv")
+    with open(a.out + f"_{tag}.json", "w") as fh:
+        json.dump(s, fh, indent=1)
