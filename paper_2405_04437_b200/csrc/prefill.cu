@@ -114,6 +114,12 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // number of KV tiles a query tile starting at row q0 needs
 __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   if (q0 >= p.n_q) return 0;
@@ -269,20 +275,35 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     for (int j = 0; j < n; ++j) {
       ptx::mbar_wait(&s_full[x], j & 1);
       fence_after();
-      // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap)
+      // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
+      // Only diagonal / tail tiles need the per-element mask; the others take the plain path.
       const int k0 = j * kBN;
       const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
       const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
+      const bool warp_mask = __any_sync(0xffffffffu, need_mask);
       float mx = -INFINITY;
+      if (!warp_mask) {
+        float m3 = -INFINITY;
 #pragma unroll
-      for (int c0 = 0; c0 < kBN; c0 += 32) {
-        uint32_t r[32];
-        TMEM_LD32(tS + c0, r);
-        tmem_wait_ld();
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD32(tS + c0, r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float v = (c0 + c < lim) ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, v);
+          for (int c = 0; c < 32; c += 2) m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+        }
+        mx = m3 * p.scale_log2;     // scale > 0: max commutes with the scaling
+      } else {
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD32(tS + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float v = (c0 + c < lim) ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
+            mx = fmaxf(mx, v);
+          }
         }
       }
       // lazy rescale: keep the stale max unless it grows by more than 2^8 (warp-uniform decision)
@@ -306,9 +327,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
         m_run = m_new;
       }
-      // pass 2: P = exp2(S*scale - m) -> bf16 into TMEM over the S columns already consumed
+      // pass 2: P = exp2(S*scale - m) -> bf16 into TMEM over the S columns already consumed.
+      // Packed f32x2 FMA/ADD (FFMA2/FADD2) halve the FMA-pipe instructions; MUFU does the exp2.
       const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      float lsum = 0.f;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      const float2 nm2 = make_float2(neg_m, neg_m);
+      float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c0 = 0; c0 < kBN; c0 += 32) {
         uint32_t r[32], pk[16];
@@ -316,13 +340,18 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const float p0 = (c0 + c < lim) ? ptx::fast_exp2(fmaf(__uint_as_float(r[c]), p.scale_log2, neg_m)) : 0.f;
-          const float p1 = (c0 + c + 1 < lim) ? ptx::fast_exp2(fmaf(__uint_as_float(r[c + 1]), p.scale_log2, neg_m)) : 0.f;
-          lsum += p0 + p1;
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
+          float p0 = ptx::fast_exp2(x.x), p1 = ptx::fast_exp2(x.y);
+          if (warp_mask) {
+            p0 = (c0 + c < lim) ? p0 : 0.f;
+            p1 = (c0 + c + 1 < lim) ? p1 : 0.f;
+          }
+          acc2 = __fadd2_rn(acc2, make_float2(p0, p1));
           pk[c / 2] = ptx::pack_bf16(p0, p1);
         }
         TMEM_ST16(tS + c0 / 2, pk);
       }
+      const float lsum = acc2.x + acc2.y;
       l_run += lsum;
       tmem_wait_st();
       fence_before();
