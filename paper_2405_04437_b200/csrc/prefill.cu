@@ -114,10 +114,64 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// 2^x on the FMA pipe (FA4-style MUFU offload): round-to-nearest via the 1.5·2^23 magic add,
+// degree-3 polynomial on [-0.5, 0.5] (max rel. err 2.2e-4, far below bf16's 3.9e-3), exponent
+// via integer add.  Inputs below -127 flush to ~0 (masked entries are zeroed explicitly).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));
+  float2 q = __ffma2_rn(f, make_float2(0.05286731580314504f, 0.05286731580314504f),
+                        make_float2(0.2421521458456525f, 0.2421521458456525f));
+  q = __ffma2_rn(q, f, make_float2(0.6935868335103712f, 0.6935868335103712f));
+  q = __ffma2_rn(q, f, make_float2(0.9999627473381362f, 0.9999627473381362f));
+  const int ex = (__float_as_int(t.x) - 0x4B400000) << 23;
+  const int ey = (__float_as_int(t.y) - 0x4B400000) << 23;
+  return make_float2(__int_as_float(__float_as_int(q.x) + ex), __int_as_float(__float_as_int(q.y) + ey));
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
+}
+
+// Pass 2 of the online softmax for one 128-column S row: P = exp2(S*scale - m) packed to bf16
+// and stored over the S columns already consumed; returns the (pairwise) row sum.  MASK=false
+// (all but the diagonal/tail tiles) carries no per-element compare/select.
+template <bool MASK, int POLY>
+__device__ __forceinline__ float2 softmax_p_pass(uint32_t tS, float2 sc2, float2 nm2, int lim) {
+  float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c0 = 0; c0 < kBN; c0 += 32) {
+    uint32_t r[32], pk[16];
+    TMEM_LD32(tS + c0, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
+      float p0, p1;
+      if (((c / 2) & 3) < POLY) {       // this share of the exps runs on the FMA pipe
+        const float2 e = exp2_poly2(x);
+        p0 = e.x;
+        p1 = e.y;
+      } else {
+        p0 = ptx::fast_exp2(x.x);
+        p1 = ptx::fast_exp2(x.y);
+      }
+      if (MASK) {
+        p0 = (c0 + c < lim) ? p0 : 0.f;
+        p1 = (c0 + c + 1 < lim) ? p1 : 0.f;
+      }
+      acc2 = __fadd2_rn(acc2, make_float2(p0, p1));
+      pk[c / 2] = ptx::pack_bf16(p0, p1);
+    }
+    TMEM_ST16(tS + c0 / 2, pk);
+  }
+  return acc2;
 }
 
 // number of KV tiles a query tile starting at row q0 needs
@@ -132,6 +186,7 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
+template <int POLY>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, Params p) {
@@ -332,25 +387,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
       const float2 nm2 = make_float2(neg_m, neg_m);
-      float2 acc2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c0 = 0; c0 < kBN; c0 += 32) {
-        uint32_t r[32], pk[16];
-        TMEM_LD32(tS + c0, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
-          float p0 = ptx::fast_exp2(x.x), p1 = ptx::fast_exp2(x.y);
-          if (warp_mask) {
-            p0 = (c0 + c < lim) ? p0 : 0.f;
-            p1 = (c0 + c + 1 < lim) ? p1 : 0.f;
-          }
-          acc2 = __fadd2_rn(acc2, make_float2(p0, p1));
-          pk[c / 2] = ptx::pack_bf16(p0, p1);
-        }
-        TMEM_ST16(tS + c0 / 2, pk);
-      }
+      const float2 acc2 = warp_mask ? softmax_p_pass<true, POLY>(tS, sc2, nm2, lim)
+                                    : softmax_p_pass<false, POLY>(tS, sc2, nm2, lim);
       const float lsum = acc2.x + acc2.y;
       l_run += lsum;
       tmem_wait_st();
@@ -448,15 +486,20 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.causal = causal ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)pf::kD);
   p.scale_log2 = scale * 1.4426950408889634f;
-  static bool attr = false;
-  if (!attr) {
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  pf::kSmemBytes),
-             "prefill smem attribute");
-    attr = true;
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("VATTN_PF_POLY");
+    poly = e ? std::max(0, std::min(3, atoi(e))) : 1;
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
   }
   dim3 grid(p.n_pairs, hq);
-  pf::prefill_kernel<<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
