@@ -327,6 +327,127 @@ def bench_decode(args, world, rank, local):
     return result
 
 
+# ----------------------------------------------------------------------------- extras
+def _time_ms(fn, iters=10, warm=3):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def extra_prefill(local):
+    """BASELINE config 3: Yi-6B 16K prompt appended into a request slot of the virtual cache,
+    then causal tcgen05 prefill attention over it (one layer; 32 Q / 4 KV heads, D 128)."""
+    import torch
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import kv_append, prefill_attention
+    from paper_2405_04437_b200.geometry import yi_6b
+
+    dev = torch.device("cuda", local)
+    S = 16384
+    g = yi_6b(max_context=S, max_batch=1)
+    g = g.__class__(**{**g.to_dict(), "n_layers": 1})
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2), device=local)
+    rid = mgr.alloc_reqid()
+    t0 = time.perf_counter()
+    assert mgr.step([S]).ok
+    map_ms = (time.perf_counter() - t0) * 1e3
+    gen = torch.Generator(device=dev).manual_seed(0)
+    kn = torch.randn(1, S, 4, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+    vn = torch.randn(1, S, 4, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+    q = torch.randn(S, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    zero = torch.zeros(1, dtype=torch.int32, device=dev)
+    idx = torch.tensor([rid], dtype=torch.int32, device=dev)
+    app_ms = _time_ms(lambda: kv_append(mgr, 0, kn, vn, zero, idx), iters=20)
+    pf_ms = _time_ms(lambda: prefill_attention(mgr, 0, q, rid, out=out), iters=10)
+    pk = peaks()
+    flops = 2.0 * S * S * 128 * 32
+    tf = flops / (pf_ms * 1e-3) / 1e12
+    app_bytes = 2 * 2 * S * 4 * 128 * 2
+    mgr.close()
+    return {"workload": "yi-6b prefill 16K causal (1 layer, 32 Q / 4 KV heads, D 128)",
+            "prefill_ms": pf_ms, "prefill_tflops": tf,
+            "prefill_frac_of_measured_burst": tf / pk["bf16_tflops"], "prefill_frac_of_2250_nominal": tf / 2250.0,
+            "flops": flops, "append_us": app_ms * 1e3, "append_gbs": app_bytes / (app_ms * 1e-3) / 1e9,
+            "append_frac_hbm": app_bytes / (app_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "map_16k_prompt_ms": map_ms}
+
+
+def extra_paged(local):
+    """Contiguous (vAttention) vs paged-layout decode kernel on identical K/V (L8 layer)."""
+    import torch
+
+    from paper_2405_04437_b200.attention import decode_attention_paged, decode_attention_raw
+
+    dev = torch.device("cuda", local)
+    B, hq, hkv, d, L = 64, 32, 8, 128, 4096
+    gen = torch.Generator(device=dev).manual_seed(1)
+    k = torch.randn(B, L, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    v = torch.randn(B, L, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    q = torch.randn(B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    seq = torch.full((B,), L, dtype=torch.int32, device=dev)
+    byt = 2 * B * L * hkv * d * 2
+    res = {"contiguous_us": _time_ms(lambda: decode_attention_raw(q, k, v, seq)) * 1e3}
+    for bs in (16, 256):
+        nb = L // bs
+        perm = torch.randperm(B * nb, device=dev, generator=gen)
+        kp = torch.empty_like(k).view(B * nb, bs, hkv, d)
+        vp = torch.empty_like(v).view(B * nb, bs, hkv, d)
+        kp[perm] = k.view(B * nb, bs, hkv, d)
+        vp[perm] = v.view(B * nb, bs, hkv, d)
+        bt = perm.view(B, nb).to(torch.int32)
+        res[f"paged_bs{bs}_us"] = _time_ms(lambda: decode_attention_paged(q, kp, vp, bt, seq)) * 1e3
+        o_ref = decode_attention_raw(q, k, v, seq)
+        o_pg = decode_attention_paged(q, kp, vp, bt, seq)
+        res[f"paged_bs{bs}_max_abs_diff_vs_contiguous"] = float((o_ref.float() - o_pg.float()).abs().max())
+        del kp, vp
+    for key in list(res):
+        if key.endswith("_us"):
+            res[key.replace("_us", "_gbs")] = byt / (res[key] * 1e-6) / 1e9
+    res["paged_bs16_slowdown"] = res["paged_bs16_us"] / res["contiguous_us"]
+    res["paged_bs256_slowdown"] = res["paged_bs256_us"] / res["contiguous_us"]
+    return res
+
+
+def extra_serving(local, requests=48):
+    """BASELINE config 5: Algorithm-1 loop on the config-5 trace (Llama-3-8B shape), real kernels
+    + dense-layer compute proxy (reference IterationModel), sync vs overlapped+deferred+eager."""
+    from paper_2405_04437_b200.geometry import llama3_8b
+    from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run
+
+    rows = load_trace_csv(ROOT / "tests" / "golden" / "trace_config5.csv")[:requests]
+    g = llama3_8b(max_context=4096, max_batch=64)
+    eager = median_prompt_groups(rows, g, MB2)
+    out = {"trace": f"tests/golden/trace_config5.csv first {requests} requests", "eager_groups": eager}
+    for mode in ("sync", "overlapped"):
+        m = run(rows, g, mode=mode, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
+                eager_groups=eager if mode == "overlapped" else 0, reclaim_threshold=0.10,
+                preemption_cap=100_000, dense_proxy=IterationModel())
+        s = m.summary()
+        its = m.iterations
+        dec = [r.exposed_ms for r in its if r.prefills == 0]
+        out[mode] = {k: s[k] for k in ("iterations", "tokens_per_s", "exposed_map_ms_per_iter",
+                                       "exposed_map_ms_p99", "exposed_map_ms_max", "sync_alloc_ms_total",
+                                       "stall_ms_total", "preemptions")}
+        out[mode]["exposed_map_ms_per_decode_iter"] = sum(dec) / max(1, len(dec))
+        out[mode]["exposed_map_ms_median"] = statistics.median([r.exposed_ms for r in its]) if its else 0.0
+        out[mode]["exposed_breakdown_ms"] = {k: sum(getattr(r, k) for r in its) for k in
+                                             ("t_admit_ms", "t_bgwait_ms", "t_step_ms", "t_retire_ms")}
+        out[mode]["driver_set_access_ms_total"] = sum(r.drv_set_access_ms for r in its)
+        out[mode]["driver_maps_total"] = sum(r.drv_maps for r in its)
+    return out
+
+
 # ----------------------------------------------------------------------------- CPU baseline
 class CpuDecodeSample:
     """Oracle port (fp32 torch on all host cores + the oracle allocator) on a bounded sample of
@@ -425,6 +546,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["l8_decode", "y34_decode"], default="l8_decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip prefill / paged / serving sub-benches")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
@@ -451,6 +573,15 @@ def main(argv=None):
             "e2e": res.pop("e2e"), "clocks": res.pop("clocks"), "gpu_launches": res.pop("gpu_launches"),
             **res,
         }
+        if not args.no_extras and world == 1:
+            extras = {}
+            for name, fn in (("prefill", extra_prefill), ("paged_vs_contiguous", extra_paged),
+                             ("serving", extra_serving)):
+                try:
+                    extras[name] = fn(local)
+                except Exception as e:   # an extra must not void the headline line
+                    extras[name] = {"error": repr(e)[:300]}
+            line["extras"] = extras
         print(json.dumps(line), flush=True)
     return 0
 

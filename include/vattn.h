@@ -89,6 +89,9 @@ typedef struct vattn_config {
   int32_t batch_set_access;    /* 1: coalesce cuMemSetAccess over contiguous page runs */
   const vattn_latency_entry* latency;  /* NULL = Table 2 defaults (vmm.py:55-68) */
   int32_t n_latency;
+  /* B200 addition: physically pre-map pages each active slot needs within this many more tokens
+   * (background jobs with VATTN_BG_PREFETCH); logical state stays the reference's. 0 = off. */
+  int32_t prefetch_tokens;
 } vattn_config;
 
 typedef struct vattn_t vattn_t;
@@ -112,6 +115,7 @@ typedef struct vattn_counters {
   int64_t real_maps, real_unmaps, real_set_access_calls, real_creates, real_releases;
   double real_map_wall_us, real_unmap_wall_us, real_create_wall_us, real_set_access_wall_us;
   double init_wall_us;
+  int64_t spec_maps, spec_hits, spec_steals, spec_pages;   /* physical prefetch */
 } vattn_counters;
 
 typedef struct vattn_bg_result {
@@ -131,6 +135,8 @@ typedef struct vattn_bg_result {
 /* vattn_iteration_step: defer eager/reclaim past step onto the background thread when the
  * result is provably identical */
 #define VATTN_ITER_DEFER 16u
+/* run the physical prefetch (see vattn_config.prefetch_tokens) at the end of the job */
+#define VATTN_BG_PREFETCH 32u
 
 typedef struct vattn_iteration_result {
   int32_t ok;                  /* step ok (preempt on 0) */
@@ -176,6 +182,8 @@ vattn_status vattn_mark_use(vattn_t* h, void* stream);
 
 /* ---- introspection ------------------------------------------------------------------ */
 vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out);
+/* same, without joining the background queue (monitoring; may race with a running job) */
+vattn_status vattn_counters_peek(vattn_t* h, vattn_counters* out);
 /* 5 int64 per slot: active, context_len, mapped_groups, phase(0 inactive,1 prefill,2 decode),
  * freed_seq */
 vattn_status vattn_slot_state(vattn_t* h, int64_t* out, int64_t cap_slots);
@@ -200,6 +208,10 @@ vattn_status vattn_vmm_microbench(int32_t device, int64_t page_bytes, int32_t n_
  * (big_handle=1) or one handle each, with `extra_handles` other live allocations. */
 vattn_status vattn_vmm_slice_probe(int32_t device, int32_t n_pages, int32_t big_handle,
                                    int32_t extra_handles, double* out);
+
+/* Probe: map + set_access of `n_pages` fresh 2 MiB pages from `n_threads` threads at once
+ * (out[0] µs/page, out[1] total ms, out[2] unmap µs/page). */
+vattn_status vattn_vmm_parallel_probe(int32_t device, int32_t n_pages, int32_t n_threads, double* out);
 
 /* ---- kernels (bf16 K/V/Q/O; layouts in DESIGN.md §3) --------------------------------- */
 /* Write k_new/v_new [batch, n_new, Hkv, D] at rows cache_seqlens[b] + i of slot

@@ -36,7 +36,7 @@ class Config(C.Structure):
         ("eager_groups", c_i64), ("sliced", c_i32),
         ("backend", c_i32), ("device", c_i32), ("release_physical", c_i32),
         ("log_events", c_i32), ("batch_set_access", c_i32),
-        ("latency", C.POINTER(LatencyEntry)), ("n_latency", c_i32),
+        ("latency", C.POINTER(LatencyEntry)), ("n_latency", c_i32), ("prefetch_tokens", c_i32),
     ]
 
 
@@ -52,7 +52,8 @@ class Counters(C.Structure):
         ("init_us", c_f64), ("charged_us", c_f64)] + [(n, c_i64) for n in (
             "real_maps", "real_unmaps", "real_set_access_calls", "real_creates", "real_releases")] + [
         (n, c_f64) for n in ("real_map_wall_us", "real_unmap_wall_us", "real_create_wall_us",
-                             "real_set_access_wall_us", "init_wall_us")]
+                             "real_set_access_wall_us", "init_wall_us")] + [
+        (n, c_i64) for n in ("spec_maps", "spec_hits", "spec_steals", "spec_pages")]
 
 
 class BgResult(C.Structure):
@@ -72,7 +73,7 @@ class IterationResult(C.Structure):
                 ("sync_bg_wall_us", c_f64), ("wall_us", c_f64)]
 
 
-BG_EXECUTE_PLAN, BG_EAGER, BG_RECLAIM, BG_CREDIT, ITER_DEFER = 1, 2, 4, 8, 16
+BG_EXECUTE_PLAN, BG_EAGER, BG_RECLAIM, BG_CREDIT, ITER_DEFER, BG_PREFETCH = 1, 2, 4, 8, 16, 32
 
 # every symbol include/vattn.h declares, with its ctypes signature
 SIGNATURES = {
@@ -94,6 +95,7 @@ SIGNATURES = {
     "vattn_bg_wait": (c_i32, [c_vp, C.POINTER(BgResult)]),
     "vattn_mark_use": (c_i32, [c_vp, c_vp]),
     "vattn_counters_get": (c_i32, [c_vp, C.POINTER(Counters)]),
+    "vattn_counters_peek": (c_i32, [c_vp, C.POINTER(Counters)]),
     "vattn_slot_state": (c_i32, [c_vp, P_i64, c_i64]),
     "vattn_api_count": (c_i32, []),
     "vattn_api_name": (C.c_char_p, [c_i32]),
@@ -113,6 +115,7 @@ SIGNATURES = {
                                    c_i32, c_i32, c_vp, c_f32, c_i32, c_vp, c_i64, c_vp]),
     "vattn_vmm_microbench": (c_i32, [c_i32, c_i64, c_i32, c_i32, C.POINTER(c_f64)]),
     "vattn_vmm_slice_probe": (c_i32, [c_i32, c_i32, c_i32, c_i32, C.POINTER(c_f64)]),
+    "vattn_vmm_parallel_probe": (c_i32, [c_i32, c_i32, c_i32, C.POINTER(c_f64)]),
     "vattn_compute_proxy": (c_i32, [c_u64, c_vp]),
     "vattn_decode_num_splits": (c_i32, [c_i32, c_i32, c_i32]),
     "vattn_decode_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),

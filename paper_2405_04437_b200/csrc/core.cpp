@@ -236,7 +236,12 @@ class Manager {
 
   // ---- real driver ----
   CUmemGenericAllocationHandle real_create();
+  CUmemGenericAllocationHandle take_unattached();
+  CUmemGenericAllocationHandle steal_spec();
   void real_release(CUmemGenericAllocationHandle hnd);
+ public:
+  void prefetch();
+ private:
   void real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle hnd);
   void real_unmap(int32_t b, int64_t off);
   void flush_access();
@@ -287,7 +292,15 @@ class Manager {
   CUdevice cu_dev_ = 0;
   CUcontext ctx_ = nullptr;
   std::vector<CUdeviceptr> va_;
-  std::vector<CUmemGenericAllocationHandle> real_precreated_, real_recycle_;
+  // Physical 2 MiB handles not attached to a shadow handle (pre-created reserve + recycled),
+  // and speculative mappings: pages mapped ahead of the reference's schedule by prefetch().
+  // Invariant: phys_free_.size() + spec_.size() == handles the shadow considers unattached.
+  std::vector<CUmemGenericAllocationHandle> phys_free_;
+  std::unordered_map<int64_t, CUmemGenericAllocationHandle> spec_;   // key b*buffer_size+off
+  std::deque<int64_t> spec_order_;
+  int64_t prefetch_tokens_ = 0;
+  std::atomic<bool> prefetch_cancel_{false};   // set by any join: prefetch is optional work
+  int64_t spec_maps_ = 0, spec_hits_ = 0, spec_steals_ = 0;
   CUmemAllocationProp prop_{};
   CUmemAccessDesc access_{};
   std::vector<int64_t> run_begin_, run_end_;  // pending cuMemSetAccess page runs per buffer
@@ -349,6 +362,7 @@ Manager::Manager(const vattn_config& c) {
   release_physical_ = c.release_physical != 0;
   log_events_ = c.log_events != 0;
   batch_access_ = c.batch_set_access != 0;
+  prefetch_tokens_ = std::max<int64_t>(0, c.prefetch_tokens);
 
   lat_ = LatencyTable::table2();
   if (c.latency && c.n_latency > 0) {
@@ -448,8 +462,12 @@ Manager::~Manager() {
     for (auto& kv : buf_maps_[b]) d.MemUnmap(va_[b] + kv.first, (size_t)t_);
   for (auto& kv : handles_)
     if (kv.second.real) d.MemRelease(kv.second.real);
-  for (auto h : real_precreated_) d.MemRelease(h);
-  for (auto h : real_recycle_) d.MemRelease(h);
+  for (auto& kv : spec_) {
+    const int64_t b = kv.first / buffer_size_, off = kv.first % buffer_size_;
+    d.MemUnmap(va_[b] + off, (size_t)t_);
+    d.MemRelease(kv.second);
+  }
+  for (auto h : phys_free_) d.MemRelease(h);
   for (size_t b = 0; b < va_.size(); ++b) d.MemAddressFree(va_[b], (size_t)buffer_size_);
   if (use_event_) cudaEventDestroy(use_event_);
 }
@@ -500,14 +518,14 @@ double Manager::dev_precreate(int64_t count) {
   if (count < 0) throw Fail(VATTN_VALUE_ERROR, "count must be >= 0");
   if (free_bytes() < count * t_) throw Fail(VATTN_POOL_EXHAUSTED, "cannot pre-create page-groups");
   if (real()) {
-    real_precreated_.reserve((size_t)count);
+    phys_free_.reserve(phys_free_.size() + (size_t)count);
     for (int64_t i = 0; i < count; ++i) {
       CUmemGenericAllocationHandle h = 0;
       const double t0 = now_us();
       check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
       real_create_us_ += now_us() - t0;
       real_creates_ += 1;
-      real_precreated_.push_back(h);
+      phys_free_.push_back(h);
     }
   }
   created_ += count;
@@ -519,10 +537,7 @@ int64_t Manager::dev_take_precreated() {
   if (precreated_ < 1) throw Fail(VATTN_POOL_EXHAUSTED, "no pre-created handles available");
   precreated_ -= 1;
   const int64_t id = new_handle_id();
-  if (real()) {
-    handles_[id].real = real_precreated_.back();
-    real_precreated_.pop_back();
-  }
+  if (real()) handles_[id].real = take_unattached();
   return id;
 }
 
@@ -534,7 +549,18 @@ double Manager::dev_map(int32_t b, int64_t off, int64_t hid) {
   if (off % t_ != 0) throw Fail(VATTN_ALIGNMENT_ERROR, "offset not aligned");
   if (off < 0 || off + t_ > buffer_size_) throw Fail(VATTN_MAPPING_ERROR, "offset out of range");
   if (buf_maps_[b].count(off)) throw Fail(VATTN_MAPPING_ERROR, "offset already backed");
-  if (real()) real_map(b, off, h.real);
+  if (real()) {
+    auto sp = spec_.find((int64_t)b * buffer_size_ + off);
+    if (sp != spec_.end()) {            // prefetched: already mapped and accessible, adopt it
+      if (h.real) phys_free_.push_back(h.real);
+      h.real = sp->second;
+      spec_.erase(sp);
+      spec_hits_ += 1;
+    } else {
+      if (!h.real) h.real = steal_spec();
+      real_map(b, off, h.real);
+    }
+  }
   h.mapped = true;
   h.buf = b;
   h.off = off;
@@ -563,12 +589,68 @@ double Manager::dev_unmap_release(int32_t b, int64_t off) {
 }
 
 // ---- real driver ----------------------------------------------------------------------------
-CUmemGenericAllocationHandle Manager::real_create() {
-  if (!real_recycle_.empty()) {  // a 2 MiB handle whose shadow was released earlier
-    auto h = real_recycle_.back();
-    real_recycle_.pop_back();
+// An unattached physical handle for a shadow handle; 0 = "all of them are holding speculative
+// pages": resolved in dev_map (adopt the page if it is the one being mapped, else steal one).
+CUmemGenericAllocationHandle Manager::take_unattached() {
+  if (!phys_free_.empty()) {
+    auto h = phys_free_.back();
+    phys_free_.pop_back();
     return h;
   }
+  if (spec_.empty()) throw Fail(VATTN_BAD_STATE, "physical pool accounting error");
+  return 0;
+}
+
+CUmemGenericAllocationHandle Manager::steal_spec() {
+  while (!spec_order_.empty()) {
+    const int64_t key = spec_order_.front();
+    spec_order_.pop_front();
+    auto it = spec_.find(key);
+    if (it == spec_.end()) continue;   // already adopted
+    const auto h = it->second;
+    spec_.erase(it);
+    real_unmap((int32_t)(key / buffer_size_), key % buffer_size_);
+    spec_steals_ += 1;
+    return h;
+  }
+  throw Fail(VATTN_BAD_STATE, "no speculative page to steal");
+}
+
+// Physical prefetch (B200 addition, not in the reference): map the pages each active slot will
+// need within `prefetch_tokens_` more tokens ahead of the reference's schedule, from handles the
+// shadow considers unattached.  Logical state (slots, counters, events) is untouched; when the
+// reference logic maps such a page later it adopts the mapping with no driver call.  Keeps one
+// group's worth of handles free so the reference path rarely has to steal.
+void Manager::prefetch() {
+  if (!real() || prefetch_tokens_ <= 0) return;
+  const size_t reserve = (size_t)(2 * buffer_count_);
+  for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+    const Slot& s = slots_[r];
+    if (!s.active) continue;
+    const int64_t target = std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_);
+    for (int64_t g = s.mapped_groups; g < target; ++g) {
+      const int64_t off = slot_offset(r, g);
+      for (int64_t b = 0; b < buffer_count_; ++b) {
+        const int64_t key = b * buffer_size_ + off;
+        if (spec_.count(key) || buf_maps_[b].count(off)) continue;
+        if (phys_free_.size() <= reserve || prefetch_cancel_.load(std::memory_order_relaxed)) {
+          flush_access();
+          return;
+        }
+        const auto h = phys_free_.back();
+        phys_free_.pop_back();
+        real_map((int32_t)b, off, h);
+        spec_[key] = h;
+        spec_order_.push_back(key);
+        spec_maps_ += 1;
+      }
+    }
+  }
+  flush_access();
+}
+
+CUmemGenericAllocationHandle Manager::real_create() {
+  if (!phys_free_.empty() || !spec_.empty()) return take_unattached();
   CUmemGenericAllocationHandle h = 0;
   const double t0 = now_us();
   check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
@@ -578,7 +660,7 @@ CUmemGenericAllocationHandle Manager::real_create() {
 }
 
 void Manager::real_release(CUmemGenericAllocationHandle h) {
-  if (!release_physical_) { real_recycle_.push_back(h); return; }
+  if (!release_physical_) { phys_free_.push_back(h); return; }
   check_cu(driver().MemRelease(h), "cuMemRelease");
   real_releases_ += 1;
 }
@@ -914,6 +996,7 @@ void Manager::bg_loop() {
         res.reclaim_us = r.second;
       }
       flush_access();
+      if (job.flags & VATTN_BG_PREFETCH) prefetch();
     } catch (const Fail& f) {
       st = f.code;
       err = f.what();
@@ -942,6 +1025,7 @@ void Manager::bg_loop() {
 double Manager::join_bg() {
   std::unique_lock<std::mutex> lk(bg_mu_);
   if (bg_completed_ == bg_submitted_) return 0.0;
+  prefetch_cancel_.store(true, std::memory_order_relaxed);
   const double t0 = now_us();
   bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
   return now_us() - t0;
@@ -950,6 +1034,7 @@ double Manager::join_bg() {
 double Manager::join_noncommuting() {
   std::unique_lock<std::mutex> lk(bg_mu_);
   if (bg_completed_ >= bg_last_noncommuting_) return 0.0;
+  prefetch_cancel_.store(true, std::memory_order_relaxed);
   const double t0 = now_us();
   bg_cv_.wait(lk, [&] { return bg_completed_ >= bg_last_noncommuting_; });
   return now_us() - t0;
@@ -964,6 +1049,7 @@ void Manager::bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t 
   job.eager_k = eager_k;
   job.seq = ++bg_submitted_;
   if (flags & (VATTN_BG_EAGER | VATTN_BG_RECLAIM)) bg_last_noncommuting_ = job.seq;
+  prefetch_cancel_.store(false, std::memory_order_relaxed);
   bg_queue_.push_back(std::move(job));
   bg_cv_.notify_all();
 }
@@ -971,6 +1057,7 @@ void Manager::bg_submit(const int64_t* trip, int64_t n, uint32_t flags, int64_t 
 void Manager::bg_wait(vattn_bg_result* out) {
   std::unique_lock<std::mutex> lk(bg_mu_);
   const double t0 = now_us();
+  if (bg_completed_ != bg_submitted_) prefetch_cancel_.store(true, std::memory_order_relaxed);
   bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
   const double waited = now_us() - t0;
   vattn_bg_result r = bg_res_;
@@ -1043,6 +1130,10 @@ void Manager::counters(vattn_counters* o) const {
   o->real_create_wall_us = real_create_us_;
   o->real_set_access_wall_us = real_access_us_;
   o->init_wall_us = init_wall_us_;
+  o->spec_maps = spec_maps_;
+  o->spec_hits = spec_hits_;
+  o->spec_steals = spec_steals_;
+  o->spec_pages = (int64_t)spec_.size();
 }
 
 void Manager::slot_state(int64_t* out) const {
@@ -1347,6 +1438,12 @@ vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out) {
   return api_call(h, [&](Manager& m) { m.counters(out); });
 }
 
+vattn_status vattn_counters_peek(vattn_t* h, vattn_counters* out) {
+  // No join: a snapshot that may race with a running background job (monitoring only).
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->counters(out); });
+}
+
 vattn_status vattn_slot_state(vattn_t* h, int64_t* out, int64_t cap) {
   return api_call(h, [&](Manager& m) {
     if (cap < m.max_batch()) throw Fail(VATTN_VALUE_ERROR, "slot buffer too small");
@@ -1553,6 +1650,51 @@ vattn_status vattn_vmm_slice_probe(int32_t device, int32_t n_pages, int32_t big_
     for (int i = 0; i < extra_handles; ++i) d.MemUnmap(xva + (size_t)i * pg, pg);
     for (auto x : extra) d.MemRelease(x);
     if (extra_handles > 0) d.MemAddressFree(xva, pg * extra_handles);
+  });
+}
+
+
+// Probe: wall time to map + set access `n_pages` 2 MiB pages (fresh handles) using `n_threads`
+// threads concurrently (out[0] = µs per page, out[1] = total ms), then unmap (out[2] µs/page).
+vattn_status vattn_vmm_parallel_probe(int32_t device, int32_t n_pages, int32_t n_threads, double* out) {
+  return guard([&] {
+    using vattn::check_cu;
+    const vattn::Driver& d = vattn::driver();
+    vattn::check_rt(cudaSetDevice(device), "cudaSetDevice");
+    vattn::check_rt(cudaFree(nullptr), "context init");
+    CUcontext ctx = nullptr;
+    check_cu(d.CtxGetCurrent(&ctx), "ctx");
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    const size_t pg = 2u << 20;
+    std::vector<CUmemGenericAllocationHandle> h((size_t)n_pages);
+    for (auto& x : h) check_cu(d.MemCreate(&x, pg, &prop, 0), "cuMemCreate");
+    CUdeviceptr va = 0;
+    check_cu(d.MemAddressReserve(&va, pg * n_pages * 2, pg, 0, 0), "reserve");
+    auto work = [&](int t) {
+      d.CtxSetCurrent(ctx);
+      for (int i = t; i < n_pages; i += n_threads) {
+        const CUdeviceptr p = va + (size_t)(2 * i) * pg;
+        if (d.MemMap(p, pg, 0, h[i], 0) != CUDA_SUCCESS) return;
+        d.MemSetAccess(p, pg, &acc, 1);
+      }
+    };
+    double t0 = vattn::now_us();
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+    out[1] = (vattn::now_us() - t0) / 1e3;
+    out[0] = out[1] * 1e3 / n_pages;
+    t0 = vattn::now_us();
+    for (int i = 0; i < n_pages; ++i) d.MemUnmap(va + (size_t)(2 * i) * pg, pg);
+    out[2] = (vattn::now_us() - t0) / n_pages;
+    d.MemAddressFree(va, pg * n_pages * 2);
+    for (auto x : h) d.MemRelease(x);
   });
 }
 

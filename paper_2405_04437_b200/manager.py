@@ -194,7 +194,7 @@ class KVCacheManager:
 
     def __init__(self, geometry, config, *, backend: str | None = None, device: int | None = None,
                  log_events: bool | None = None, release_physical: bool = False,
-                 batch_set_access: bool = True):
+                 batch_set_access: bool = True, prefetch_tokens: int = 0):
         g = as_geometry(geometry)
         if g.max_batch < 1:
             raise ValueError("geometry.max_batch must be >= 1 to serve requests")
@@ -225,6 +225,7 @@ class KVCacheManager:
         cfg.release_physical = int(release_physical)
         cfg.log_events = int(backend == "shadow" if log_events is None else log_events)
         cfg.batch_set_access = int(batch_set_access)
+        cfg.prefetch_tokens = int(prefetch_tokens)
         lat, n_lat = _latency_entries(getattr(config, "latency_model", None))
         if lat is not None:
             cfg.latency, cfg.n_latency = C.cast(lat[0], C.POINTER(_abi.LatencyEntry)), n_lat
@@ -363,13 +364,15 @@ class KVCacheManager:
 
     # -- the background mapping thread (§6.1.1/§6.1.2; simulator.py:199-203 order) ----------------
     def bg_submit(self, plan=None, *, execute_plan: bool = True, eager: bool = False,
-                  reclaim: bool = False, eager_k: int | None = None, credit: bool = False) -> None:
+                  reclaim: bool = False, eager_k: int | None = None, credit: bool = False,
+                  prefetch: bool = False) -> None:
         """Queue execute_plan → eager_prepare → reclaim on the background thread.  Every other
         call joins the queue first (free_reqid only waits for queued eager/reclaim), so state is
         never mutated concurrently.  credit=True: the plan runs ahead of the next admission;
         alloc_reqid then ranks slots as if it had run after (the reference's order)."""
         flags = ((_abi.BG_EXECUTE_PLAN if execute_plan else 0) | (_abi.BG_EAGER if eager else 0)
-                 | (_abi.BG_RECLAIM if reclaim else 0) | (_abi.BG_CREDIT if credit else 0))
+                 | (_abi.BG_RECLAIM if reclaim else 0) | (_abi.BG_CREDIT if credit else 0)
+                 | (_abi.BG_PREFETCH if prefetch else 0))
         if plan is None or plan is self._last_plan:
             arr, n = None, 0
         else:
@@ -424,10 +427,16 @@ class KVCacheManager:
             "charged_us": c.charged_us,
         }
 
-    def driver_stats(self) -> dict:
+    def peek_counters(self) -> _abi.Counters:
+        """Counters without joining the background thread (monitoring only)."""
+        c = _abi.Counters()
+        check(lib().vattn_counters_peek(self._h, C.byref(c)))
+        return c
+
+    def driver_stats(self, peek: bool = False) -> dict:
         """Measured real-driver cost (CUDA backend)."""
-        c = self._counters()
-        return {k: getattr(c, k) for k, _ in _abi.Counters._fields_ if k.startswith(("real_", "init_wall"))}
+        c = self.peek_counters() if peek else self._counters()
+        return {k: getattr(c, k) for k, _ in _abi.Counters._fields_ if k.startswith(("real_", "init_wall", "spec_"))}
 
     # -- virtual tensors (Table 3 `init` returns the KV cache tensors, PAPER.md:434-437) ---------
     def _view(self, layer: int, kind: int):

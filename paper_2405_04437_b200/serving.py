@@ -67,10 +67,22 @@ class IterationRecord:
     kernel_ms: float = 0.0
     bg_wall_ms: float = 0.0
     deferred: int = 0
+    # real driver activity during this iteration (CUDA backend)
+    drv_maps: int = 0
+    drv_unmaps: int = 0
+    drv_set_access_ms: float = 0.0
+    drv_unmap_ms: float = 0.0
+    drv_create_ms: float = 0.0
+    t_admit_ms: float = 0.0
+    t_bgwait_ms: float = 0.0
+    t_step_ms: float = 0.0
+    t_retire_ms: float = 0.0
 
     REF_FIELDS = ("iteration", "end_ms", "batch", "prefills", "tokens", "compute_ms", "sync_alloc_ms",
                   "stall_ms", "cpu_ms", "committed_bytes", "used_bytes", "alloc_bytes", "preemptions")
-    CSV_FIELDS = REF_FIELDS + ("exposed_ms", "kernel_ms", "bg_wall_ms", "deferred")
+    CSV_FIELDS = REF_FIELDS + ("exposed_ms", "kernel_ms", "bg_wall_ms", "deferred", "drv_maps", "drv_unmaps",
+                               "drv_set_access_ms", "drv_unmap_ms", "drv_create_ms", "t_admit_ms",
+                               "t_bgwait_ms", "t_step_ms", "t_retire_ms")
 
     def row(self, fields=CSV_FIELDS) -> list:
         return [getattr(self, f) for f in fields]
@@ -230,7 +242,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         iteration_model: IterationModel | None = None, preemption_cap: int = 1000,
         backend: str | None = None, defer: bool | None = None, observer=None,
         max_iterations: int | None = None, model: SyntheticModel | None = None,
-        manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None) -> ServingMetrics:
+        manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
+        prefetch_tokens: int = 0) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31)."""
     if mode not in ("sync", "overlapped"):
         raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
@@ -247,7 +260,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         geometry, ManagerConfig(page_group_size=int(page_group_size), pool_bytes=pool_bytes,
                                 reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
                                 sliced=sliced, pre_create_fraction=pre_create_fraction),
-        backend=backend or ("cuda" if wall else "shadow"))
+        backend=backend or ("cuda" if wall else "shadow"), prefetch_tokens=prefetch_tokens)
     if wall and model is None:
         model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1,
                                dense_model=dense_proxy)
@@ -266,6 +279,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     prev_alloc_cum = mgr.vmm.total_mapped_bytes
     t_start = time.perf_counter()
     overlapped = mode == "overlapped"
+    drv_prev = mgr.driver_stats(peek=True) if wall else None
 
     while pending or running:
         if max_iterations is not None and iteration >= max_iterations:
@@ -292,6 +306,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             seq_lens[rid] = rec[1]
         if not running and pending:
             raise SimulationAborted("no request can be admitted into an empty batch")
+        t_adm = time.perf_counter()
         # -- background work + step (line 13) --
         bg_us = 0.0
         bg_wall_ms = 0.0
@@ -299,6 +314,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         if overlapped:
             bgr = mgr.bg_wait()                  # the plan executed during the previous compute
             bg_wall_ms = bgr.bg_wall_us / 1000.0
+        t_bgw = time.perf_counter()
+        if overlapped:
             it_res = mgr.iteration_step(seq_lens, eager=True, reclaim=True, defer=defer)
             bg_us = bgr.plan_us + bgr.eager_us + bgr.reclaim_us + it_res.eager_us + it_res.reclaim_us
             ok, us = it_res.ok, it_res.sync_us
@@ -308,6 +325,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             ok, us = r.ok, r.sync_us
         overflow_us = max(0.0, bg_us - prev_compute_budget_us)
         sync_us = us
+        t_stp = time.perf_counter()
         preempted_here = 0
         while not ok:
             if not running:
@@ -324,16 +342,21 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             r = mgr.step(seq_lens)
             ok = r.ok
             sync_us += r.sync_us
-        exposed_ms = (time.perf_counter() - t_exp) * 1e3
         if observer is not None:
             observer(mgr, list(seq_lens), iteration)
 
         batch = len(running)
         tokens = sum(seq_lens[rid] for rid in running)
         prefills = sum(1 for r in running.values() if r.produced == 0)
-        # quiescent-point counters (before this iteration's plan starts mapping in background)
-        alloc_cum = mgr.vmm.total_mapped_bytes
-        committed = mgr.committed_bytes()
+        # quiescent-point counters (before this iteration's plan starts mapping in background).
+        # Wall clock: peek, so a deferred eager/reclaim job keeps running behind the kernels.
+        if wall:
+            cnt = mgr.peek_counters()
+            alloc_cum, committed = cnt.total_mapped_bytes, cnt.mapped * cnt.page_group_size
+        else:
+            alloc_cum = mgr.vmm.total_mapped_bytes
+            committed = mgr.committed_bytes()
+        exposed_ms = (time.perf_counter() - t_exp) * 1e3
         # -- compute (line 14) + overlapped planning of the next iteration's maps --
         kernel_ms = 0.0
         if wall and batch:
@@ -346,7 +369,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             for rid in running:
                 next_seq[rid] = min(seq_lens[rid] + 1, geometry.max_context)
             plan = mgr.plan_overlap(next_seq)
-            mgr.bg_submit(plan, credit=True)     # maps run on the bg thread during the kernels
+            # maps run on the bg thread during the kernels (+ physical prefetch further ahead)
+            mgr.bg_submit(plan, credit=True, prefetch=prefetch_tokens > 0)
         if wall and batch:
             torch.cuda.synchronize()
             kernel_ms = (time.perf_counter() - t_k) * 1e3
@@ -362,9 +386,19 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             committed_bytes=committed, used_bytes=tokens * token_bytes, alloc_bytes=alloc_cum - prev_alloc_cum,
             preemptions=preempted_here, exposed_ms=exposed_ms if wall else 0.0, kernel_ms=kernel_ms,
             bg_wall_ms=bg_wall_ms, deferred=deferred))
+        if wall:
+            drv = mgr.driver_stats(peek=True)
+            rec = metrics.iterations[-1]
+            rec.drv_maps = drv["real_maps"] - drv_prev["real_maps"]
+            rec.drv_unmaps = drv["real_unmaps"] - drv_prev["real_unmaps"]
+            rec.drv_set_access_ms = (drv["real_set_access_wall_us"] - drv_prev["real_set_access_wall_us"]) / 1e3
+            rec.drv_unmap_ms = (drv["real_unmap_wall_us"] - drv_prev["real_unmap_wall_us"]) / 1e3
+            rec.drv_create_ms = (drv["real_create_wall_us"] - drv_prev["real_create_wall_us"]) / 1e3
+            drv_prev = drv
         prev_alloc_cum = alloc_cum
         prev_compute_budget_us = compute_ms * 1000.0
-        # -- retire (lines 15-22) --
+        # -- retire (lines 15-22); free_reqid waits for deferred eager/reclaim: that is exposed too --
+        t_ret = time.perf_counter()
         for rid in list(running):
             st = running[rid]
             st.produced += 1
@@ -377,6 +411,15 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             else:
                 st.ctx += 1
                 seq_lens[rid] = st.ctx
+        if wall:
+            post = (time.perf_counter() - t_ret) * 1e3
+            rec = metrics.iterations[-1]
+            rec.exposed_ms += post
+            rec.stall_ms += post
+            rec.t_admit_ms = (t_adm - t_exp) * 1e3
+            rec.t_bgwait_ms = (t_bgw - t_adm) * 1e3
+            rec.t_step_ms = (t_stp - t_bgw) * 1e3
+            rec.t_retire_ms = post
         iteration += 1
     if overlapped:
         mgr.bg_wait()

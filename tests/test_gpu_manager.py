@@ -125,3 +125,71 @@ def test_decode_through_manager_l8_shape_with_growth():
         lens = nxt
     assert mgr.slots[rids[-1]].mapped_groups == 2     # 1022+8 tokens crossed 1024
     mgr.close()
+
+
+def test_physical_prefetch_keeps_logical_state_and_data():
+    """Prefetch maps pages ahead of the reference schedule; the logical state must equal the
+    oracle's after every call and kernels must read/write the adopted pages correctly."""
+    _cuda()
+    import random
+
+    from oracle.allocator import Geometry, OracleManager
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention, kv_append
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
+    pool = 24 * 4 * MB2
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool), prefetch_tokens=1500)
+    om = OracleManager(Geometry(2, 8, 128, 2, 4096, 4), MB2, pool_bytes=pool)
+    rng = random.Random(0)
+    gen = torch.Generator().manual_seed(9)
+    host_k = torch.zeros(4, 4096, 8, 128, dtype=torch.bfloat16)
+    host_v = torch.zeros_like(host_k)
+    lens = [0] * 4
+    for it in range(60):
+        if it % 9 == 0 and 0 in lens:
+            r = mgr.alloc_reqid()
+            assert r == om.alloc_reqid()
+            lens[r] = rng.randint(1, 900)
+            new = {r: lens[r]}
+        else:
+            new = {}
+            for r in range(4):
+                if lens[r]:
+                    add = rng.choice([1, 1, 64, 300])
+                    if lens[r] + add <= 4096:
+                        new[r] = add
+                        lens[r] += add
+        res = mgr.step(lens)
+        ok, us = om.step(lens)
+        assert (res.ok, res.sync_us) == (ok, us)
+        for r, n in new.items():          # append the new rows of this step (layer 0)
+            p0 = lens[r] - n
+            kn = torch.randn(1, n, 8, 128, generator=gen).to(torch.bfloat16)
+            vn = torch.randn(1, n, 8, 128, generator=gen).to(torch.bfloat16)
+            host_k[r, p0:lens[r]] = kn[0]
+            host_v[r, p0:lens[r]] = vn[0]
+            kv_append(mgr, 0, kn.to(dev), vn.to(dev), torch.tensor([p0], dtype=torch.int32, device=dev),
+                      torch.tensor([r], dtype=torch.int32, device=dev))
+        act = [r for r in range(4) if lens[r]]
+        q = torch.randn(len(act), 32, 128, generator=gen).to(torch.bfloat16)
+        seq = torch.tensor([lens[r] for r in act], dtype=torch.int32)
+        idx = torch.tensor(act, dtype=torch.int32)
+        out = decode_attention(mgr, 0, q.to(dev), seq.to(dev), idx.to(dev))
+        mgr.bg_submit(execute_plan=False, prefetch=True)   # speculative maps during the kernel
+        ref = decode_ref(q, host_k, host_v, seq, idx)
+        torch.cuda.synchronize()
+        assert max_rel_err(out.cpu(), ref) <= 2e-2, it
+        mgr.bg_wait()
+        st = mgr.parity_state()
+        assert st["mapped"] == om.dev.mapped and st["created"] == om.dev.created
+        assert [s[2] for s in st["slots"]] == [s[2] for s in om.slots]
+        if it % 13 == 12:                 # retire one
+            r = max(act)
+            mgr.free_reqid(r)
+            om.free_reqid(r)
+            lens[r] = 0
+    ds = mgr.driver_stats()
+    assert ds["spec_maps"] > 0 and ds["spec_hits"] > 0
+    mgr.close()

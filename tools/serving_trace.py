@@ -19,6 +19,7 @@ ap.add_argument("--mode", default="overlapped")
 ap.add_argument("--requests", type=int, default=128)
 ap.add_argument("--pool-gib", type=int, default=40)
 ap.add_argument("--no-defer", action="store_true")
+ap.add_argument("--prefetch", type=int, default=0, help="physical prefetch lookahead in tokens")
 ap.add_argument("--out", default=None)
 ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel dense-layer time on the GPU")
 a = ap.parse_args()
@@ -28,14 +29,14 @@ eager = median_prompt_groups(rows, g, MB2)
 m = run(rows, g, mode=a.mode, clock="wall", page_group_size=MB2, pool_bytes=a.pool_gib * 1024 ** 3,
         eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
         preemption_cap=100_000, defer=not a.no_defer,
-        dense_proxy=IterationModel() if a.dense_proxy else None)
+        dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
-          "dense_proxy": a.dense_proxy})
+          "dense_proxy": a.dense_proxy, "prefetch": a.prefetch})
 print(json.dumps(s))
 if a.out:
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
-    tag = a.mode + ("_dense" if a.dense_proxy else "")
+    tag = a.mode + ("_dense" if a.dense_proxy else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
     m.write_iterations_csv(a.out + f"_{tag}.csv")
     with open(a.out + f"_{tag}.json", "w") as fh:
         json.dump(s, fh, indent=1)
