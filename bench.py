@@ -176,7 +176,8 @@ def bench_decode(args, world, rank, local):
     import torch
 
     from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
-    from paper_2405_04437_b200.attention import decode_attention, decode_num_splits, kv_append
+    from paper_2405_04437_b200.attention import (decode_attention, decode_attention_append, decode_num_splits,
+                                                 kv_append)
 
     dev = torch.device("cuda", local)
     g, ctx, wname = decode_geometry(args.workload, world)
@@ -227,12 +228,15 @@ def bench_decode(args, world, rank, local):
         exposed = time.perf_counter() - t_h
         assert r.ok
         p = state["pos"]
-        seqlen = p + 1
         for layer in range(N):
-            kv_append(mgr, layer, kn_[layer], vn_[layer], p, idx)
             if dec_events is not None:
                 dec_events[layer][0].record(stream)
-            decode_attention(mgr, layer, q_[layer], seqlen, idx, out=out_[layer], num_splits=splits)
+            if args.unfused:
+                kv_append(mgr, layer, kn_[layer], vn_[layer], p, idx)
+                decode_attention(mgr, layer, q_[layer], p + 1, idx, out=out_[layer], num_splits=splits)
+            else:   # one launch: append the new token at row p and attend over p + 1 rows
+                decode_attention_append(mgr, layer, q_[layer], kn_[layer], vn_[layer], p, idx,
+                                        out=out_[layer], num_splits=splits)
             if dec_events is not None:
                 dec_events[layer][1].record(stream)
         p.add_(1)
@@ -317,11 +321,13 @@ def bench_decode(args, world, rank, local):
                                       "real_set_access_wall_us", "real_creates", "init_wall_us")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "kernel": "decode_kernel<128,4,false>", "peak_source": pk["source"]},
+                     "kernel": "decode_kernel<128,4,false>" + ("" if args.unfused else " (fused append)"),
+                     "peak_source": pk["source"]},
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "clocks": clk,
-        "gpu_launches": steps * N * (2 + (1 if splits > 1 else 0)),
+        "gpu_launches": steps * N * ((2 if args.unfused else 1) + (1 if splits > 1 else 0)),
+        "decode_kernel_mode": "unfused append+decode" if args.unfused else "fused append+decode (k=/v= semantics)",
     }
     mgr.close()
     return result
@@ -547,6 +553,7 @@ def main(argv=None):
     ap.add_argument("--workload", choices=["l8_decode", "y34_decode"], default="l8_decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip prefill / paged / serving sub-benches")
+    ap.add_argument("--unfused", action="store_true", help="separate kv_append + decode launches per layer")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

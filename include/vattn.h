@@ -223,6 +223,13 @@ vattn_status vattn_kv_append(vattn_t* h, int32_t layer, const void* k_new, const
 vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, int32_t batch,
                           const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
                           float scale, int32_t num_splits /* 0 = auto */, void* stream);
+/* Fused KV-append + decode (flash_attn_with_kvcache k=/v= semantics):
+ * k_new/v_new [batch, Hkv, D] go to row cache_seqlens[b] (length BEFORE the token) of slot
+ * cache_batch_idx[b], and attention runs over cache_seqlens[b] + 1 rows.  One launch. */
+vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const void* k_new,
+                                 const void* v_new, void* out, int32_t batch,
+                                 const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                                 float scale, int32_t num_splits, void* stream);
 /* causal (bottom-right) prefill of q [n_q, Hq, D] against slot rows [0, kv_len). */
 vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                            int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
@@ -250,6 +257,11 @@ vattn_status vattn_decode_raw(const vattn_cache_desc* c, const void* q, void* ou
 vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                int32_t n_q_heads, int32_t req_slot, int32_t kv_len, float scale,
                                int32_t causal, void* stream);
+vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, const void* k_new,
+                                     const void* v_new, void* out, int32_t batch, int32_t n_q_heads,
+                                     const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                                     float scale, int32_t num_splits, void* workspace,
+                                     int64_t workspace_bytes, void* stream);
 /* Paged-layout comparison kernel (PagedAttention block table; PAPER.md:602 block sizes):
  * pools [num_blocks, block_size, Hkv, D], block_table [batch, max_blocks] int32. */
 vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,

@@ -105,6 +105,9 @@ SIGNATURES = {
     "vattn_buffer_base": (c_i32, [c_vp, c_i32, C.POINTER(c_u64)]),
     "vattn_kv_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "vattn_decode": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
+    "vattn_decode_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
+    "vattn_decode_append_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                        c_f32, c_i32, c_vp, c_i64, c_vp]),
     "vattn_prefill": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_f32, c_i32, c_vp]),
     "vattn_kv_append_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "vattn_decode_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_f32,

@@ -77,6 +77,22 @@ def decode_attention(mgr, layer: int, q, cache_seqlens, cache_batch_idx=None, so
     return out
 
 
+def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cache_batch_idx=None,
+                            softmax_scale=None, out=None, num_splits: int = 0, stream=None):
+    """Fused KV-append + decode (flash_attn_with_kvcache k=/v=): k_new/v_new [B, Hkv, D] are
+    written at row cache_seqlens[b] (the length before the token) and attended to, one launch."""
+    _need_cuda(q, k_new, v_new)
+    q, k_new, v_new = _bf16(q, "q"), _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    if out is None:
+        out = torch.empty_like(q)
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    check(lib().vattn_decode_append(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), q.shape[0],
+                                    _ptr(seq), _ptr(idx), float(scale), int(num_splits), C.c_void_p(_stream(stream))))
+    return out
+
+
 def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None, causal=True,
                       softmax_scale=None, out=None, stream=None):
     """Causal (bottom-right aligned) attention of q [S, Hq, D] over rows [0, kv_len) of slot
@@ -147,6 +163,22 @@ def decode_attention_raw(q, k_cache, v_cache, cache_seqlens, cache_batch_idx=Non
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
     check(lib().vattn_decode_raw(C.byref(desc), _ptr(q), _ptr(out), b, hq, _ptr(seq), _ptr(idx), float(scale),
                                  int(num_splits), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+    return out
+
+
+def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx=None,
+                                softmax_scale=None, out=None, num_splits: int = 0, stream=None):
+    desc = cache_desc(k_cache, v_cache)
+    q, k_new, v_new = _bf16(q, "q"), _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    out = torch.empty_like(q) if out is None else out
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    b, hq, d = q.shape
+    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0))
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_decode_append_raw(C.byref(desc), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), b, hq,
+                                        _ptr(seq), _ptr(idx), float(scale), int(num_splits), _ptr(ws), ws.numel(),
+                                        C.c_void_p(_stream(stream))))
     return out
 
 

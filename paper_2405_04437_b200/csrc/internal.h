@@ -76,7 +76,8 @@ void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const 
                       const int32_t* batch_idx, cudaStream_t st);
 void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                    int batch, int hq, const int32_t* seqlens, const int32_t* batch_idx,
-                   float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st);
+                   float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st,
+                   const void* k_new = nullptr, const void* v_new = nullptr);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
                     cudaStream_t st);

@@ -76,6 +76,13 @@ struct DecodeParams {
   int32_t max_blocks, block_size, box_tokens;
   int32_t hq, group, num_splits;
   float scale_log2;
+  // fused append (flash-attn k=/v= semantics): seqlens are the lengths BEFORE the new token,
+  // which is written to row seqlens[b] of the slot and attended to (nullptr = plain decode)
+  const __nv_bfloat16* k_new;   // [batch, hkv, D]
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* k_cache;       // base of the layer's K region (row address computed below)
+  __nv_bfloat16* v_cache;
+  int64_t slot_stride, token_stride;
 };
 
 template <int D, int STAGES>
@@ -104,7 +111,9 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
 
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int seqlen = __ldg(p.seqlens + b);
+  const bool fused = p.k_new != nullptr;
+  const int pos_new = fused ? __ldg(p.seqlens + b) : -1;      // row receiving the new token
+  const int seqlen = fused ? pos_new + 1 : __ldg(p.seqlens + b);
   const int n_tiles_all = (seqlen + kTile - 1) / kTile;
   const int tps = (n_tiles_all + p.num_splits - 1) / p.num_splits;
   const int tile_begin = split * tps;
@@ -190,6 +199,25 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
     const uint32_t vs = ks + L::kTileBytes;
     const int my_tok0 = (tile_begin + it) * kTile + warp * 16;
     const int valid = min(16, seqlen - my_tok0);
+    if (fused && pos_new >= my_tok0 && pos_new < my_tok0 + 16) {
+      // This warp owns the new token's row: patch it into the landed smem tile (the TMA copy
+      // may predate the global write) and persist it to the cache.  Lanes 0-15 carry K,
+      // 16-31 V; D/8 16-byte chunks per row.
+      const int r = pos_new - (tile_begin + it) * kTile;
+      const int64_t src = ((int64_t)b * (p.hq / p.group) + kvh) * D;
+      const int64_t dst = (int64_t)slot * p.slot_stride + (int64_t)pos_new * p.token_stride +
+                          (int64_t)kvh * D * 2;
+      for (int c = lane % 16; c < D / 8; c += 16) {
+        const bool is_v = lane >= 16;
+        const uint4 val = *reinterpret_cast<const uint4*>((is_v ? p.v_new : p.k_new) + src + c * 8);
+        const uint32_t a = ptx::swz128((is_v ? vs : ks) + (c >> 3) * L::kHalfBytes, r, c & 7);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(val.x), "r"(val.y), "r"(val.z),
+                     "r"(val.w));
+        *reinterpret_cast<uint4*>(reinterpret_cast<char*>(is_v ? p.v_cache : p.k_cache) + dst + c * 16) = val;
+      }
+      __syncwarp();
+      ptx::fence_proxy_async();
+    }
     if (valid > 0) {
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
@@ -481,11 +509,18 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
   }
 }
 
+struct FusedAppend {
+  const void* k_new;
+  const void* v_new;
+  const CacheView* view;
+};
+
 static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, int hkv, int hq,
                           const void* q, void* out, int batch, const int32_t* seqlens,
                           const int32_t* batch_idx, const int32_t* block_table, int max_blocks,
                           int block_size, int box_tokens, float scale, int num_splits,
-                          int max_len, void* ws, int64_t ws_bytes, bool paged, cudaStream_t st) {
+                          int max_len, void* ws, int64_t ws_bytes, bool paged, cudaStream_t st,
+                          const FusedAppend* fa = nullptr) {
   if (hq % hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
   const int group = hq / hkv;
   if (group > 16) throw Fail(VATTN_UNSUPPORTED, "GQA group larger than 16");
@@ -506,6 +541,14 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   p.num_splits = num_splits;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)d);
   p.scale_log2 = scale * 1.4426950408889634f;
+  if (fa) {
+    p.k_new = reinterpret_cast<const __nv_bfloat16*>(fa->k_new);
+    p.v_new = reinterpret_cast<const __nv_bfloat16*>(fa->v_new);
+    p.k_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->k_base);
+    p.v_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->v_base);
+    p.slot_stride = fa->view->slot_stride;
+    p.token_stride = fa->view->token_stride;
+  }
   if (num_splits > 1) {
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, d, num_splits);
     if (!ws || ws_bytes < need) throw Fail(VATTN_VALUE_ERROR, "decode workspace too small");
@@ -524,7 +567,8 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
 
 void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void* out, int batch,
                    int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
-                   int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                   int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st, const void* k_new,
+                   const void* v_new) {
   check_view(v);
   // Token extent = every row inside the slot stride, so a 64-row tile that starts below seqlen
   // never takes TMA's out-of-bounds path (which faults on VMM-backed maps when the box
@@ -533,8 +577,9 @@ void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void
   const int tokens = (int)std::max<int64_t>(v.slot_tokens, std::min<int64_t>(rows, INT32_MAX));
   const CUtensorMap km = cached_map(ks, v.k_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
   const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
+  FusedAppend fa{k_new, v_new, &v};
   decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
-                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st);
+                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr);
 }
 
 }  // namespace vattn
@@ -594,7 +639,19 @@ vattn_status vattn_decode_raw(const vattn_cache_desc* c, const void* q, void* ou
   return kguard([&] {
     const vattn::CacheView v = vattn::view_from_desc(c);
     vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, seqlens, batch_idx, scale, num_splits,
-                         ws, ws_bytes, (cudaStream_t)stream);
+                         ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr);
+  });
+}
+
+vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, const void* k_new,
+                                     const void* v_new, void* out, int32_t batch, int32_t hq,
+                                     const int32_t* cache_seqlens, const int32_t* batch_idx,
+                                     float scale, int32_t num_splits, void* ws, int64_t ws_bytes,
+                                     void* stream) {
+  return kguard([&] {
+    const vattn::CacheView v = vattn::view_from_desc(c);
+    vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
+                         num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
   });
 }
 

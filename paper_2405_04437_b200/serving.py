@@ -193,7 +193,7 @@ class SyntheticModel:
 
     def forward(self, prefills, decodes) -> None:
         """prefills: [(slot, prompt_len)]; decodes: [(slot, ctx)] (ctx includes the new token)."""
-        from .attention import decode_attention, kv_append, prefill_attention
+        from .attention import decode_attention_append, kv_append, prefill_attention
 
         t = self.t
         for slot, n in prefills:
@@ -204,11 +204,10 @@ class SyntheticModel:
         if decodes:
             B = len(decodes)
             idx = t.tensor([s for s, _ in decodes], dtype=t.int32, device=self.dev)
-            after = t.tensor([c for _, c in decodes], dtype=t.int32, device=self.dev)
-            before = after - 1
-            for layer in range(self.layers):
-                kv_append(self.mgr, layer, self.k_dec[:B], self.v_dec[:B], before, idx)
-                decode_attention(self.mgr, layer, self.q_dec[:B], after, idx, out=self.out_dec[:B])
+            before = t.tensor([c - 1 for _, c in decodes], dtype=t.int32, device=self.dev)
+            for layer in range(self.layers):   # fused: append row ctx-1 and attend over ctx rows
+                decode_attention_append(self.mgr, layer, self.q_dec[:B], self.k_dec[:B], self.v_dec[:B],
+                                        before, idx, out=self.out_dec[:B])
         if self.dense_model is not None:
             # the dense layers (QKV/O projections, MLP) of the iteration, as device time
             import ctypes as C

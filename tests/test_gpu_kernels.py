@@ -128,3 +128,26 @@ def test_kv_append_raw_bit_exact():
         kv_append_raw(kd, vd, kn.to(dev), vn.to(dev), seq.to(dev), idx.to(dev))
         assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)
         k, v = kr, vr
+
+
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_fused_append_decode_matches_append_then_decode(splits):
+    """flash-attn k=/v= semantics: the new row is written at cache_seqlens[b] and attended to."""
+    from paper_2405_04437_b200.attention import decode_attention_append_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(21)
+    B, hq, hkv, d, L = 5, 56, 8, 128, 1024
+    k, v = _mk_cache(B + 1, L, hkv, d, gen)
+    lens = torch.tensor([0, 63, 64, 500, 1023], dtype=torch.int32)   # lengths BEFORE the token
+    idx = torch.tensor([5, 0, 3, 1, 2], dtype=torch.int32)
+    q = _rand((B, hq, d), gen)
+    kn, vn = _rand((B, hkv, d), gen), _rand((B, hkv, d), gen)
+    kr, vr = kv_append_ref(k, v, kn.unsqueeze(1), vn.unsqueeze(1), lens, idx)
+    ref = decode_ref(q, kr, vr, lens + 1, idx)
+    kd, vd = k.to(dev), v.to(dev)
+    out = decode_attention_append_raw(q.to(dev), kd, vd, kn.to(dev), vn.to(dev), lens.to(dev), idx.to(dev),
+                                      num_splits=splits)
+    torch.cuda.synchronize()
+    assert max_rel_err(out.cpu(), ref) <= TOL
+    assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)
