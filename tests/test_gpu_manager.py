@@ -193,3 +193,47 @@ def test_physical_prefetch_keeps_logical_state_and_data():
     ds = mgr.driver_stats()
     assert ds["spec_maps"] > 0 and ds["spec_hits"] > 0
     mgr.close()
+
+
+def test_sliced_layout_kernels():
+    """Layer-sliced layout ([B, L, N, H, D], manager.py:93-96): two buffers,
+    token stride N·H·D·P; the same kernels serve it through the layer view."""
+    _cuda()
+    from oracle.attention import prefill_ref
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention_append, kv_append, prefill_attention
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(3, 4, 128, 2, max_context=2048, max_batch=3, n_q_heads_total=16)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, sliced=True))
+    assert mgr.buffer_count == 2
+    r = mgr.alloc_reqid()
+    lens = [0, 0, 0]
+    S = 700
+    lens[r] = S + 1
+    assert mgr.step(lens).ok
+    gen = torch.Generator().manual_seed(4)
+    for layer in range(3):
+        kn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
+        vn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
+        q = torch.randn(S, 16, 128, generator=gen).to(torch.bfloat16)
+        kv_append(mgr, layer, kn.to(dev), vn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                  torch.tensor([r], dtype=torch.int32, device=dev))
+        out = prefill_attention(mgr, layer, q.to(dev), r)
+        torch.cuda.synchronize()
+        assert max_rel_err(out.cpu(), prefill_ref(q, kn[0], vn[0])) <= 2e-2
+        # decode one more token with the fused kernel
+        k1 = torch.randn(1, 4, 128, generator=gen).to(torch.bfloat16)
+        v1 = torch.randn(1, 4, 128, generator=gen).to(torch.bfloat16)
+        q1 = torch.randn(1, 16, 128, generator=gen).to(torch.bfloat16)
+        o1 = decode_attention_append(mgr, layer, q1.to(dev), k1.to(dev), v1.to(dev),
+                                     torch.tensor([S], dtype=torch.int32, device=dev),
+                                     torch.tensor([r], dtype=torch.int32, device=dev))
+        kc = torch.cat([kn[0], k1], 0).unsqueeze(0)
+        vc = torch.cat([vn[0], v1], 0).unsqueeze(0)
+        ref = decode_ref(q1, kc, vc, torch.tensor([S + 1], dtype=torch.int32))
+        torch.cuda.synchronize()
+        assert max_rel_err(o1.cpu(), ref) <= 2e-2
+        # the view sees the sliced strides
+        assert torch.equal(mgr.k_cache(layer)[r, :S].cpu(), kn[0])
+    mgr.close()
