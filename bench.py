@@ -275,6 +275,11 @@ def bench_decode(args, world, rank, local):
     dec_us = statistics.mean(dec_ms) * 1e3
     pk = peaks()
     achieved = dec_bytes / (dec_us * 1e-6) / 1e9
+    kernel_name = "decode_kernel<128,4,false>" + ("" if args.unfused else " (fused append)")
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists() and args.workload == "l8_decode":
+        traffic = json.loads(tf.read_text()).get(kernel_name, {}).get("traffic_bytes")
 
     # ---- e2e through the public API with host buffers (pinned) ----
     qh = q.cpu().pin_memory()
@@ -320,9 +325,9 @@ def bench_decode(args, world, rank, local):
         "driver": {k: st[k] for k in ("real_maps", "real_set_access_calls", "real_map_wall_us",
                                       "real_set_access_wall_us", "real_creates", "init_wall_us")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "kernel": "decode_kernel<128,4,false>" + ("" if args.unfused else " (fused append)"),
-                     "peak_source": pk["source"]},
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes": dec_bytes, "kernel": kernel_name,
+                     "peak_source": pk["source"], "traffic_source": "profiles/ncu_traffic.json (ncu --set full)"},
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "clocks": clk,
