@@ -58,8 +58,8 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 // instruction descriptor, kind::f16: bf16 x bf16 -> f32, M=128, N=128
-__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((kBN >> 3) << 17) |
+__host__ __device__ constexpr uint32_t idesc(bool b_mn_major, int n = 128) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
          ((kBM >> 4) << 24);
 }
 __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -434,6 +434,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   }
 }
 
+
 }  // namespace pf
 
 static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
@@ -488,7 +489,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.scale_log2 = scale * 1.4426950408889634f;
   static int poly = -1;
   if (poly < 0) {
-    const char* e = getenv("VATTN_PF_POLY");
+    const char* e = getenv("VATTN_PF_POLY");   // share of exp2 on the FMA pipe, in quarters
     poly = e ? std::max(0, std::min(3, atoi(e))) : 1;
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
