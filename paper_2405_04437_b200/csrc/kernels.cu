@@ -479,10 +479,12 @@ void launch_kv_append(KernelState*, int, const CacheView& v, const void* k_new, 
 constexpr int kMaxSplits = 64;
 
 static int auto_splits(int units, int max_len) {
+  // Measured on B200 (tools/decode_split_sweep.py): one CTA per (batch row, KV head) already
+  // streams at full HBM bandwidth once ~128 of them run (deep 4-stage TMA ring per CTA), so
+  // split only below that; keep >= 4 tiles (256 tokens) per split.
   const int tiles = std::max(1, (max_len + kTile - 1) / kTile);
-  const int target = num_sms() * 2;  // two resident CTAs per SM
-  int s = (target + units - 1) / units;
-  s = std::min(s, std::max(1, tiles / 4));  // keep >= 4 tiles (256 tokens) per split
+  int s = (128 + units - 1) / units;
+  s = std::min(s, std::max(1, tiles / 4));
   return std::max(1, std::min(s, kMaxSplits));
 }
 
