@@ -219,7 +219,7 @@ def bench_decode(args, world, rank, local):
     state = {"seq": list(seq), "pos": pos}
     splits = decode_num_splits(B, hkv, ctx + 1)
 
-    def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out):
+    def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out, pre_layer=None, post_layer=None):
         nxt = list(state["seq"])
         for r in rids:
             nxt[r] += 1
@@ -229,6 +229,8 @@ def bench_decode(args, world, rank, local):
         assert r.ok
         p = state["pos"]
         for layer in range(N):
+            if pre_layer is not None:
+                pre_layer(layer)
             if dec_events is not None:
                 dec_events[layer][0].record(stream)
             if args.unfused:
@@ -239,6 +241,8 @@ def bench_decode(args, world, rank, local):
                                         out=out_[layer], num_splits=splits)
             if dec_events is not None:
                 dec_events[layer][1].record(stream)
+            if post_layer is not None:
+                post_layer(layer)
         p.add_(1)
         state["seq"] = nxt
         nn = list(nxt)
@@ -288,12 +292,35 @@ def bench_decode(args, world, rank, local):
     q_d, kn_d, vn_d = torch.empty_like(q), torch.empty_like(kn), torch.empty_like(vn)
     e2e_steps = max(3, min(steps, 20))
 
+    # Per-layer pipelined transfers: layer l's q/k/v H2D (one copy stream) and its output D2H
+    # (a second stream, PCIe is full duplex) overlap the kernels of the neighbouring layers.
+    h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    h2d_ev = [torch.cuda.Event() for _ in range(N)]
+    done_ev = [torch.cuda.Event() for _ in range(N)]
+    first = [True]
+
+    def pre_layer(layer):
+        stream.wait_event(h2d_ev[layer])
+
+    def post_layer(layer):
+        done_ev[layer].record(stream)
+        d2h_s.wait_event(done_ev[layer])
+        with torch.cuda.stream(d2h_s):
+            outh[layer].copy_(out[layer], non_blocking=True)
+
     def e2e_step():
-        q_d.copy_(qh, non_blocking=True)
-        kn_d.copy_(knh, non_blocking=True)
-        vn_d.copy_(vnh, non_blocking=True)
-        one_step(None, q_d, kn_d, vn_d, out)
-        outh.copy_(out, non_blocking=True)
+        h2d_s.wait_stream(stream)
+        with torch.cuda.stream(h2d_s):
+            for layer in range(N):
+                if not first[0]:
+                    h2d_s.wait_event(done_ev[layer])     # previous step finished reading layer l
+                q_d[layer].copy_(qh[layer], non_blocking=True)
+                kn_d[layer].copy_(knh[layer], non_blocking=True)
+                vn_d[layer].copy_(vnh[layer], non_blocking=True)
+                h2d_ev[layer].record(h2d_s)
+        first[0] = False
+        one_step(None, q_d, kn_d, vn_d, out, pre_layer=pre_layer, post_layer=post_layer)
+        stream.wait_stream(d2h_s)                       # the step ends when its outputs are on the host
 
     e2e_step()
     torch.cuda.synchronize()
