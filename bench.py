@@ -412,13 +412,28 @@ def extra_prefill(local):
     flops = 2.0 * S * S * 128 * 32
     tf = flops / (pf_ms * 1e-3) / 1e12
     app_bytes = 2 * 2 * S * 4 * 128 * 2
+    # paged-layout variant of the same kernel on identical K/V (PAPER.md:606-623 comparison)
+    from paper_2405_04437_b200.attention import prefill_attention_paged
+    paged = {}
+    kc, vc = mgr.k_cache(0)[rid, :S].contiguous(), mgr.v_cache(0)[rid, :S].contiguous()
+    for bs in (16, 256):
+        nb = S // bs
+        perm = torch.randperm(nb, device=dev, generator=gen)
+        kp = torch.empty(nb, bs, 4, 128, device=dev, dtype=torch.bfloat16)
+        vp = torch.empty_like(kp)
+        kp[perm] = kc.view(nb, bs, 4, 128)
+        vp[perm] = vc.view(nb, bs, 4, 128)
+        bt = perm.to(torch.int32)
+        ms = _time_ms(lambda: prefill_attention_paged(q, kp, vp, bt, S), iters=10)
+        paged[f"paged_bs{bs}_ms"] = ms
+        paged[f"paged_bs{bs}_slowdown"] = ms / pf_ms
     mgr.close()
     return {"workload": "yi-6b prefill 16K causal (1 layer, 32 Q / 4 KV heads, D 128)",
             "prefill_ms": pf_ms, "prefill_tflops": tf,
             "prefill_frac_of_measured_burst": tf / pk["bf16_tflops"], "prefill_frac_of_2250_nominal": tf / 2250.0,
             "flops": flops, "append_us": app_ms * 1e3, "append_gbs": app_bytes / (app_ms * 1e-3) / 1e9,
             "append_frac_hbm": app_bytes / (app_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "map_16k_prompt_ms": map_ms}
+            "map_16k_prompt_ms": map_ms, **paged}
 
 
 def extra_paged(local):

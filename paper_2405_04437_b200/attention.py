@@ -217,3 +217,20 @@ def prefill_attention_raw(q, k_cache, v_cache, req_slot: int, kv_len: int, causa
     check(lib().vattn_prefill_raw(C.byref(desc), _ptr(q), _ptr(out), n_q, hq, int(req_slot), int(kv_len),
                                   float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
     return out
+
+
+def prefill_attention_paged(q, k_pool, v_pool, block_table, kv_len: int, causal=True, softmax_scale=None,
+                            out=None, stream=None):
+    """PagedAttention-layout comparison for prefill: the same tcgen05 kernel, K/V tiles gathered
+    block by block through `block_table` [max_blocks] (one request).  Pool rows past kv_len in the
+    last block must be finite (they are multiplied by zero)."""
+    _need_cuda(q, k_pool, v_pool)
+    q, k_pool, v_pool = _bf16(q, "q"), _bf16(k_pool, "k_pool"), _bf16(v_pool, "v_pool")
+    out = torch.empty_like(q) if out is None else out
+    bt = _i32(block_table, "block_table")
+    n_q, hq, d = q.shape
+    nb, bs, hkv, _ = k_pool.shape
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_prefill_paged(_ptr(q), _ptr(k_pool), _ptr(v_pool), nb, bs, hkv, d, _ptr(bt), int(kv_len),
+                                    _ptr(out), n_q, hq, float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
+    return out

@@ -49,6 +49,9 @@ struct Params {
   int q_off;               // kv_len - n_q  (bottom-right causal alignment)
   int causal;
   float scale_log2;
+  // paged comparison variant: K/V tiles gathered block by block through a block table
+  const int32_t* block_table;
+  int block_size, box_tokens;
 };
 
 // ---- tcgen05 wrappers -------------------------------------------------------------------
@@ -186,7 +189,7 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
-template <int POLY>
+template <int POLY, bool PAGED = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, Params p) {
@@ -250,15 +253,39 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const int s = j % kStages;
         if (j >= kStages) ptx::mbar_wait(&kv_empty[s], ((j / kStages) - 1) & 1);
         ptx::mbar_arrive_expect_tx(&k_full[s], kTileBytes);
+        if constexpr (!PAGED) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          ptx::tma_load_3d(smem + kKOff + s * kTileBytes + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
-                           j * kBN);
-        ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            ptx::tma_load_3d(smem + kKOff + s * kTileBytes + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
+                             j * kBN);
+          ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          ptx::tma_load_3d(smem + kVOff + s * kTileBytes + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
-                           j * kBN);
+          for (int h = 0; h < 2; ++h)
+            ptx::tma_load_3d(smem + kVOff + s * kTileBytes + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
+                             j * kBN);
+        } else {
+          // PagedAttention layout: one TMA box per KV block (4-D map over [D, Hkv, block, n_blocks])
+          const int last_blk = (p.kv_len - 1) / p.block_size;
+          for (int sub = 0; sub < kBN / p.box_tokens; ++sub) {
+            const int tok = j * kBN + sub * p.box_tokens;
+            const int blk = __ldg(p.block_table + min(tok / p.block_size, last_blk));
+            const int within = tok % p.block_size;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ptx::tma_load_4d(smem + kKOff + s * kTileBytes + h * kHalf + sub * p.box_tokens * 128, &kmap,
+                               &k_full[s], h * 64, kvh, within, blk);
+          }
+          ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+          for (int sub = 0; sub < kBN / p.box_tokens; ++sub) {
+            const int tok = j * kBN + sub * p.box_tokens;
+            const int blk = __ldg(p.block_table + min(tok / p.block_size, last_blk));
+            const int within = tok % p.block_size;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ptx::tma_load_4d(smem + kVOff + s * kTileBytes + h * kHalf + sub * p.box_tokens * 128, &vmap,
+                               &v_full[s], h * 64, kvh, within, blk);
+          }
+        }
       }
     }
   } else if (warp == 9) {
@@ -504,7 +531,70 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
+void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool, int num_blocks,
+                          int block_size, int hkv, const int32_t* block_table, int kv_len, void* out,
+                          int n_q, int hq, float scale, bool causal, cudaStream_t st) {
+  if (hq % hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
+  if (block_size <= 0 || (block_size < pf::kBN && pf::kBN % block_size) ||
+      (block_size >= pf::kBN && block_size % pf::kBN))
+    throw Fail(VATTN_UNSUPPORTED, "block_size must divide 128 or be a multiple of 128");
+  if (n_q <= 0 || kv_len <= 0) return;
+  const int box = std::min(block_size, pf::kBN);
+  cuuint64_t qd[3] = {(cuuint64_t)pf::kD, (cuuint64_t)hq, (cuuint64_t)n_q};
+  cuuint64_t qs[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)hq * pf::kD * 2};
+  cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
+  const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  const uint64_t row = (uint64_t)hkv * pf::kD * 2;
+  cuuint64_t kd[4] = {(cuuint64_t)pf::kD, (cuuint64_t)hkv, (cuuint64_t)block_size, (cuuint64_t)num_blocks};
+  cuuint64_t ks[3] = {(cuuint64_t)pf::kD * 2, row, row * block_size};
+  cuuint32_t kb[4] = {64, 1, (cuuint32_t)box, 1};
+  const CUtensorMap kmap = make_map(const_cast<void*>(k_pool), 4, kd, ks, kb);
+  const CUtensorMap vmap = make_map(const_cast<void*>(v_pool), 4, kd, ks, kb);
+  pf::Params p{};
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.n_q = n_q;
+  p.hq = hq;
+  p.group = hq / hkv;
+  p.kv_len = kv_len;
+  p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
+  p.q_off = kv_len - n_q;
+  p.causal = causal ? 1 : 0;
+  if (scale <= 0.f) scale = 1.f / sqrtf((float)pf::kD);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.block_table = block_table;
+  p.block_size = block_size;
+  p.box_tokens = box;
+  static bool attr = false;
+  if (!attr) {
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  pf::kSmemBytes), "smem attr");
+    attr = true;
+  }
+  dim3 grid(p.n_pairs, hq);
+  pf::prefill_kernel<1, true><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  check_rt(cudaGetLastError(), "prefill (paged) launch");
+}
+
 }  // namespace vattn
+
+extern "C" vattn_status vattn_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
+                                            int32_t num_blocks, int32_t block_size, int32_t n_kv_heads,
+                                            int32_t head_dim, const int32_t* block_table, int32_t kv_len,
+                                            void* out, int32_t n_q, int32_t n_q_heads, float scale,
+                                            int32_t causal, void* stream) {
+  try {
+    if (head_dim != vattn::pf::kD) throw vattn::Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 128");
+    vattn::launch_prefill_paged(q, k_pool, v_pool, num_blocks, block_size, n_kv_heads, block_table, kv_len, out,
+                                n_q, n_q_heads, scale, causal != 0, (cudaStream_t)stream);
+    return VATTN_OK;
+  } catch (const vattn::Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
+}
 
 extern "C" vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                           int32_t hq, int32_t slot, int32_t kv_len, float scale,

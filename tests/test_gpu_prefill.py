@@ -96,3 +96,28 @@ def test_prefill_through_manager_after_append():
     ref = prefill_ref(q, kn[0], vn[0])
     assert max_rel_err(out.cpu(), ref) <= TOL
     mgr.close()
+
+
+@pytest.mark.parametrize("block_size", [16, 128, 256])
+def test_prefill_paged_matches_contiguous(block_size):
+    """The paged-layout comparison kernel computes the same attention as the contiguous one."""
+    from paper_2405_04437_b200.attention import prefill_attention_paged, prefill_attention_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(12)
+    S, hq, hkv = 1000, 32, 4
+    nb = (S + block_size - 1) // block_size
+    k = torch.randn(1, nb * block_size, hkv, 128, generator=gen).to(torch.bfloat16)
+    v = torch.randn(1, nb * block_size, hkv, 128, generator=gen).to(torch.bfloat16)
+    q = torch.randn(S, hq, 128, generator=gen).to(torch.bfloat16)
+    perm = torch.randperm(nb + 5, generator=gen)[:nb]
+    kp = torch.randn(nb + 5, block_size, hkv, 128, generator=gen).to(torch.bfloat16)
+    vp = torch.randn(nb + 5, block_size, hkv, 128, generator=gen).to(torch.bfloat16)
+    kp[perm] = k[0].view(nb, block_size, hkv, 128)
+    vp[perm] = v[0].view(nb, block_size, hkv, 128)
+    ref = prefill_ref(q, k[0, :S], v[0, :S])
+    out_p = prefill_attention_paged(q.to(dev), kp.to(dev), vp.to(dev), perm.to(torch.int32).to(dev), S)
+    out_c = prefill_attention_raw(q.to(dev), k.to(dev), v.to(dev), 0, S)
+    torch.cuda.synchronize()
+    assert max_rel_err(out_p.cpu(), ref) <= TOL
+    assert torch.equal(out_p.cpu(), out_c.cpu())
