@@ -472,6 +472,36 @@ def extra_paged(local):
     return res
 
 
+def extra_y34_shards(local):
+    """BASELINE config 4 per rank: Yi-34B decode (B 128, ctx 8K, 56 Q / 8 KV heads) with KV heads
+    sharded over G GPUs — each rank's shard measured on this GPU (no collective on the path, so
+    G ranks run these in parallel; the optional output all-gather is excluded)."""
+    import torch
+
+    from paper_2405_04437_b200.attention import decode_attention_append_raw
+
+    dev = torch.device("cuda", local)
+    B, L = 128, 8192
+    pk = peaks()
+    out = {}
+    for G in (1, 2, 4, 8):
+        hq, hkv = 56 // G, 8 // G
+        gen = torch.Generator(device=dev).manual_seed(G)
+        k = torch.randn(B, L + 64, hkv, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        v = torch.randn_like(k)
+        q = torch.randn(B, hq, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        kn = torch.randn(B, hkv, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        vn = torch.randn_like(kn)
+        pos = torch.full((B,), L - 1, dtype=torch.int32, device=dev)
+        us = _time_ms(lambda: decode_attention_append_raw(q, k, v, kn, vn, pos), iters=10) * 1e3
+        byt = 2 * B * L * hkv * 128 * 2 + 2 * B * hq * 128 * 2
+        out[f"G{G}"] = {"hq": hq, "hkv": hkv, "us_per_layer": us, "gbs": byt / (us * 1e-6) / 1e9,
+                        "frac_hbm": byt / (us * 1e-6) / 1e9 / pk["hbm_gbs"], "bytes_per_gpu": byt,
+                        "job_tokens_per_s_per_layer": B / (us * 1e-6)}
+        del k, v
+    return out
+
+
 def extra_serving(local, requests=48):
     """BASELINE config 5: Algorithm-1 loop on the config-5 trace (Llama-3-8B shape), real kernels
     + dense-layer compute proxy (reference IterationModel), sync vs overlapped+deferred+eager."""
@@ -630,7 +660,7 @@ def main(argv=None):
         if not args.no_extras and world == 1:
             extras = {}
             for name, fn in (("prefill", extra_prefill), ("paged_vs_contiguous", extra_paged),
-                             ("serving", extra_serving)):
+                             ("y34_shards", extra_y34_shards), ("serving", extra_serving)):
                 try:
                     extras[name] = fn(local)
                 except Exception as e:   # an extra must not void the headline line
