@@ -506,7 +506,7 @@ def extra_serving(local, requests=48):
     """BASELINE config 5: Algorithm-1 loop on the config-5 trace (Llama-3-8B shape), real kernels
     + dense-layer compute proxy (reference IterationModel), sync vs overlapped+deferred+eager."""
     from paper_2405_04437_b200.geometry import llama3_8b
-    from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run
+    from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run, run_paged
 
     rows = load_trace_csv(ROOT / "tests" / "golden" / "trace_config5.csv")[:requests]
     g = llama3_8b(max_context=4096, max_batch=64)
@@ -528,6 +528,15 @@ def extra_serving(local, requests=48):
                                              ("t_admit_ms", "t_bgwait_ms", "t_step_ms", "t_retire_ms")}
         out[mode]["driver_set_access_ms_total"] = sum(r.drv_set_access_ms for r in its)
         out[mode]["driver_maps_total"] = sum(r.drv_maps for r in its)
+        out[mode]["kernel_ms_total"] = s["kernel_ms_total"]
+    # PagedAttention layout with the in-repo paged kernels (block 16), same trace and proxy
+    import torch
+    torch.cuda.empty_cache()
+    m = run_paged(rows, g, block_size=16, pool_bytes=24 * GIB, dense_proxy=IterationModel(), device=local)
+    s = m.summary()
+    out["paged_bs16"] = {k: s[k] for k in ("iterations", "tokens_per_s", "exposed_map_ms_per_iter",
+                                           "kernel_ms_total", "preemptions")}
+    out["paged_bs16"]["note"] = "exposed = host block allocation + block-table preparation + upload"
     return out
 
 

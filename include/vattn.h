@@ -275,6 +275,12 @@ vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v
 vattn_status vattn_compute_proxy(uint64_t ns, void* stream);
 /* split count the auto heuristic picks for `batch` rows x Hkv heads at max_seqlen tokens */
 int32_t vattn_decode_num_splits(int32_t batch, int32_t n_kv_heads, int32_t max_seqlen);
+/* Paged-layout append (comparison path): row cache_seqlens[b] + i of sequence b goes to block
+ * block_table[b][pos / block_size], row pos % block_size of pools [num_blocks, block_size, Hkv, D]. */
+vattn_status vattn_kv_append_paged(const void* k_new, const void* v_new, void* k_pool, void* v_pool,
+                                   int32_t block_size, int32_t n_kv_heads, int32_t head_dim,
+                                   const int32_t* block_table, int32_t max_blocks_per_seq, int32_t batch,
+                                   int32_t n_new, const int32_t* cache_seqlens, void* stream);
 /* Paged-layout causal prefill (same tcgen05 kernel, K/V gathered per block): pools
  * [num_blocks, block_size, Hkv, D], block_table [max_blocks] int32 for the one request. */
 vattn_status vattn_prefill_paged(const void* q, const void* k_pool, const void* v_pool,

@@ -116,6 +116,8 @@ SIGNATURES = {
                                   c_f32, c_i32, c_vp]),
     "vattn_decode_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp,
                                    c_i32, c_i32, c_vp, c_f32, c_i32, c_vp, c_i64, c_vp]),
+    "vattn_kv_append_paged": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_i32,
+                                      c_vp, c_vp]),
     "vattn_prefill_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp, c_i32, c_i32,
                                     c_f32, c_i32, c_vp]),
     "vattn_vmm_microbench": (c_i32, [c_i32, c_i64, c_i32, c_i32, C.POINTER(c_f64)]),

@@ -234,3 +234,18 @@ def prefill_attention_paged(q, k_pool, v_pool, block_table, kv_len: int, causal=
     check(lib().vattn_prefill_paged(_ptr(q), _ptr(k_pool), _ptr(v_pool), nb, bs, hkv, d, _ptr(bt), int(kv_len),
                                     _ptr(out), n_q, hq, float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
     return out
+
+
+def kv_append_paged(k_pool, v_pool, k_new, v_new, block_table, cache_seqlens, stream=None):
+    """PagedAttention-layout append: k_new/v_new [B, T, Hkv, D] (or [B, Hkv, D]) at rows
+    cache_seqlens[b] + i, located through block_table [B, max_blocks]."""
+    _need_cuda(k_pool, v_pool, k_new, v_new)
+    if k_new.dim() == 3:
+        k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
+    k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    bt = _i32(block_table, "block_table")
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    nb, bs, hkv, d = k_pool.shape
+    check(lib().vattn_kv_append_paged(_ptr(k_new), _ptr(v_new), _ptr(k_pool), _ptr(v_pool), bs, hkv, d, _ptr(bt),
+                                      bt.shape[-1], k_new.shape[0], k_new.shape[1], _ptr(seq),
+                                      C.c_void_p(_stream(stream))))

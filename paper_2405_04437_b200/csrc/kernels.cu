@@ -60,6 +60,35 @@ __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
   }
 }
 
+// PagedAttention-layout append (comparison path): row (b, i) goes to block
+// table[b][pos / block_size], row pos % block_size, pools [num_blocks, block_size, Hkv, D].
+struct PagedAppendParams {
+  const uint4* k_src;
+  const uint4* v_src;
+  char* k_pool;
+  char* v_pool;
+  const int32_t* seqlens;
+  const int32_t* block_table;
+  int32_t max_blocks, block_size, n_new, chunks_per_row;
+  int64_t total_chunks, row_bytes;
+};
+
+__global__ void __launch_bounds__(256) kv_append_paged_kernel(PagedAppendParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < p.total_chunks; c += stride) {
+    const int64_t row = c / p.chunks_per_row;
+    const int32_t within = (int32_t)(c - row * p.chunks_per_row);
+    const int32_t b = (int32_t)(row / p.n_new);
+    const int32_t i = (int32_t)(row - (int64_t)b * p.n_new);
+    const int32_t pos = __ldg(p.seqlens + b) + i;
+    const int32_t blk = __ldg(p.block_table + (int64_t)b * p.max_blocks + pos / p.block_size);
+    const int64_t dst = ((int64_t)blk * p.block_size + pos % p.block_size) * p.row_bytes + (int64_t)within * 16;
+    const uint4 kv = __ldg(p.k_src + c), vv = __ldg(p.v_src + c);
+    *reinterpret_cast<uint4*>(p.k_pool + dst) = kv;
+    *reinterpret_cast<uint4*>(p.v_pool + dst) = vv;
+  }
+}
+
 // ------------------------------------------------------------------------------ decode
 constexpr int kTile = 64;        // tokens per pipeline stage
 constexpr int kConsumerWarps = 4;  // each owns 16 tokens of a tile
@@ -654,6 +683,32 @@ vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, c
     const vattn::CacheView v = vattn::view_from_desc(c);
     vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
+  });
+}
+
+vattn_status vattn_kv_append_paged(const void* k_new, const void* v_new, void* k_pool, void* v_pool,
+                                   int32_t block_size, int32_t n_kv_heads, int32_t head_dim,
+                                   const int32_t* block_table, int32_t max_blocks_per_seq, int32_t batch,
+                                   int32_t n_new, const int32_t* cache_seqlens, void* stream) {
+  return kguard([&] {
+    if (batch <= 0 || n_new <= 0) return;
+    vattn::PagedAppendParams p;
+    p.k_src = reinterpret_cast<const uint4*>(k_new);
+    p.v_src = reinterpret_cast<const uint4*>(v_new);
+    p.k_pool = reinterpret_cast<char*>(k_pool);
+    p.v_pool = reinterpret_cast<char*>(v_pool);
+    p.seqlens = cache_seqlens;
+    p.block_table = block_table;
+    p.max_blocks = max_blocks_per_seq;
+    p.block_size = block_size;
+    p.n_new = n_new;
+    p.row_bytes = (int64_t)n_kv_heads * head_dim * 2;
+    p.chunks_per_row = (int32_t)(p.row_bytes / 16);
+    p.total_chunks = (int64_t)batch * n_new * p.chunks_per_row;
+    const int64_t want = (p.total_chunks + 255) / 256;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)vattn::num_sms() * 8));
+    vattn::kv_append_paged_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(p);
+    vattn::check_rt(cudaGetLastError(), "kv_append_paged launch");
   });
 }
 

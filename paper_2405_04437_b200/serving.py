@@ -423,3 +423,158 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     if overlapped:
         mgr.bg_wait()
     return metrics
+
+
+# ----------------------------------------------------------------------------- paged comparison
+class _BlockPool:
+    """PagedAttention-style block allocator (the reference's PagedBlockAllocator semantics,
+    kvsim/baselines.py:57-98): one logical block id covers `block_size` tokens of every layer;
+    requests grow block by block and free everything on completion."""
+
+    def __init__(self, total_blocks: int, block_size: int):
+        self.free = deque(range(total_blocks))
+        self.block_size = block_size
+        self.owned: dict[int, list[int]] = {}
+
+    def grow(self, rid: int, tokens: int) -> bool:
+        need = -(-tokens // self.block_size) - len(self.owned.setdefault(rid, []))
+        if need > len(self.free):
+            return False
+        for _ in range(max(0, need)):
+            self.owned[rid].append(self.free.popleft())
+        return True
+
+    def release(self, rid: int) -> None:
+        self.free.extend(self.owned.pop(rid, []))
+
+
+def run_paged(records, geometry, *, block_size: int = 16, pool_bytes: int = 24 * 1024 ** 3,
+              dense_proxy: IterationModel | None = None, preemption_cap: int = 100_000,
+              device: int = 0) -> ServingMetrics:
+    """Algorithm-1 loop on the PagedAttention layout with the in-repo paged kernels (config-5
+    comparison): per iteration the block tables of the running requests are built on the host and
+    uploaded ("block-table preparation"), then paged append / prefill / decode run.
+    `exposed_ms` = host time outside the kernels (block allocation + table preparation + upload)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from ._abi import check, lib
+    from .attention import decode_attention_paged, kv_append_paged, prefill_attention_paged
+
+    dev = torch.device("cuda", device)
+    g = geometry
+    L, hq, hkv, d = g.n_layers, g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
+    row = hkv * d * 2
+    total_blocks = pool_bytes // (2 * L * block_size * row)
+    k_pools = [torch.zeros(total_blocks, block_size, hkv, d, device=dev, dtype=torch.bfloat16) for _ in range(L)]
+    v_pools = [torch.zeros_like(k_pools[0]) for _ in range(L)]
+    pool = _BlockPool(total_blocks, block_size)
+    max_blocks = -(-g.max_context // block_size)
+    max_prompt = max((p for _, p, _ in records), default=1)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    q_pf = torch.randn(max_prompt, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    k_pf = torch.randn(1, max_prompt, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    v_pf = torch.randn_like(k_pf)
+    q_dec = torch.randn(g.max_batch, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    k_dec = torch.randn(g.max_batch, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    v_dec = torch.randn_like(k_dec)
+    out_pf, out_dec = torch.empty_like(q_pf), torch.empty_like(q_dec)
+    table_host = torch.zeros(g.max_batch, max_blocks, dtype=torch.int32).pin_memory()
+    table_dev = torch.zeros(g.max_batch, max_blocks, dtype=torch.int32, device=dev)
+    seq_host = torch.zeros(g.max_batch, dtype=torch.int32).pin_memory()
+    seq_dev = torch.zeros(g.max_batch, dtype=torch.int32, device=dev)
+    zero = torch.zeros(1, dtype=torch.int32, device=dev)
+    token_bytes = 2 * g.n_layers * g.per_token_layer_bytes
+
+    metrics = ServingMetrics()
+    pending: deque = deque(enumerate(records))
+    running: dict[int, _Running] = {}
+    free_slots = deque(range(g.max_batch))
+    admit_counter = 0
+    iteration = 0
+    t_start = time.perf_counter()
+    while pending or running:
+        t0 = time.perf_counter()
+        clock_ms = (t0 - t_start) * 1e3
+        if not running and pending and pending[0][1][0] > clock_ms:
+            time.sleep((pending[0][1][0] - clock_ms) / 1e3)
+            clock_ms = pending[0][1][0]
+        t_exp = time.perf_counter()
+        while pending and pending[0][1][0] <= clock_ms and free_slots:
+            idx, rec = pending.popleft()
+            rid = free_slots.popleft()
+            running[rid] = _Running(idx, rec[1], rec[2], ctx=rec[1], admit_order=admit_counter)
+            admit_counter += 1
+        preempted = 0
+        for rid in sorted(running, key=lambda r: running[r].admit_order):
+            while rid in running and not pool.grow(rid, running[rid].ctx):
+                victim = max(running, key=lambda r: running[r].admit_order)
+                st = running.pop(victim)
+                pool.release(victim)
+                free_slots.append(victim)
+                pending.appendleft((st.record_index, records[st.record_index]))
+                preempted += 1
+                metrics.preemptions += 1
+                if metrics.preemptions > preemption_cap:
+                    raise SimulationAborted("paged: preemption cap")
+        pf = [rid for rid, r in running.items() if r.produced == 0]
+        dec = [rid for rid, r in running.items() if r.produced > 0]
+        # host-side block-table preparation for this iteration (padded [B, max_blocks])
+        tbl = table_host.numpy()
+        sq = seq_host.numpy()
+        order = pf + dec
+        for i, rid in enumerate(order):
+            blks = pool.owned[rid]
+            tbl[i, :len(blks)] = blks
+            sq[i] = running[rid].ctx - (1 if rid in dec else 0)
+        table_dev.copy_(table_host, non_blocking=True)
+        seq_dev.copy_(seq_host, non_blocking=True)
+        exposed_ms = (time.perf_counter() - t_exp) * 1e3
+        t_k = time.perf_counter()
+        batch = len(running)
+        if batch:
+            for i, rid in enumerate(pf):
+                n = running[rid].ctx
+                for layer in range(L):
+                    kv_append_paged(k_pools[layer], v_pools[layer], k_pf[:, :n], v_pf[:, :n],
+                                    table_dev[i:i + 1], zero)
+                    prefill_attention_paged(q_pf[:n], k_pools[layer], v_pools[layer], table_dev[i], n,
+                                            out=out_pf[:n])
+            if dec:
+                o = len(pf)
+                Bd = len(dec)
+                tb = table_dev[o:o + Bd]
+                before = seq_dev[o:o + Bd]
+                after = before + 1
+                for layer in range(L):
+                    kv_append_paged(k_pools[layer], v_pools[layer], k_dec[:Bd], v_dec[:Bd], tb, before)
+                    decode_attention_paged(q_dec[:Bd], k_pools[layer], v_pools[layer], tb, after, out=out_dec[:Bd])
+            if dense_proxy is not None:
+                tokens_now = sum(running[r].ctx for r in pf) + len(dec)
+                check(lib().vattn_compute_proxy(int(dense_proxy.compute_ms(tokens_now) * 1e6),
+                                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            torch.cuda.synchronize()
+        kernel_ms = (time.perf_counter() - t_k) * 1e3
+        tokens = sum(r.ctx for r in running.values())
+        metrics.iterations.append(IterationRecord(
+            iteration=iteration, end_ms=(time.perf_counter() - t_start) * 1e3, batch=batch, prefills=len(pf),
+            tokens=tokens, compute_ms=kernel_ms, sync_alloc_ms=0.0, stall_ms=exposed_ms, cpu_ms=exposed_ms,
+            committed_bytes=sum(len(b) for b in pool.owned.values()) * block_size * token_bytes,
+            used_bytes=tokens * token_bytes, alloc_bytes=0, preemptions=preempted, exposed_ms=exposed_ms,
+            kernel_ms=kernel_ms))
+        for rid in list(running):
+            st = running[rid]
+            st.produced += 1
+            if st.produced >= st.decode_tokens:
+                metrics.completed_requests += 1
+                metrics.generated_tokens += st.decode_tokens
+                pool.release(rid)
+                del running[rid]
+                free_slots.append(rid)
+                free_slots = deque(sorted(free_slots))
+            else:
+                st.ctx += 1
+        iteration += 1
+    return metrics

@@ -151,3 +151,25 @@ def test_fused_append_decode_matches_append_then_decode(splits):
     torch.cuda.synchronize()
     assert max_rel_err(out.cpu(), ref) <= TOL
     assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)
+
+
+def test_kv_append_paged_bit_exact():
+    from paper_2405_04437_b200.attention import kv_append_paged
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(8)
+    bs, hkv, d, nb = 16, 8, 128, 40
+    kp, vp = _mk_cache(nb, bs, hkv, d, gen)
+    B, T = 3, 20
+    table = torch.randperm(nb, generator=gen)[: B * 6].view(B, 6).to(torch.int32)
+    seq = torch.tensor([0, 17, 70], dtype=torch.int32)
+    kn, vn = _rand((B, T, hkv, d), gen), _rand((B, T, hkv, d), gen)
+    kr, vr = kp.clone(), vp.clone()
+    for b in range(B):
+        for i in range(T):
+            pos = int(seq[b]) + i
+            kr[table[b, pos // bs], pos % bs] = kn[b, i]
+            vr[table[b, pos // bs], pos % bs] = vn[b, i]
+    kd, vd = kp.to(dev), vp.to(dev)
+    kv_append_paged(kd, vd, kn.to(dev), vn.to(dev), table.to(dev), seq.to(dev))
+    assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)

@@ -11,7 +11,8 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 
 from paper_2405_04437_b200.geometry import llama3_8b  # noqa: E402
-from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run  # noqa: E402
+from paper_2405_04437_b200.serving import (IterationModel, load_trace_csv, median_prompt_groups, run,  # noqa: E402
+                                           run_paged)
 
 MB2 = 2 * 1024 * 1024
 ap = argparse.ArgumentParser()
@@ -26,10 +27,14 @@ a = ap.parse_args()
 rows = load_trace_csv(Path("tests/golden/trace_config5.csv"))[: a.requests]
 g = llama3_8b(max_context=4096, max_batch=64)
 eager = median_prompt_groups(rows, g, MB2)
-m = run(rows, g, mode=a.mode, clock="wall", page_group_size=MB2, pool_bytes=a.pool_gib * 1024 ** 3,
-        eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
-        preemption_cap=100_000, defer=not a.no_defer,
-        dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch)
+if a.mode == "paged":
+    m = run_paged(rows, g, block_size=16, pool_bytes=a.pool_gib * 1024 ** 3,
+                  dense_proxy=IterationModel() if a.dense_proxy else None)
+else:
+    m = run(rows, g, mode=a.mode, clock="wall", page_group_size=MB2, pool_bytes=a.pool_gib * 1024 ** 3,
+            eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
+            preemption_cap=100_000, defer=not a.no_defer,
+            dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
           "dense_proxy": a.dense_proxy, "prefetch": a.prefetch})
