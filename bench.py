@@ -512,10 +512,18 @@ def extra_serving(local, requests=48):
     g = llama3_8b(max_context=4096, max_batch=64)
     eager = median_prompt_groups(rows, g, MB2)
     out = {"trace": f"tests/golden/trace_config5.csv first {requests} requests", "eager_groups": eager}
-    for mode in ("sync", "overlapped"):
-        m = run(rows, g, mode=mode, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
-                eager_groups=eager if mode == "overlapped" else 0, reclaim_threshold=0.10,
-                preemption_cap=100_000, dense_proxy=IterationModel())
+    variants = {
+        "sync": dict(mode="sync"),
+        "overlapped": dict(mode="overlapped"),
+        # B200 additions on top (logical state unchanged): physical prefetch of decode growth
+        # 256 tokens ahead + speculative eager pre-mapping of the 4 likely-next slots
+        "overlapped_prefetch": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
+                                    prefetch_slot_tokens=3072),
+    }
+    for mode, kw in variants.items():
+        m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
+                eager_groups=eager if kw["mode"] == "overlapped" else 0, reclaim_threshold=0.10,
+                preemption_cap=100_000, dense_proxy=IterationModel(), **kw)
         s = m.summary()
         its = m.iterations
         dec = [r.exposed_ms for r in its if r.prefills == 0]

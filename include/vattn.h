@@ -92,6 +92,10 @@ typedef struct vattn_config {
   /* B200 addition: physically pre-map pages each active slot needs within this many more tokens
    * (background jobs with VATTN_BG_PREFETCH); logical state stays the reference's. 0 = off. */
   int32_t prefetch_tokens;
+  /* ...and physically pre-map the next `prefetch_slots` slots alloc_reqid would hand out, up to
+   * `prefetch_slot_tokens` tokens of prompt (speculative eager; logical state untouched) */
+  int32_t prefetch_slots;
+  int32_t prefetch_slot_tokens;
 } vattn_config;
 
 typedef struct vattn_t vattn_t;

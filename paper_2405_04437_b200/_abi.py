@@ -37,6 +37,7 @@ class Config(C.Structure):
         ("backend", c_i32), ("device", c_i32), ("release_physical", c_i32),
         ("log_events", c_i32), ("batch_set_access", c_i32),
         ("latency", C.POINTER(LatencyEntry)), ("n_latency", c_i32), ("prefetch_tokens", c_i32),
+        ("prefetch_slots", c_i32), ("prefetch_slot_tokens", c_i32),
     ]
 
 

@@ -299,6 +299,7 @@ class Manager {
   std::unordered_map<int64_t, CUmemGenericAllocationHandle> spec_;   // key b*buffer_size+off
   std::deque<int64_t> spec_order_;
   int64_t prefetch_tokens_ = 0;
+  int64_t prefetch_slots_ = 0, prefetch_slot_tokens_ = 0;   // speculative eager for likely-next slots
   std::atomic<bool> prefetch_cancel_{false};   // set by any join: prefetch is optional work
   int64_t spec_maps_ = 0, spec_hits_ = 0, spec_steals_ = 0;
   CUmemAllocationProp prop_{};
@@ -363,6 +364,8 @@ Manager::Manager(const vattn_config& c) {
   log_events_ = c.log_events != 0;
   batch_access_ = c.batch_set_access != 0;
   prefetch_tokens_ = std::max<int64_t>(0, c.prefetch_tokens);
+  prefetch_slots_ = std::max<int64_t>(0, c.prefetch_slots);
+  prefetch_slot_tokens_ = std::max<int64_t>(0, c.prefetch_slot_tokens);
 
   lat_ = LatencyTable::table2();
   if (c.latency && c.n_latency > 0) {
@@ -622,29 +625,49 @@ CUmemGenericAllocationHandle Manager::steal_spec() {
 // reference logic maps such a page later it adopts the mapping with no driver call.  Keeps one
 // group's worth of handles free so the reference path rarely has to steal.
 void Manager::prefetch() {
-  if (!real() || prefetch_tokens_ <= 0) return;
+  if (!real() || (prefetch_tokens_ <= 0 && prefetch_slots_ <= 0)) return;
   const size_t reserve = (size_t)(2 * buffer_count_);
-  for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
-    const Slot& s = slots_[r];
-    if (!s.active) continue;
-    const int64_t target = std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_);
-    for (int64_t g = s.mapped_groups; g < target; ++g) {
+  // map [g0, g1) of slot r speculatively; false = stop (pool reserve reached or cancelled)
+  auto spec_range = [&](int32_t r, int64_t g0, int64_t g1) {
+    for (int64_t g = g0; g < g1; ++g) {
       const int64_t off = slot_offset(r, g);
       for (int64_t b = 0; b < buffer_count_; ++b) {
         const int64_t key = b * buffer_size_ + off;
         if (spec_.count(key) || buf_maps_[b].count(off)) continue;
-        if (phys_free_.size() <= reserve || prefetch_cancel_.load(std::memory_order_relaxed)) {
-          flush_access();
-          return;
-        }
+        if (phys_free_.size() <= reserve || prefetch_cancel_.load(std::memory_order_relaxed)) return false;
         const auto h = phys_free_.back();
         phys_free_.pop_back();
         real_map((int32_t)b, off, h);
+        flush_access();                 // per page: a join waits for at most one driver call
         spec_[key] = h;
         spec_order_.push_back(key);
         spec_maps_ += 1;
       }
     }
+    return true;
+  };
+  // 1. decode growth of active slots within prefetch_tokens_ more tokens
+  if (prefetch_tokens_ > 0)
+    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+      const Slot& s = slots_[r];
+      if (!s.active) continue;
+      const int64_t target = std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_);
+      if (!spec_range(r, s.mapped_groups, target)) { flush_access(); return; }
+    }
+  // 2. speculative eager: the slots alloc_reqid would hand out next (eager slot first, then by
+  //    (mapped_groups, -req_id), manager.py:166-174) up to prefetch_slot_tokens_ of prompt
+  if (prefetch_slots_ > 0 && prefetch_slot_tokens_ > 0) {
+    std::vector<int32_t> cand;
+    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r)
+      if (!slots_[r].active) cand.push_back(r);
+    std::stable_sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b) {
+      const bool ea = a == eager_slot_, eb = b == eager_slot_;
+      if (ea != eb) return ea;
+      return slots_[a].mapped_groups > slots_[b].mapped_groups;
+    });
+    const int64_t target = std::min(groups_required(prefetch_slot_tokens_), groups_per_slot_);
+    for (size_t i = 0; i < cand.size() && (int64_t)i < prefetch_slots_; ++i)
+      if (!spec_range(cand[i], slots_[cand[i]].mapped_groups, target)) break;
   }
   flush_access();
 }

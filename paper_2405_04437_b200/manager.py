@@ -194,7 +194,8 @@ class KVCacheManager:
 
     def __init__(self, geometry, config, *, backend: str | None = None, device: int | None = None,
                  log_events: bool | None = None, release_physical: bool = False,
-                 batch_set_access: bool = True, prefetch_tokens: int = 0):
+                 batch_set_access: bool = True, prefetch_tokens: int = 0, prefetch_slots: int = 0,
+                 prefetch_slot_tokens: int = 0):
         g = as_geometry(geometry)
         if g.max_batch < 1:
             raise ValueError("geometry.max_batch must be >= 1 to serve requests")
@@ -226,6 +227,8 @@ class KVCacheManager:
         cfg.log_events = int(backend == "shadow" if log_events is None else log_events)
         cfg.batch_set_access = int(batch_set_access)
         cfg.prefetch_tokens = int(prefetch_tokens)
+        cfg.prefetch_slots = int(prefetch_slots)
+        cfg.prefetch_slot_tokens = int(prefetch_slot_tokens)
         lat, n_lat = _latency_entries(getattr(config, "latency_model", None))
         if lat is not None:
             cfg.latency, cfg.n_latency = C.cast(lat[0], C.POINTER(_abi.LatencyEntry)), n_lat

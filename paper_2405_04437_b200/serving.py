@@ -242,7 +242,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         backend: str | None = None, defer: bool | None = None, observer=None,
         max_iterations: int | None = None, model: SyntheticModel | None = None,
         manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
-        prefetch_tokens: int = 0) -> ServingMetrics:
+        prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31)."""
     if mode not in ("sync", "overlapped"):
         raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
@@ -259,7 +259,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         geometry, ManagerConfig(page_group_size=int(page_group_size), pool_bytes=pool_bytes,
                                 reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
                                 sliced=sliced, pre_create_fraction=pre_create_fraction),
-        backend=backend or ("cuda" if wall else "shadow"), prefetch_tokens=prefetch_tokens)
+        backend=backend or ("cuda" if wall else "shadow"), prefetch_tokens=prefetch_tokens,
+        prefetch_slots=prefetch_slots, prefetch_slot_tokens=prefetch_slot_tokens)
     if wall and model is None:
         model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1,
                                dense_model=dense_proxy)
@@ -369,7 +370,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
                 next_seq[rid] = min(seq_lens[rid] + 1, geometry.max_context)
             plan = mgr.plan_overlap(next_seq)
             # maps run on the bg thread during the kernels (+ physical prefetch further ahead)
-            mgr.bg_submit(plan, credit=True, prefetch=prefetch_tokens > 0)
+            mgr.bg_submit(plan, credit=True, prefetch=prefetch_tokens > 0 or prefetch_slots > 0)
         if wall and batch:
             torch.cuda.synchronize()
             kernel_ms = (time.perf_counter() - t_k) * 1e3

@@ -21,6 +21,8 @@ ap.add_argument("--requests", type=int, default=128)
 ap.add_argument("--pool-gib", type=int, default=40)
 ap.add_argument("--no-defer", action="store_true")
 ap.add_argument("--prefetch", type=int, default=0, help="physical prefetch lookahead in tokens")
+ap.add_argument("--spec-slots", type=int, default=0, help="speculative eager: slots to pre-map physically")
+ap.add_argument("--spec-tokens", type=int, default=0, help="speculative eager: prompt tokens per slot")
 ap.add_argument("--out", default=None)
 ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel dense-layer time on the GPU")
 a = ap.parse_args()
@@ -34,14 +36,16 @@ else:
     m = run(rows, g, mode=a.mode, clock="wall", page_group_size=MB2, pool_bytes=a.pool_gib * 1024 ** 3,
             eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
             preemption_cap=100_000, defer=not a.no_defer,
-            dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch)
+            dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch,
+            prefetch_slots=a.spec_slots, prefetch_slot_tokens=a.spec_tokens)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
           "dense_proxy": a.dense_proxy, "prefetch": a.prefetch})
 print(json.dumps(s))
 if a.out:
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
-    tag = a.mode + ("_dense" if a.dense_proxy else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
+    tag = (a.mode + ("_dense" if a.dense_proxy else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
+           + (f"_ss{a.spec_slots}x{a.spec_tokens}" if a.spec_slots else ""))
     m.write_iterations_csv(a.out + f"_{tag}.csv")
     with open(a.out + f"_{tag}.json", "w") as fh:
         json.dump(s, fh, indent=1)
