@@ -127,9 +127,11 @@ def test_decode_through_manager_l8_shape_with_growth():
     mgr.close()
 
 
-def test_physical_prefetch_keeps_logical_state_and_data():
-    """Prefetch maps pages ahead of the reference schedule; the logical state must equal the
-    oracle's after every call and kernels must read/write the adopted pages correctly."""
+@pytest.mark.parametrize("spec_slots", [0, 2])
+def test_physical_prefetch_keeps_logical_state_and_data(spec_slots):
+    """Prefetch (and speculative eager) maps pages ahead of the reference schedule; the logical
+    state must equal the oracle's after every call and kernels must read/write the adopted pages
+    correctly."""
     _cuda()
     import random
 
@@ -140,7 +142,8 @@ def test_physical_prefetch_keeps_logical_state_and_data():
     dev = torch.device("cuda")
     g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
     pool = 24 * 4 * MB2
-    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool), prefetch_tokens=1500)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool), prefetch_tokens=1500,
+                         prefetch_slots=spec_slots, prefetch_slot_tokens=1800)
     om = OracleManager(Geometry(2, 8, 128, 2, 4096, 4), MB2, pool_bytes=pool)
     rng = random.Random(0)
     gen = torch.Generator().manual_seed(9)
