@@ -255,6 +255,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     if defer is None:
         defer = wall               # model clock keeps the reference's exact call order
     im = iteration_model or IterationModel()
+    own_manager = manager is None
     mgr = manager or KVCacheManager(
         geometry, ManagerConfig(page_group_size=int(page_group_size), pool_bytes=pool_bytes,
                                 reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
@@ -423,6 +424,12 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         iteration += 1
     if overlapped:
         mgr.bg_wait()
+    if own_manager:
+        if wall:
+            import torch
+            torch.cuda.synchronize()
+            model = None
+        mgr.close()              # release the physical pool now, not at garbage collection
     return metrics
 
 
@@ -578,4 +585,6 @@ def run_paged(records, geometry, *, block_size: int = 16, pool_bytes: int = 24 *
             else:
                 st.ctx += 1
         iteration += 1
+    del k_pools, v_pools
+    torch.cuda.empty_cache()
     return metrics
