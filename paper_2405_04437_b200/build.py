@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     def compile_one(src: str) -> tuple[str, str]:
         obj = obj_dir / (src + ".o")
         lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
-        cmd = [cc, *lang, *ARCH, *NVCC_FLAGS, *inc, "-c", str(CSRC / src), "-o", str(obj)]
+        extra = os.environ.get("VATTN_EXTRA_NVCC", "").split()
+        cmd = [cc, *lang, *ARCH, *NVCC_FLAGS, *extra, *inc, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

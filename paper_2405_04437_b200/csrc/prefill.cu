@@ -177,6 +177,20 @@ __device__ __forceinline__ float2 softmax_p_pass(uint32_t tS, float2 sc2, float2
   return acc2;
 }
 
+#ifdef VATTN_PF_TRACE
+// debug timeline of CTA (0, 0): [role][j][event] clock64 stamps (build with -DVATTN_PF_TRACE)
+__device__ unsigned long long g_pf_trace[4][160][4];
+__device__ __forceinline__ unsigned long long pf_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+#define PF_TRACE(role, j, ev) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 160) g_pf_trace[role][j][ev] = pf_clock()
+#else
+#define PF_TRACE(role, j, ev)
+#endif
+
 // number of KV tiles a query tile starting at row q0 needs
 __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   if (q0 >= p.n_q) return 0;
@@ -327,7 +341,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         fence_after();
         for (int x = 0; x < 2; ++x) {
           if (j >= nX[x]) continue;
+          PF_TRACE(2 + x, j, 0);
           ptx::mbar_wait(&p_full[x], j & 1);
+          PF_TRACE(2 + x, j, 1);
           fence_after();
           issue_pv(x, j);
           if (j + 1 == nX[x]) {
@@ -355,7 +371,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const uint32_t tO = lane_base + 256 + x * 128;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n; ++j) {
+      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
       ptx::mbar_wait(&s_full[x], j & 1);
+      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 1);
       fence_after();
       // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
       // Only diagonal / tail tiles need the per-element mask; the others take the plain path.
@@ -363,6 +381,49 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
       const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
       const bool warp_mask = __any_sync(0xffffffffu, need_mask);
+      if (!warp_mask && m_run != -INFINITY) {
+        // Single pass (common case): exponentiate against the running max while tracking the
+        // new row max; P stays in registers until the max is known not to have grown by more
+        // than 2^8 (then the stale max is kept, as the lazy rescale would anyway).
+        const float2 sc2f = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2f = make_float2(-m_run, -m_run);
+        uint32_t pk[kBN / 2];
+        float m3 = -INFINITY;
+        float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD32(tS + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            const float2 xx = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2f, nm2f);
+            float p0, p1;
+            if (((c / 2) & 3) < POLY) {
+              const float2 e = exp2_poly2(xx);
+              p0 = e.x;
+              p1 = e.y;
+            } else {
+              p0 = ptx::fast_exp2(xx.x);
+              p1 = ptx::fast_exp2(xx.y);
+            }
+            acc2 = __fadd2_rn(acc2, make_float2(p0, p1));
+            pk[(c0 + c) / 2] = ptx::pack_bf16(p0, p1);
+          }
+        }
+        if (!__any_sync(0xffffffffu, m3 * p.scale_log2 > m_run + kRescaleThreshold)) {
+#pragma unroll
+          for (int c = 0; c < kBN / 2; c += 16) TMEM_ST16(tS + c, (pk + c));
+          l_run += acc2.x + acc2.y;
+          tmem_wait_st();
+          fence_before();
+          ptx::mbar_arrive(&p_full[x]);
+          if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
+          continue;
+        }
+        // rare: the max jumped; fall through to the two-pass path (S is still intact)
+      }
       float mx = -INFINITY;
       if (!warp_mask) {
         float m3 = -INFINITY;
@@ -421,6 +482,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       tmem_wait_st();
       fence_before();
       ptx::mbar_arrive(&p_full[x]);
+      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
     }
     // ---- epilogue: O / l -> bf16 -> global ----
     if (n > 0) {
@@ -517,7 +579,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   static int poly = -1;
   if (poly < 0) {
     const char* e = getenv("VATTN_PF_POLY");   // share of exp2 on the FMA pipe, in quarters
-    poly = e ? std::max(0, std::min(3, atoi(e))) : 1;
+    poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
@@ -566,12 +628,12 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
   p.box_tokens = box;
   static bool attr = false;
   if (!attr) {
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   pf::kSmemBytes), "smem attr");
     attr = true;
   }
   dim3 grid(p.n_pairs, hq);
-  pf::prefill_kernel<1, true><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
 }
 
@@ -595,6 +657,12 @@ extern "C" vattn_status vattn_prefill_paged(const void* q, const void* k_pool, c
     return VATTN_BAD_STATE;
   }
 }
+
+#ifdef VATTN_PF_TRACE
+extern "C" int vattn_debug_prefill_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, vattn::pf::g_pf_trace, sizeof(vattn::pf::g_pf_trace));
+}
+#endif
 
 extern "C" vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                           int32_t hq, int32_t slot, int32_t kv_len, float scale,

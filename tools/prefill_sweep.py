@@ -1,11 +1,10 @@
 import os, subprocess, sys
 res = {}
-cfgs = [("1", "0"), ("1", "1"), ("2", "0"), ("2", "1"), ("2", "2")]
 for rep in range(2):
-    for ver, pp in cfgs:
-        r = subprocess.run([sys.executable, "tools/quick_prefill.py"],
-                           env=dict(os.environ, VATTN_PF_POLY=pp, VATTN_PF_VERSION=ver), capture_output=True, text=True)
-        line = (r.stdout.splitlines() or [r.stderr[-200:]])[0]
-        res.setdefault((ver, pp), []).append(line.split()[-4] if r.stdout else line)
+    for pp in ("0", "1"):
+        r = subprocess.run([sys.executable, "tools/quick_prefill.py"], env=dict(os.environ, VATTN_PF_POLY=pp),
+                           capture_output=True, text=True)
+        lines = r.stdout.splitlines()
+        res.setdefault(pp, []).append([l.split()[-4] for l in lines] if lines else r.stderr[-200:])
 for k, v in res.items():
-    print("version", k[0], "poly", k[1], "TFLOP/s at 16K:", v)
+    print("poly", k, "TFLOP/s at 16K/8K/4K:", v)
