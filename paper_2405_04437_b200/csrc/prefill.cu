@@ -191,6 +191,35 @@ __device__ __forceinline__ unsigned long long pf_clock() {
 #define PF_TRACE(role, j, ev)
 #endif
 
+// Half a row (64 keys at TMEM columns [tS, tS+64)): P = exp2(S*scale - m) packed into pk[32],
+// row max of the raw scores into m3, pairwise sum into acc.
+template <int POLY>
+__device__ __forceinline__ void softmax_half(uint32_t tS, float2 sc2, float2 nm2, uint32_t* pk, float& m3,
+                                             float2& acc) {
+#pragma unroll
+  for (int c0 = 0; c0 < 64; c0 += 32) {
+    uint32_t r[32];
+    TMEM_LD32(tS + c0, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      const float2 xx = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
+      float p0, p1;
+      if (((c / 2) & 3) < POLY) {
+        const float2 e = exp2_poly2(xx);
+        p0 = e.x;
+        p1 = e.y;
+      } else {
+        p0 = ptx::fast_exp2(xx.x);
+        p1 = ptx::fast_exp2(xx.y);
+      }
+      acc = __fadd2_rn(acc, make_float2(p0, p1));
+      pk[(c0 + c) / 2] = ptx::pack_bf16(p0, p1);
+    }
+  }
+}
+
 // number of KV tiles a query tile starting at row q0 needs
 __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   if (q0 >= p.n_q) return 0;
@@ -383,46 +412,69 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       const bool warp_mask = __any_sync(0xffffffffu, need_mask);
       if (!warp_mask && m_run != -INFINITY) {
         // Single pass (common case): exponentiate against the running max while tracking the
-        // new row max; P stays in registers until the max is known not to have grown by more
-        // than 2^8 (then the stale max is kept, as the lazy rescale would anyway).
+        // row max, half a row (64 keys) at a time; each half's P is stored only once its keys
+        // are known not to raise the max by more than 2^8 (then the stale max is kept, as the
+        // lazy rescale would).  S columns a half still needs are never overwritten early.
         const float2 sc2f = make_float2(p.scale_log2, p.scale_log2);
         const float2 nm2f = make_float2(-m_run, -m_run);
-        uint32_t pk[kBN / 2];
-        float m3 = -INFINITY;
-        float2 acc2 = make_float2(0.f, 0.f);
+        float m_lo = -INFINITY;
+        float2 acc_lo = make_float2(0.f, 0.f);
+        uint32_t pk[32];
+        softmax_half<POLY>(tS + 0, sc2f, nm2f, pk, m_lo, acc_lo);
+        if (!__any_sync(0xffffffffu, m_lo * p.scale_log2 > m_run + kRescaleThreshold)) {
+          TMEM_ST16(tS + 0, pk);
+          TMEM_ST16(tS + 16, (pk + 16));
+          float m_hi = -INFINITY;
+          float2 acc_hi = make_float2(0.f, 0.f);
+          softmax_half<POLY>(tS + 64, sc2f, nm2f, pk, m_hi, acc_hi);
+          const float mx_hi = m_hi * p.scale_log2;
+          if (!__any_sync(0xffffffffu, mx_hi > m_run + kRescaleThreshold)) {
+            TMEM_ST16(tS + 32, pk);
+            TMEM_ST16(tS + 48, (pk + 16));
+            l_run += (acc_lo.x + acc_lo.y) + (acc_hi.x + acc_hi.y);
+          } else {
+            // rare: keys 64..127 raised the max.  Rescale O and l, rescale the stored P of keys
+            // 0..63 in place, recompute keys 64..127 from S (intact) against the new max.
+            const float m_new = fmaxf(m_run, fmaxf(mx_hi, m_lo * p.scale_log2));
+            const float f = ptx::fast_exp2(m_run - m_new);
+            if (j > 0) {
+#pragma unroll 1
+              for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t o[32];
+                TMEM_LD32(tO + c0, o);
+                tmem_wait_ld();
 #pragma unroll
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
-          uint32_t r[32];
-          TMEM_LD32(tS + c0, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-            const float2 xx = __ffma2_rn(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2f, nm2f);
-            float p0, p1;
-            if (((c / 2) & 3) < POLY) {
-              const float2 e = exp2_poly2(xx);
-              p0 = e.x;
-              p1 = e.y;
-            } else {
-              p0 = ptx::fast_exp2(xx.x);
-              p1 = ptx::fast_exp2(xx.y);
+                for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+                TMEM_ST32(tO + c0, o);
+              }
             }
-            acc2 = __fadd2_rn(acc2, make_float2(p0, p1));
-            pk[(c0 + c) / 2] = ptx::pack_bf16(p0, p1);
-          }
-        }
-        if (!__any_sync(0xffffffffu, m3 * p.scale_log2 > m_run + kRescaleThreshold)) {
+            {
+              uint32_t pl[32];
+              TMEM_LD32(tS + 0, pl);
+              tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < kBN / 2; c += 16) TMEM_ST16(tS + c, (pk + c));
-          l_run += acc2.x + acc2.y;
+              for (int c = 0; c < 32; ++c) {
+                __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&pl[c]);
+                const float2 fv = __bfloat1622float2(v);
+                pl[c] = ptx::pack_bf16(fv.x * f, fv.y * f);
+              }
+              TMEM_ST32(tS + 0, pl);
+            }
+            float m_dummy = -INFINITY;
+            float2 acc_new = make_float2(0.f, 0.f);
+            softmax_half<POLY>(tS + 64, sc2f, make_float2(-m_new, -m_new), pk, m_dummy, acc_new);
+            TMEM_ST16(tS + 32, pk);
+            TMEM_ST16(tS + 48, (pk + 16));
+            l_run = l_run * f + (acc_lo.x + acc_lo.y) * f + (acc_new.x + acc_new.y);
+            m_run = m_new;
+          }
           tmem_wait_st();
           fence_before();
           ptx::mbar_arrive(&p_full[x]);
           if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
           continue;
         }
-        // rare: the max jumped; fall through to the two-pass path (S is still intact)
+        // rare: the first half already raised the max: two-pass path below (nothing stored yet)
       }
       float mx = -INFINITY;
       if (!warp_mask) {

@@ -121,3 +121,25 @@ def test_prefill_paged_matches_contiguous(block_size):
     torch.cuda.synchronize()
     assert max_rel_err(out_p.cpu(), ref) <= TOL
     assert torch.equal(out_p.cpu(), out_c.cpu())
+
+
+def test_prefill_max_jumps_take_the_rescale_paths():
+    """Keys with large norms late in the sequence make the running row max jump by far more than
+    2^8 inside a tile's second half and first half: the single-pass softmax must rescale O, l and
+    the already-stored P correctly."""
+    from paper_2405_04437_b200.attention import prefill_attention_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(31)
+    S, hq, hkv = 1024, 16, 2
+    k = torch.randn(1, S, hkv, 128, generator=gen)
+    v = torch.randn(1, S, hkv, 128, generator=gen)
+    q = torch.randn(S, hq, 128, generator=gen)
+    for pos in (200, 300, 357, 700, 1000):      # second halves and first halves of 128-key tiles
+        k[0, pos] *= 12.0
+    k, v, q = k.to(torch.bfloat16), v.to(torch.bfloat16), q.to(torch.bfloat16)
+    ref = prefill_ref(q, k[0], v[0])
+    out = prefill_attention_raw(q.to(dev), k.to(dev), v.to(dev), 0, S)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    assert max_rel_err(out.cpu(), ref) <= TOL
