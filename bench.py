@@ -279,7 +279,7 @@ def bench_decode(args, world, rank, local):
     dec_us = statistics.mean(dec_ms) * 1e3
     pk = peaks()
     achieved = dec_bytes / (dec_us * 1e-6) / 1e9
-    kernel_name = "decode_kernel<128,4,false>" + ("" if args.unfused else " (fused append)")
+    kernel_name = "decode_kernel<128,3,false>" + ("" if args.unfused else " (fused append)")
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists() and args.workload == "l8_decode":

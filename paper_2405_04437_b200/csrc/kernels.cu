@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <climits>
+#include <cstdlib>
 #include <tuple>
 
 #include "internal.h"
@@ -588,7 +589,16 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
                                           (int64_t)batch * hq * num_splits * d * 4);
   }
   if (d == 128) {
+    // Measured (tools/decode_stage_sweep.py): with >= 2 CTAs per SM worth of work a 3-stage ring
+    // (97 KB smem, 2 CTAs/SM) beats the 4-stage one (L8 layer 6.9 vs 6.2 TB/s); with fewer CTAs
+    // the deeper per-CTA pipeline wins (B 128 x 1 KV head: 6.6 vs 6.3 TB/s).
+    static const int forced = [] {
+      const char* e = getenv("VATTN_DEC_STAGES");
+      return e ? atoi(e) : 0;
+    }();
+    const int stages = forced ? forced : (batch * hkv * p.num_splits >= 2 * num_sms() ? 3 : 4);
     if (paged) run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
+    else if (stages == 3) run_decode<128, 3, false>(km, vm, p, batch, hkv, st);
     else run_decode<128, 4, false>(km, vm, p, batch, hkv, st);
   } else {
     if (paged) run_decode<64, 6, true>(km, vm, p, batch, hkv, st);
