@@ -597,9 +597,14 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
       return e ? atoi(e) : 0;
     }();
     const int stages = forced ? forced : (batch * hkv * p.num_splits >= 2 * num_sms() ? 3 : 4);
-    if (paged) run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
-    else if (stages == 3) run_decode<128, 3, false>(km, vm, p, batch, hkv, st);
-    else run_decode<128, 4, false>(km, vm, p, batch, hkv, st);
+    if (paged) {   // same rule, so the paged comparison differs from the contiguous path only in layout
+      if (stages == 3) run_decode<128, 3, true>(km, vm, p, batch, hkv, st);
+      else run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
+    } else if (stages == 3) {
+      run_decode<128, 3, false>(km, vm, p, batch, hkv, st);
+    } else {
+      run_decode<128, 4, false>(km, vm, p, batch, hkv, st);
+    }
   } else {
     if (paged) run_decode<64, 6, true>(km, vm, p, batch, hkv, st);
     else run_decode<64, 6, false>(km, vm, p, batch, hkv, st);
