@@ -472,6 +472,68 @@ def extra_paged(local):
     return res
 
 
+def extra_libraries(local):
+    """Library kernels on identical inputs, for context (not on the product path).
+    * flash-attn 2.8.3: the kernels vAttention runs unmodified.
+    * cuDNN SDPA through torch.
+    Shapes are the L8 decode layer and the Y6 16K causal prefill."""
+    import torch
+
+    from paper_2405_04437_b200.attention import decode_attention_raw, prefill_attention_raw
+
+    dev = torch.device("cuda", local)
+    res = {}
+    gen = torch.Generator(device=dev).manual_seed(3)
+    B, hq, hkv, d, L = 64, 32, 8, 128, 4096
+    k = torch.randn(B, L, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    v = torch.randn_like(k)
+    q = torch.randn(B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    seq = torch.full((B,), L, dtype=torch.int32, device=dev)
+    byt = 2 * B * L * hkv * d * 2
+    ours = _time_ms(lambda: decode_attention_raw(q, k, v, seq)) * 1e3
+    res["decode_l8_ours_us"] = ours
+    try:
+        import flash_attn
+
+        q4 = q.unsqueeze(1)
+        fa = _time_ms(lambda: flash_attn.flash_attn_with_kvcache(q4, k, v, cache_seqlens=seq)) * 1e3
+        res["decode_l8_flash_attn_us"] = fa
+        res["decode_l8_flash_attn_gbs"] = byt / (fa * 1e-6) / 1e9
+        res["decode_l8_speedup_vs_flash_attn"] = fa / ours
+    except Exception as e:
+        res["flash_attn_decode_error"] = repr(e)[:200]
+    del k, v
+    S, hq, hkv = 16384, 32, 4
+    kc = torch.randn(1, S, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    vc = torch.randn_like(kc)
+    qp = torch.randn(S, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    flops = 2.0 * S * S * d * hq
+    ours = _time_ms(lambda: prefill_attention_raw(qp, kc, vc, 0, S))
+    res["prefill_y6_ours_tflops"] = flops / (ours * 1e-3) / 1e12
+    try:
+        import flash_attn
+
+        fa = _time_ms(lambda: flash_attn.flash_attn_func(qp.unsqueeze(0), kc, vc, causal=True), iters=5)
+        res["prefill_y6_flash_attn_tflops"] = flops / (fa * 1e-3) / 1e12
+        res["prefill_y6_speedup_vs_flash_attn"] = fa / ours
+    except Exception as e:
+        res["flash_attn_prefill_error"] = repr(e)[:200]
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        qh = qp.transpose(0, 1).unsqueeze(0)                              # [1, Hq, S, D]
+        kh = kc[0].repeat_interleave(hq // hkv, dim=1).transpose(0, 1).unsqueeze(0)
+        vh = vc[0].repeat_interleave(hq // hkv, dim=1).transpose(0, 1).unsqueeze(0)
+        with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+            cd = _time_ms(lambda: torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True),
+                          iters=5)
+        res["prefill_y6_cudnn_sdpa_tflops"] = flops / (cd * 1e-3) / 1e12
+        res["prefill_y6_speedup_vs_cudnn_sdpa"] = cd / ours
+    except Exception as e:
+        res["cudnn_prefill_error"] = repr(e)[:200]
+    return res
+
+
 def extra_y34_shards(local):
     """BASELINE config 4 per rank: Yi-34B decode (B 128, ctx 8K, 56 Q / 8 KV heads) with KV heads
     sharded over G GPUs — each rank's shard measured on this GPU (no collective on the path, so
@@ -677,7 +739,8 @@ def main(argv=None):
         if not args.no_extras and world == 1:
             extras = {}
             for name, fn in (("prefill", extra_prefill), ("paged_vs_contiguous", extra_paged),
-                             ("y34_shards", extra_y34_shards), ("serving", extra_serving)):
+                             ("y34_shards", extra_y34_shards), ("libraries", extra_libraries),
+                             ("serving", extra_serving)):
                 try:
                     extras[name] = fn(local)
                 except Exception as e:   # an extra must not void the headline line
