@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import torch
 
@@ -47,6 +48,31 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+# Opt-in guard (VATTN_CHECK_BOUNDS=1): check on the host, before launch, that every cache row a
+# kernel will touch is backed by a mapped page-group.  The kernels trust cache_seqlens (it lives
+# on the device); a row past the mapped prefix of a slot would fault the GPU context instead of
+# raising.  Costs one device->host copy of the index vectors per call, so it is off by default.
+CHECK_BOUNDS = os.environ.get("VATTN_CHECK_BOUNDS", "0") not in ("", "0")
+
+
+def check_bounds(mgr, cache_seqlens, cache_batch_idx=None, extra_rows: int = 0) -> None:
+    """Raise ValueError unless rows [0, cache_seqlens[b] + extra_rows) of slot cache_batch_idx[b]
+    are all backed (reference contract: only stepped lengths may be touched, manager.py:255-296)."""
+    seq = cache_seqlens.tolist() if isinstance(cache_seqlens, torch.Tensor) else list(cache_seqlens)
+    if cache_batch_idx is None:
+        idx = list(range(len(seq)))
+    else:
+        idx = cache_batch_idx.tolist() if isinstance(cache_batch_idx, torch.Tensor) else list(cache_batch_idx)
+    slots = mgr.slots
+    for b, (n, r) in enumerate(zip(seq, idx)):
+        if not 0 <= r < len(slots):
+            raise ValueError(f"cache_batch_idx[{b}] = {r} is not a slot (max_batch {len(slots)})")
+        backed = slots[r].mapped_groups * mgr.page_group_size // mgr.per_buffer_token_bytes
+        if n < 0 or n + extra_rows > backed:
+            raise ValueError(f"row {b}: slot {r} needs {n + extra_rows} tokens but only {backed} are mapped "
+                             f"(call step() with the grown lengths first)")
+
+
 # ------------------------------------------------------------------ manager-backed ops
 def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None):
     """Write k_new/v_new [B, T, Hkv, D] (or [B, Hkv, D] for one token) at rows
@@ -58,6 +84,8 @@ def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None
     k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    if CHECK_BOUNDS:
+        check_bounds(mgr, seq, idx, extra_rows=k_new.shape[1])
     check(lib().vattn_kv_append(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
                                 _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
 
@@ -72,6 +100,8 @@ def decode_attention(mgr, layer: int, q, cache_seqlens, cache_batch_idx=None, so
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    if CHECK_BOUNDS:
+        check_bounds(mgr, seq, idx)
     check(lib().vattn_decode(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], _ptr(seq), _ptr(idx),
                              float(scale), int(num_splits), C.c_void_p(_stream(stream))))
     return out
@@ -88,6 +118,8 @@ def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cac
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    if CHECK_BOUNDS:
+        check_bounds(mgr, seq, idx, extra_rows=1)
     check(lib().vattn_decode_append(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), q.shape[0],
                                     _ptr(seq), _ptr(idx), float(scale), int(num_splits), C.c_void_p(_stream(stream))))
     return out
@@ -103,6 +135,8 @@ def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None
         out = torch.empty_like(q)
     kv_len = q.shape[0] if kv_len is None else kv_len
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    if CHECK_BOUNDS:
+        check_bounds(mgr, [kv_len], [req_id])
     check(lib().vattn_prefill(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
                               float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
     return out

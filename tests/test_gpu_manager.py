@@ -240,3 +240,29 @@ def test_sliced_layout_kernels():
         # the view sees the sliced strides
         assert torch.equal(mgr.k_cache(layer)[r, :S].cpu(), kn[0])
     mgr.close()
+
+
+def test_bounds_guard_raises_instead_of_faulting(monkeypatch):
+    """VATTN_CHECK_BOUNDS: a length past the mapped prefix is a ValueError, not a GPU fault."""
+    _cuda()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, attention
+    from paper_2405_04437_b200.geometry import ModelGeometry
+
+    monkeypatch.setattr(attention, "CHECK_BOUNDS", True)
+    dev = torch.device("cuda")
+    g = ModelGeometry(1, 8, 128, 2, max_context=8192, max_batch=2, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=16 * MB2))
+    try:
+        r = mgr.alloc_reqid()
+        lens = [0, 0]
+        lens[r] = 1000
+        assert mgr.step(lens).ok                     # one 2 MiB group = 1024 tokens mapped
+        q = torch.randn(1, 32, 128, device=dev, dtype=torch.bfloat16)
+        idx = torch.tensor([r], dtype=torch.int32, device=dev)
+        with pytest.raises(ValueError, match="mapped"):
+            attention.decode_attention(mgr, 0, q, torch.tensor([5000], dtype=torch.int32, device=dev), idx)
+        out = attention.decode_attention(mgr, 0, q, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+    finally:
+        mgr.close()
