@@ -259,6 +259,8 @@ def test_bounds_guard_raises_instead_of_faulting(monkeypatch):
         assert mgr.step(lens).ok                     # one 2 MiB group = 1024 tokens mapped
         q = torch.randn(1, 32, 128, device=dev, dtype=torch.bfloat16)
         idx = torch.tensor([r], dtype=torch.int32, device=dev)
+        kv = torch.randn(1, 1024, 8, 128, device=dev, dtype=torch.bfloat16)   # fresh pages hold garbage
+        attention.kv_append(mgr, 0, kv, kv, torch.zeros(1, dtype=torch.int32, device=dev), idx)
         with pytest.raises(ValueError, match="mapped"):
             attention.decode_attention(mgr, 0, q, torch.tensor([5000], dtype=torch.int32, device=dev), idx)
         out = attention.decode_attention(mgr, 0, q, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
