@@ -176,8 +176,9 @@ def bench_decode(args, world, rank, local):
     import torch
 
     from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
-    from paper_2405_04437_b200.attention import (decode_attention, decode_attention_append, decode_num_splits,
-                                                 kv_append)
+    from paper_2405_04437_b200.attention import (decode_attention, decode_attention_append, decode_attention_gather,
+                                                 decode_num_splits, kv_append)
+    from paper_2405_04437_b200.parallel import gather_heads
 
     dev = torch.device("cuda", local)
     g, ctx, wname = decode_geometry(args.workload, world)
@@ -218,6 +219,10 @@ def bench_decode(args, world, rank, local):
 
     state = {"seq": list(seq), "pos": pos}
     splits = decode_num_splits(B, hkv, ctx + 1)
+    hg = None
+    if args.gather == "fused" and world > 1:
+        from paper_2405_04437_b200.parallel import HeadGather
+        hg = HeadGather.create(B, hq * world, d, device=local)
 
     def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out, pre_layer=None, post_layer=None):
         nxt = list(state["seq"])
@@ -233,7 +238,14 @@ def bench_decode(args, world, rank, local):
                 pre_layer(layer)
             if dec_events is not None:
                 dec_events[layer][0].record(stream)
-            if args.unfused:
+            if hg is not None:      # fused decode + head all-gather over peer memory
+                decode_attention_gather(mgr, layer, q_[layer], hg, p, idx, k_new=kn_[layer], v_new=vn_[layer],
+                                        num_splits=splits)
+            elif args.gather == "nccl":
+                decode_attention_append(mgr, layer, q_[layer], kn_[layer], vn_[layer], p, idx,
+                                        out=out_[layer], num_splits=splits)
+                gather_heads(out_[layer])
+            elif args.unfused:
                 kv_append(mgr, layer, kn_[layer], vn_[layer], p, idx)
                 decode_attention(mgr, layer, q_[layer], p + 1, idx, out=out_[layer], num_splits=splits)
             else:   # one launch: append the new token at row p and attend over p + 1 rows
@@ -333,6 +345,7 @@ def bench_decode(args, world, rank, local):
     e2e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps)
     h2d = qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2
     d2h = outh.numel() * 2
+    gather_cmp = head_gather_compare(mgr, q, out, pos, idx, splits, world, local) if world > 1 else None
     st = mgr.driver_stats()
     result = {
         "metric": "decode_attn_tokens_per_s",
@@ -358,11 +371,67 @@ def bench_decode(args, world, rank, local):
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "clocks": clk,
-        "gpu_launches": steps * N * ((2 if args.unfused else 1) + (1 if splits > 1 else 0)),
+        "gpu_launches": steps * N * ((2 if args.unfused and hg is None else 1) + (1 if splits > 1 else 0)
+                                     + (1 if hg is not None else 0)),
+        "head_gather_mode": args.gather if world > 1 else "none (1 GPU)",
         "decode_kernel_mode": "unfused append+decode" if args.unfused else "fused append+decode (k=/v= semantics)",
     }
+    if gather_cmp is not None:
+        result["head_gather"] = gather_cmp
+    if hg is not None:
+        hg.close()
     mgr.close()
     return result
+
+
+def head_gather_compare(mgr, q, out, pos, idx, splits, world, local, iters=20):
+    """N>1 only (all ranks): one layer's decode alone, with the fused peer-memory head gather,
+    and followed by an NCCL all_gather of the heads; device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_04437_b200.attention import decode_attention, decode_attention_gather
+    from paper_2405_04437_b200.parallel import HeadGather, gather_heads
+
+    B, hq, d = q.shape[1], q.shape[2], q.shape[3]
+    stream = torch.cuda.current_stream()
+    hg, err = None, None
+    try:
+        hg = HeadGather.create(B, hq * world, d, device=local)
+    except Exception as e:          # report, but every rank must agree before timing
+        err = repr(e)[:200]
+    ok = torch.tensor([0 if err else 1], device=q.device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / iters * 1e3)
+
+    res = {"layer_decode_us": timed(lambda: decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits)),
+           "nccl_us": timed(lambda: gather_heads(decode_attention(mgr, 0, q[0], pos, idx, out=out[0],
+                                                                  num_splits=splits)))}
+    if int(ok.item()) == 1:
+        res["fused_us"] = timed(lambda: decode_attention_gather(mgr, 0, q[0], hg, pos, idx, num_splits=splits))
+        ref = gather_heads(decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits))
+        got = decode_attention_gather(mgr, 0, q[0], hg, pos, idx, num_splits=splits)
+        torch.cuda.synchronize()
+        res["fused_equals_nccl"] = bool(torch.equal(ref, got))
+        res["timed_out_ranks"] = hg.timed_out_ranks()
+    else:
+        res["fused_error"] = err or "a peer rank failed to set up the gather"
+    if hg is not None:
+        hg.close()
+    res["bytes_per_rank"] = B * hq * d * 2
+    return res
 
 
 # ----------------------------------------------------------------------------- extras
@@ -710,6 +779,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip prefill / paged / serving sub-benches")
     ap.add_argument("--unfused", action="store_true", help="separate kv_append + decode launches per layer")
+    ap.add_argument("--gather", choices=["none", "fused", "nccl"], default="none",
+                    help="N>1: all-gather the output heads every layer (fused peer-memory kernel or NCCL)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

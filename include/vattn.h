@@ -295,6 +295,44 @@ vattn_status vattn_prefill_paged(const void* q, const void* k_pool, const void* 
 int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t n_q_heads, int32_t head_dim,
                                      int32_t num_splits);
 
+/* ---- fused head all-gather over NVLink peer memory ----------------------------
+ * Replaces the NCCL all-gather of the per-rank decode outputs [B, Hq/G, D] into [B, Hq, D]
+ * (north_star: "NCCL over NVLink is used only for the final head all-gather when the caller
+ * requests full outputs"; the reference has no multi-GPU code — every worker runs the same
+ * allocator, geometry.py:96-98 kv_heads_per_worker).  The decode epilogue stores
+ * each row into every rank's full output buffer over peer memory and signals; vattn_gather_wait
+ * makes `stream` wait until all ranks' rows have landed. */
+#define VATTN_IPC_HANDLE_BYTES 64
+typedef struct vattn_gather vattn_gather_t;
+/* one per rank (collective setup): allocates this rank's full-output buffer of out_bytes
+ * (>= max_batch * Hq_total * D * 2) + signal words; writes its CUDA IPC handle
+ * (VATTN_IPC_HANDLE_BYTES) to ipc_handle for the caller to all-gather across ranks. */
+vattn_status vattn_gather_create(int32_t device, int32_t rank, int32_t world, int64_t out_bytes,
+                                 vattn_gather_t** out, void* ipc_handle);
+/* map every peer's buffer: handles = world x VATTN_IPC_HANDLE_BYTES in rank order */
+vattn_status vattn_gather_open(vattn_gather_t* g, const void* handles);
+/* `world` simulated ranks on one device in this process (out[world]); same kernels/protocol */
+vattn_status vattn_gather_create_local(int32_t device, int32_t world, int64_t out_bytes,
+                                       vattn_gather_t** out);
+/* device address of this rank's full output [batch, Hq_total, D] bf16 */
+vattn_status vattn_gather_output(vattn_gather_t* g, uint64_t* dptr);
+/* stream-ordered: wait (bounded: 10 s, env VATTN_GATHER_TIMEOUT_MS) until every rank's latest gathered launch has landed */
+vattn_status vattn_gather_wait(vattn_gather_t* g, void* stream);
+/* bit r set = the wait for rank r timed out (a rank skipped a launch) */
+vattn_status vattn_gather_check(vattn_gather_t* g, uint32_t* timed_out_mask);
+vattn_status vattn_gather_destroy(vattn_gather_t* g);
+/* decode (k_new/v_new non-NULL: fused append, as vattn_decode_append) of this rank's Hq_local
+ * heads, rows stored into every rank's full output at head offset rank * Hq_local */
+vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const void* k_new,
+                                 const void* v_new, vattn_gather_t* g, int32_t batch,
+                                 const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                                 float scale, int32_t num_splits, void* stream);
+vattn_status vattn_decode_gather_raw(const vattn_cache_desc* c, const void* q, const void* k_new,
+                                     const void* v_new, vattn_gather_t* g, int32_t batch,
+                                     int32_t n_q_heads, const int32_t* cache_seqlens,
+                                     const int32_t* cache_batch_idx, float scale, int32_t num_splits,
+                                     void* workspace, int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

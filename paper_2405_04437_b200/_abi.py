@@ -127,7 +127,19 @@ SIGNATURES = {
     "vattn_compute_proxy": (c_i32, [c_u64, c_vp]),
     "vattn_decode_num_splits": (c_i32, [c_i32, c_i32, c_i32]),
     "vattn_decode_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
+    "vattn_gather_create": (c_i32, [c_i32, c_i32, c_i32, c_i64, C.POINTER(c_vp), c_vp]),
+    "vattn_gather_open": (c_i32, [c_vp, c_vp]),
+    "vattn_gather_create_local": (c_i32, [c_i32, c_i32, c_i64, C.POINTER(c_vp)]),
+    "vattn_gather_output": (c_i32, [c_vp, C.POINTER(c_u64)]),
+    "vattn_gather_wait": (c_i32, [c_vp, c_vp]),
+    "vattn_gather_check": (c_i32, [c_vp, C.POINTER(c_u32)]),
+    "vattn_gather_destroy": (c_i32, [c_vp]),
+    "vattn_decode_gather": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
+    "vattn_decode_gather_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                        c_f32, c_i32, c_vp, c_i64, c_vp]),
 }
+
+IPC_HANDLE_BYTES = 64
 
 _lib = None
 _lock = threading.Lock()

@@ -125,6 +125,33 @@ def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cac
     return out
 
 
+def decode_attention_gather(mgr, layer: int, q, gather, cache_seqlens, cache_batch_idx=None, k_new=None,
+                            v_new=None, softmax_scale=None, num_splits: int = 0, wait: bool = True, stream=None):
+    """Decode this rank's query heads q [B, Hq/G, D] (k_new/v_new given: fused append, as
+    decode_attention_append) and all-gather the heads in the same kernel: every output row is
+    stored over NVLink peer memory into each rank's full output [B, Hq, D] at head offset
+    rank*Hq/G.  With wait=True the stream then waits for all ranks' rows; returns
+    the full-output view (`gather.output(B)`)."""
+    _need_cuda(q)
+    q = _bf16(q, "q")
+    if (k_new is None) != (v_new is None):
+        raise ValueError("k_new and v_new go together")
+    if k_new is not None:
+        _need_cuda(k_new, v_new)
+        k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    if CHECK_BOUNDS:
+        check_bounds(mgr, seq, idx, extra_rows=0 if k_new is None else 1)
+    st = C.c_void_p(_stream(stream))
+    check(lib().vattn_decode_gather(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), gather.handle, q.shape[0],
+                                    _ptr(seq), _ptr(idx), float(scale), int(num_splits), st))
+    if wait:
+        gather.wait(stream)
+    return gather.output(q.shape[0])
+
+
 def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None, causal=True,
                       softmax_scale=None, out=None, stream=None):
     """Causal (bottom-right aligned) attention of q [S, Hq, D] over rows [0, kv_len) of slot
@@ -214,6 +241,27 @@ def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens
                                         _ptr(seq), _ptr(idx), float(scale), int(num_splits), _ptr(ws), ws.numel(),
                                         C.c_void_p(_stream(stream))))
     return out
+
+
+def decode_attention_gather_raw(q, k_cache, v_cache, gather, cache_seqlens, cache_batch_idx=None, k_new=None,
+                                v_new=None, softmax_scale=None, num_splits: int = 0, wait: bool = True,
+                                stream=None):
+    """decode_attention_gather on caller-owned caches (see cache_desc)."""
+    desc = cache_desc(k_cache, v_cache)
+    q = _bf16(q, "q")
+    if k_new is not None:
+        k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
+    seq = _i32(cache_seqlens, "cache_seqlens")
+    idx = _i32(cache_batch_idx, "cache_batch_idx")
+    b, hq, d = q.shape
+    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0))
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    check(lib().vattn_decode_gather_raw(C.byref(desc), _ptr(q), _ptr(k_new), _ptr(v_new), gather.handle, b, hq,
+                                        _ptr(seq), _ptr(idx), float(scale), int(num_splits), _ptr(ws), ws.numel(),
+                                        C.c_void_p(_stream(stream))))
+    if wait:
+        gather.wait(stream)
+    return gather.output(b)
 
 
 def decode_attention_paged(q, k_pool, v_pool, block_table, seqlens, softmax_scale=None, out=None,

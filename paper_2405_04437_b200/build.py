@@ -22,7 +22,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libvattn.so"
-SOURCES = ["core.cpp", "kernels.cu", "prefill.cu"]
+SOURCES = ["core.cpp", "kernels.cu", "prefill.cu", "gather.cu"]
 HEADERS = ["internal.h", "ptx.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

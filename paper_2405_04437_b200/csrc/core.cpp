@@ -1559,6 +1559,30 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
   });
 }
 
+vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const void* k_new,
+                                 const void* v_new, vattn_gather_t* g, int32_t batch,
+                                 const int32_t* cache_seqlens, const int32_t* batch_idx, float scale,
+                                 int32_t num_splits, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    const vattn::CacheView v = h->m->layer_view(layer);
+    const int hq = h->m->hq_local();
+    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
+    if (need > h->workspace_bytes) {
+      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
+      h->workspace = nullptr;
+      h->workspace_bytes = 0;
+      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
+      h->workspace_bytes = need;
+    }
+    const vattn::GatherSink s = vattn::gather_sink(g, hq, batch, v.d);
+    vattn::launch_decode(h->m->ks, layer, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale,
+                         num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new, &s);
+    vattn::gather_commit(g, s, batch);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
 vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                            int32_t slot, int32_t kv_len, float scale, int32_t causal,
                            void* stream) {

@@ -70,6 +70,24 @@ struct KernelState;
 KernelState* kernel_state_new();
 void kernel_state_free(KernelState*);
 
+// Fused head all-gather (gather.cu): the decode epilogue stores every output row
+// straight into each rank's full [batch, Hq_total, D] buffer over NVLink peer memory (P2P
+// stores) at head offset rank*Hq_local, then the last CTA to finish raises this rank's flag in
+// every peer's signal array.  n_ranks = 0 disables it (plain local output).
+constexpr int kMaxGatherRanks = 8;
+struct GatherSink {
+  void* dst[kMaxGatherRanks];          // rank r's full output (peer-mapped; own included)
+  uint32_t* flags[kMaxGatherRanks];    // rank r's signal words, indexed by the writing rank
+  uint32_t* counter;                   // this rank's CTA-completion counter (reset by the last CTA)
+  int32_t n_ranks, rank, hq_total, head_off;
+  uint32_t epoch;
+};
+
+// gather.cu: sink for the next launch through `g` (epoch = last + 1) and its commit after the
+// launch succeeded (every rank must issue the same sequence of gathered launches).
+GatherSink gather_sink(vattn_gather_t* g, int hq_local, int batch, int head_dim);
+void gather_commit(vattn_gather_t* g, const GatherSink& s, int batch);
+
 // Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
 void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,
                       const void* v_new, int batch, int n_new, const int32_t* seqlens,
@@ -77,7 +95,8 @@ void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const 
 void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                    int batch, int hq, const int32_t* seqlens, const int32_t* batch_idx,
                    float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st,
-                   const void* k_new = nullptr, const void* v_new = nullptr);
+                   const void* k_new = nullptr, const void* v_new = nullptr,
+                   const GatherSink* sink = nullptr);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
                     cudaStream_t st);

@@ -113,7 +113,37 @@ struct DecodeParams {
   __nv_bfloat16* k_cache;       // base of the layer's K region (row address computed below)
   __nv_bfloat16* v_cache;
   int64_t slot_stride, token_stride;
+  GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
 };
+
+// ---- fused head all-gather epilogue (gather.cu owns the buffers and the wait) ----
+// Output row (b, local head h) goes to row (b, head_off + h) of every rank's full output: one
+// 2-byte P2P store per rank over NVLink, issued as each element is produced, so the exchange
+// overlaps the other CTAs' attention instead of following it.
+__device__ __forceinline__ void sink_store(const GatherSink& s, int b, int head, int c, int D,
+                                           __nv_bfloat16 v) {
+  const int64_t idx = ((int64_t)b * s.hq_total + s.head_off + head) * D + c;
+#pragma unroll 1
+  for (int r = 0; r < s.n_ranks; ++r) reinterpret_cast<__nv_bfloat16*>(s.dst[r])[idx] = v;
+}
+
+// Called by all `nthreads` threads of a CTA (named barrier 1) after their last sink_store.
+// Every writer fences at system scope; the CTA that completes the grid raises this rank's flag
+// in every peer's signal array (release, system scope) and re-arms the counter for the next
+// launch on the stream.
+__device__ __forceinline__ void sink_signal(const GatherSink& s, uint32_t total_ctas, int nthreads) {
+  __threadfence_system();
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(s.counter, 1u);
+    if (prev == total_ctas - 1) {
+      __threadfence_system();
+      for (int r = 0; r < s.n_ranks; ++r)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(s.flags[r] + s.rank), "r"(s.epoch) : "memory");
+      atomicExch(s.counter, 0u);
+    }
+  }
+}
 
 template <int D, int STAGES>
 struct DecodeSmem {
@@ -374,45 +404,59 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
     const float val = lsum > 0.f ? acc / lsum : 0.f;
     const int head = kvh * p.group + r;
     if (p.num_splits == 1) {
-      p.out[((int64_t)b * p.hq + head) * D + c] = __float2bfloat16(val);
+      if (p.sink.n_ranks) sink_store(p.sink, b, head, c, D, __float2bfloat16(val));
+      else p.out[((int64_t)b * p.hq + head) * D + c] = __float2bfloat16(val);
     } else {
       const int64_t row = ((int64_t)b * p.hq + head) * p.num_splits + split;
       p.part_o[row * D + c] = val;
       if (c == 0) p.part_lse[row] = lsum > 0.f ? M + log2f(lsum) : -INFINITY;
     }
   }
+  if (p.sink.n_ranks && p.num_splits == 1)
+    sink_signal(p.sink, gridDim.x * gridDim.y * gridDim.z, kConsumerWarps * 32);
 }
 
-// merge split partials with log-sum-exp weights (log2 domain)
+// merge split partials with log-sum-exp weights (log2 domain); with a gather sink the merged
+// rows go straight to every rank's full output (rows = batch * hq_local)
 template <int D>
 __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __restrict__ part_o,
                                                              const float* __restrict__ part_lse,
                                                              __nv_bfloat16* __restrict__ out,
-                                                             int rows, int num_splits) {
+                                                             int rows, int num_splits, int hq,
+                                                             GatherSink sink) {
   const int row = blockIdx.x * (blockDim.x / (D / 4)) + threadIdx.x / (D / 4);
   const int c4 = threadIdx.x % (D / 4);
-  if (row >= rows) return;
-  const float* lse = part_lse + (int64_t)row * num_splits;
-  float M = -INFINITY;
-  for (int s = 0; s < num_splits; ++s) M = fmaxf(M, lse[s]);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float wsum = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < num_splits; ++s) {
-      const float w = exp2f(lse[s] - M);
-      if (w == 0.f) continue;
-      const float4 v = *reinterpret_cast<const float4*>(part_o + ((int64_t)row * num_splits + s) * D + c4 * 4);
-      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
-      wsum += w;
+  if (row < rows) {
+    const float* lse = part_lse + (int64_t)row * num_splits;
+    float M = -INFINITY;
+    for (int s = 0; s < num_splits; ++s) M = fmaxf(M, lse[s]);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float wsum = 0.f;
+    if (M != -INFINITY) {
+      for (int s = 0; s < num_splits; ++s) {
+        const float w = exp2f(lse[s] - M);
+        if (w == 0.f) continue;
+        const float4 v = *reinterpret_cast<const float4*>(part_o + ((int64_t)row * num_splits + s) * D + c4 * 4);
+        acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+        wsum += w;
+      }
+    }
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    if (sink.n_ranks == 0) {
+      *reinterpret_cast<uint2*>(out + (int64_t)row * D + c4 * 4) = pk;
+    } else {
+      const int64_t idx = ((int64_t)(row / hq) * sink.hq_total + sink.head_off + row % hq) * D + c4 * 4;
+#pragma unroll 1
+      for (int r = 0; r < sink.n_ranks; ++r)
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sink.dst[r]) + idx) = pk;
     }
   }
-  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-  __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-  __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-  uint2 pk;
-  pk.x = *reinterpret_cast<uint32_t*>(&lo);
-  pk.y = *reinterpret_cast<uint32_t*>(&hi);
-  *reinterpret_cast<uint2*>(out + (int64_t)row * D + c4 * 4) = pk;
+  if (sink.n_ranks) sink_signal(sink, gridDim.x, blockDim.x);
 }
 
 // ------------------------------------------------------------------------------ compute proxy
@@ -536,7 +580,7 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
     const int rows = batch * p.hq;
     const int per_block = 128 / (D / 4);
     decode_combine_kernel<D><<<(rows + per_block - 1) / per_block, 128, 0, st>>>(
-        p.part_o, p.part_lse, p.out, rows, p.num_splits);
+        p.part_o, p.part_lse, p.out, rows, p.num_splits, p.hq, p.sink);
     check_rt(cudaGetLastError(), "combine launch");
   }
 }
@@ -552,7 +596,7 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
                           const int32_t* batch_idx, const int32_t* block_table, int max_blocks,
                           int block_size, int box_tokens, float scale, int num_splits,
                           int max_len, void* ws, int64_t ws_bytes, bool paged, cudaStream_t st,
-                          const FusedAppend* fa = nullptr) {
+                          const FusedAppend* fa = nullptr, const GatherSink* sink = nullptr) {
   if (hq % hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
   const int group = hq / hkv;
   if (group > 16) throw Fail(VATTN_UNSUPPORTED, "GQA group larger than 16");
@@ -580,6 +624,11 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
     p.v_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->v_base);
     p.slot_stride = fa->view->slot_stride;
     p.token_stride = fa->view->token_stride;
+  }
+  if (sink && sink->n_ranks) {
+    if (sink->n_ranks > kMaxGatherRanks || sink->hq_total < hq * sink->n_ranks)
+      throw Fail(VATTN_VALUE_ERROR, "gather: bad rank count or head total");
+    p.sink = *sink;
   }
   if (num_splits > 1) {
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, d, num_splits);
@@ -614,7 +663,7 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
 void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void* out, int batch,
                    int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
                    int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st, const void* k_new,
-                   const void* v_new) {
+                   const void* v_new, const GatherSink* sink) {
   check_view(v);
   // Token extent = every row inside the slot stride, so a 64-row tile that starts below seqlen
   // never takes TMA's out-of-bounds path (which faults on VMM-backed maps when the box
@@ -625,7 +674,7 @@ void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void
   const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
   FusedAppend fa{k_new, v_new, &v};
   decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
-                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr);
+                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr, sink);
 }
 
 }  // namespace vattn

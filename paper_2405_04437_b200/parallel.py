@@ -46,3 +46,131 @@ def gather_heads(local, group=None, dim: int = -2):
     out = torch.empty((world * moved.shape[0],) + tuple(moved.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, moved, group=group)
     return out.movedim(0, d)
+
+
+def exchange_handles(blob: bytes, group=None) -> list[bytes]:
+    """All-gather one fixed-size opaque handle per rank (rank order) over torch.distributed."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    got: list = [None] * world
+    dist.all_gather_object(got, bytes(blob), group=group)
+    if any(not isinstance(b, (bytes, bytearray)) or len(b) != len(blob) for b in got):
+        raise RuntimeError("gather handle exchange: ranks disagree on the handle size")
+    return [bytes(b) for b in got]
+
+
+class HeadGather:
+    """Fused output-head all-gather over NVLink peer memory.
+
+    One per rank.  Holds this rank's full output buffer [max_batch, Hq_total, D] bf16 plus the
+    peer mappings of every other rank's buffer; `attention.decode_attention_gather` makes the
+    decode kernel store each output row straight into all of them and `wait()` orders the
+    stream after every rank's rows landed.  Replaces `gather_heads` (NCCL all_gather) for the
+    decode output; `create` is collective (CUDA IPC handles exchanged over torch.distributed),
+    `local_group` simulates `world` ranks on one GPU in one process (tests, single-GPU boxes)."""
+
+    def __init__(self, handle, rank: int, world: int, max_batch: int, hq_total: int, head_dim: int, device: int):
+        self.handle = handle
+        self.rank, self.world = rank, world
+        self.max_batch, self.hq_total, self.head_dim = max_batch, hq_total, head_dim
+        self.device = device
+        self._view = None
+
+    @staticmethod
+    def _out_bytes(max_batch, hq_total, head_dim):
+        if hq_total <= 0 or max_batch <= 0 or head_dim <= 0:
+            raise ValueError("max_batch, hq_total and head_dim must be positive")
+        return max_batch * hq_total * head_dim * 2
+
+    @classmethod
+    def create(cls, max_batch: int, hq_total: int, head_dim: int, group=None, device: int | None = None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from ._abi import IPC_HANDLE_BYTES, check, lib
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if hq_total % world:
+            raise ValueError(f"{hq_total} query heads cannot be split over {world} ranks")
+        dev = torch.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        buf = (C.c_char * IPC_HANDLE_BYTES)()
+        check(lib().vattn_gather_create(dev, rank, world, cls._out_bytes(max_batch, hq_total, head_dim),
+                                        C.byref(h), buf))
+        self = cls(h, rank, world, max_batch, hq_total, head_dim, dev)
+        try:
+            blobs = exchange_handles(bytes(buf), group)
+            allh = (C.c_char * (IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(blobs))
+            check(lib().vattn_gather_open(h, allh))
+        except Exception:
+            self.close()
+            raise
+        return self
+
+    @classmethod
+    def local_group(cls, world: int, max_batch: int, hq_total: int, head_dim: int, device: int = 0):
+        import ctypes as C
+
+        from ._abi import check, lib
+
+        if hq_total % world:
+            raise ValueError(f"{hq_total} query heads cannot be split over {world} ranks")
+        hs = (C.c_void_p * world)()
+        check(lib().vattn_gather_create_local(device, world, cls._out_bytes(max_batch, hq_total, head_dim), hs))
+        return [cls(C.c_void_p(hs[r]), r, world, max_batch, hq_total, head_dim, device) for r in range(world)]
+
+    def output(self, batch: int | None = None):
+        """Non-owning [batch, Hq_total, D] bf16 view of this rank's full output buffer."""
+        import ctypes as C
+
+        import torch
+
+        from ._abi import check, lib
+
+        if self._view is None:
+            ptr = C.c_uint64()
+            check(lib().vattn_gather_output(self.handle, C.byref(ptr)))
+            dev = torch.device("cuda", self.device)
+            n = self._out_bytes(self.max_batch, self.hq_total, self.head_dim)
+            storage = torch._C._construct_storage_from_data_pointer(ptr.value, dev, n)
+            t = torch.empty(0, dtype=torch.bfloat16, device=dev)
+            t.set_(storage, 0, (self.max_batch, self.hq_total, self.head_dim))
+            self._view = t
+        return self._view if batch is None else self._view[:batch]
+
+    def wait(self, stream=None) -> None:
+        import ctypes as C
+
+        import torch
+
+        from ._abi import check, lib
+
+        s = stream if stream is not None else torch.cuda.current_stream()
+        check(lib().vattn_gather_wait(self.handle, C.c_void_p(s.cuda_stream)))
+
+    def timed_out_ranks(self) -> list[int]:
+        """Ranks whose rows a wait gave up on (a rank skipped a gathered launch); syncs."""
+        import ctypes as C
+
+        from ._abi import check, lib
+
+        m = C.c_uint32()
+        check(lib().vattn_gather_check(self.handle, C.byref(m)))
+        return [r for r in range(self.world) if m.value >> r & 1]
+
+    def close(self) -> None:
+        if self.handle is not None:
+            from ._abi import lib
+
+            self._view = None
+            lib().vattn_gather_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

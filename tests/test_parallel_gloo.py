@@ -61,6 +61,18 @@ def _worker(rank, world, port, q):
         out = gather_heads(local)
         assert out.shape == (3, full.q_heads_total, 4)
         assert torch.equal(out[0, :, 0], torch.arange(full.q_heads_total, dtype=torch.float32))
+        # fused-gather setup: IPC handles are exchanged in rank order; creating the device
+        # buffers without a GPU fails loudly (no host fallback for the gather)
+        from paper_2405_04437_b200.parallel import HeadGather, exchange_handles
+        blobs = exchange_handles(bytes([rank + 1]) * 64)
+        assert blobs == [bytes([r + 1]) * 64 for r in range(world)]
+        try:
+            HeadGather.create(4, full.q_heads_total, 128, device=0)
+            raise AssertionError("HeadGather.create succeeded without a GPU")
+        except AssertionError:
+            raise
+        except Exception:
+            pass
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
