@@ -44,6 +44,34 @@ __global__ void probe(float* out, long long* cyc) {
         a = __ffma2_rn(a, make_float2(0.99999f, 0.99999f), make_float2(1e-5f, 1e-5f));
         v[i] = __float_as_uint(a.x); v[i + 1] = __float_as_uint(a.y);
       }
+      if (MODE == 6 && (i & 1) == 0) {   // F2FP pack (cvt.rn.bf16x2.f32) on 4 independent pairs
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(v[i])), "f"(__uint_as_float(v[i + 1])));
+        v[i] ^= r;
+      }
+      if (MODE == 7 && (i & 1) == 0) {   // 2 x MUFU ex2 + 1 F2FP per pair
+        float e0, e1;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(__uint_as_float(v[i])));
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(__uint_as_float(v[i + 1])));
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(e1), "f"(e0));
+        v[i] ^= r;
+        v[i + 1] = __float_as_uint(e1) & 0xBFFFFFFFu;
+      }
+      if (MODE == 8 && (i & 1) == 0) {   // the prefill softmax mix per pair: FMNMX3, FFMA2, 2 MUFU, FADD2, F2FP
+        const float a = __uint_as_float(v[i]), b = __uint_as_float(v[i + 1]);
+        float m;
+        asm volatile("max.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(__uint_as_float(v[(i + 2) & 7])), "f"(a), "f"(b));
+        const float2 x = __ffma2_rn(make_float2(a, b), make_float2(0.125f, 0.125f), make_float2(-m, -m));
+        float e0, e1;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(x.x));
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(x.y));
+        const float2 acc = __fadd2_rn(make_float2(e0, e1), make_float2(a, b));
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(e1), "f"(e0));
+        v[i] = (__float_as_uint(acc.x) ^ r) & 0xBFFFFFFFu;
+        v[i + 1] = __float_as_uint(acc.y) & 0xBFFFFFFFu;
+      }
       if (MODE == 5 && (i & 1) == 0) {   // polynomial exp2 on 4 independent pairs; input kept in [-1, 0]
         float2 a = make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
         a = exp2_poly2(a);
@@ -65,27 +93,34 @@ int main() {
   cudaMalloc(&o, 4);
   cudaMalloc(&c, 1024 * 8);
   const char* names[] = {"ex2.approx.ftz.f32", "ex2.approx.ftz.bf16x2", "ex2.approx.f16x2", "fma.rn.f32",
-                         "ffma2 (f32x2)", "exp2_poly2 (per pair)"};
-  for (int m = 0; m < 6; ++m) {
-    for (int rep = 0; rep < 2; ++rep) {
-      if (m == 0) probe<0><<<148, 512>>>(o, c);
-      if (m == 1) probe<1><<<148, 512>>>(o, c);
-      if (m == 2) probe<2><<<148, 512>>>(o, c);
-      if (m == 3) probe<3><<<148, 512>>>(o, c);
-      if (m == 4) probe<4><<<148, 512>>>(o, c);
-      if (m == 5) probe<5><<<148, 512>>>(o, c);
+                         "ffma2 (f32x2)", "exp2_poly2 (per pair)", "cvt.rn.bf16x2.f32", "2 ex2 + 1 cvt (pair)",
+                         "softmax mix (pair)"};
+  for (int threads : {512, 128}) {
+    printf("--- %d threads per SM (%d warps per sub-partition)\n", threads, threads / 128);
+    for (int m = 0; m < 9; ++m) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (m == 0) probe<0><<<148, threads>>>(o, c);
+        if (m == 1) probe<1><<<148, threads>>>(o, c);
+        if (m == 2) probe<2><<<148, threads>>>(o, c);
+        if (m == 3) probe<3><<<148, threads>>>(o, c);
+        if (m == 4) probe<4><<<148, threads>>>(o, c);
+        if (m == 5) probe<5><<<148, threads>>>(o, c);
+        if (m == 6) probe<6><<<148, threads>>>(o, c);
+        if (m == 7) probe<7><<<148, threads>>>(o, c);
+        if (m == 8) probe<8><<<148, threads>>>(o, c);
+      }
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("%s: %s\n", names[m], cudaGetErrorString(e)); continue; }
+      long long h[148];
+      cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
+      double cyc = 0;
+      for (int i = 0; i < 148; ++i) cyc += h[i];
+      cyc /= 148;
+      // thread-level operations per SM (one CTA per SM); modes >= 4 do 4 packed ops per 8 registers
+      const double instr = (double)threads * kIters * ((m >= 4) ? 4 : 8);
+      const double results = instr * ((m == 0 || m == 3 || m == 6) ? 1 : 2);
+      printf("%-24s %6.2f instr/clk/SM  %6.2f results/clk/SM\n", names[m], instr / cyc, results / cyc);
     }
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) { printf("%s: %s\n", names[m], cudaGetErrorString(e)); continue; }
-    long long h[148];
-    cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
-    double cyc = 0;
-    for (int i = 0; i < 148; ++i) cyc += h[i];
-    cyc /= 148;
-    // thread-level operations per SM (one CTA per SM); modes 4/5 do 4 packed ops per 8 registers
-    const double instr = 512.0 * kIters * ((m >= 4) ? 4 : 8);
-    const double results = instr * ((m == 0 || m == 3) ? 1 : 2);
-    printf("%-24s %6.2f instr/clk/SM  %6.2f results/clk/SM\n", names[m], instr / cyc, results / cyc);
   }
   return 0;
 }
