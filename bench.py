@@ -633,6 +633,74 @@ def extra_y34_shards(local):
     return out
 
 
+def extra_decode_growth(local, steps=96, warm=8):
+    """Exposed map ms/iter (BASELINE metric) while decode contexts GROW across page-group
+    boundaries: Llama-3-8B shape, 32 layers, B 64, contexts staggered 3584 + 16*b (mean ~4.1K)
+    so a row crosses a 2 MiB group (64 buffers to map) every ~16 steps.  Each step = allocator
+    step + 32 fused append+decode launches + a host sync (the token sampling point of a serving
+    loop).  Modes: sync (maps inside step), overlapped (the reference's plan_overlap ->
+    execute_plan on the background thread during the kernels), overlapped + physical prefetch
+    of decode growth 64 tokens ahead (logical state unchanged)."""
+    import torch
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention_append
+    from paper_2405_04437_b200.geometry import llama3_8b
+
+    dev = torch.device("cuda", local)
+    g = llama3_8b(max_context=8192, max_batch=64)
+    B, N, hq, hkv, d = g.max_batch, g.n_layers, g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
+    ctx0 = [3584 + 16 * b for b in range(B)]
+    gen = torch.Generator(device=dev).manual_seed(0)
+    q = torch.randn(N, B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    kn = torch.randn(N, B, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    res = {"workload": "llama-3-8b decode b64, ctx 3584+16*b growing, 32 layers, 2 MiB groups",
+           "steps": steps}
+    for mode, pf in (("sync", 0), ("overlapped", 0), ("overlapped_prefetch64", 64)):
+        tok = g.per_token_layer_bytes
+        groups = max(math.ceil((c + steps + warm + 2) * tok / MB2) for c in ctx0)
+        mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=(groups + 1) * 2 * N * B * MB2,
+                                              eager_groups=0, reclaim_threshold=0.0),
+                             backend="cuda", device=local, prefetch_tokens=pf)
+        rids = [mgr.alloc_reqid() for _ in range(B)]
+        seq = [0] * B
+        for r, c in zip(rids, ctx0):
+            seq[r] = c
+        assert mgr.step(seq).ok
+        idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+        pos = torch.tensor([seq[r] for r in rids], dtype=torch.int32, device=dev)
+        exposed, crossings = [], 0
+        torch.cuda.synchronize()
+        st0 = mgr.driver_stats()
+        for it in range(warm + steps):
+            nxt = [s + 1 for s in seq]
+            crossed = sum(1 for a, b in zip(seq, nxt) if a and -(-a * tok // MB2) != -(-b * tok // MB2))
+            t0 = time.perf_counter()
+            assert mgr.step(nxt).ok
+            dt = time.perf_counter() - t0
+            for layer in range(N):
+                decode_attention_append(mgr, layer, q[layer], kn[layer], kn[layer], pos, idx, out=out[layer])
+            pos.add_(1)
+            seq = nxt
+            if mode != "sync":
+                mgr.bg_submit(mgr.plan_overlap([s + 1 for s in seq]), prefetch=pf > 0)
+            torch.cuda.synchronize()
+            if it >= warm:
+                exposed.append(dt * 1e3)
+                crossings += crossed
+        if mode != "sync":
+            mgr.bg_wait()
+        st = mgr.driver_stats()
+        mgr.close()
+        res[mode] = {"exposed_map_ms_per_iter": statistics.mean(exposed), "exposed_map_ms_p99":
+                     sorted(exposed)[int(0.99 * (len(exposed) - 1))], "exposed_map_ms_max": max(exposed),
+                     "rows_crossing_a_group": crossings, "driver_maps": st["real_maps"] - st0["real_maps"],
+                     "set_access_us_per_call": (st["real_set_access_wall_us"] - st0["real_set_access_wall_us"])
+                     / max(1, st["real_set_access_calls"] - st0["real_set_access_calls"])}
+    return res
+
+
 def extra_serving(local, requests=48):
     """BASELINE config 5: Algorithm-1 loop on the config-5 trace (Llama-3-8B shape), real kernels
     + dense-layer compute proxy (reference IterationModel), sync vs overlapped+deferred+eager."""
@@ -809,7 +877,8 @@ def main(argv=None):
         }
         if not args.no_extras and world == 1:
             extras = {}
-            for name, fn in (("prefill", extra_prefill), ("paged_vs_contiguous", extra_paged),
+            for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
+                             ("paged_vs_contiguous", extra_paged),
                              ("y34_shards", extra_y34_shards), ("libraries", extra_libraries),
                              ("serving", extra_serving)):
                 try:

@@ -242,6 +242,7 @@ class Manager {
  public:
   void prefetch();
  private:
+  CUmemGenericAllocationHandle steal_spec_locked(std::unique_lock<std::mutex>& lk);
   void real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle hnd);
   void real_unmap(int32_t b, int64_t off);
   void flush_access();
@@ -300,8 +301,25 @@ class Manager {
   std::deque<int64_t> spec_order_;
   int64_t prefetch_tokens_ = 0;
   int64_t prefetch_slots_ = 0, prefetch_slot_tokens_ = 0;   // speculative eager for likely-next slots
-  std::atomic<bool> prefetch_cancel_{false};   // set by any join: prefetch is optional work
+  std::atomic<bool> prefetch_cancel_{false};   // legacy; the detached worker never blocks a join
   int64_t spec_maps_ = 0, spec_hits_ = 0, spec_steals_ = 0;
+  // Detached prefetch worker: maps the speculative pages the bg thread chose, holding no state
+  // but its own (pf_mu_ guards phys_free_, spec_, spec_order_ and everything pf_*), so a slow
+  // or stalled driver call never blocks step / alloc / free; a control-thread map waits only
+  // when it needs exactly the page in flight.
+  std::thread pf_thread_;
+  mutable std::mutex pf_mu_;
+  std::condition_variable pf_cv_;
+  std::vector<int64_t> pf_targets_;
+  size_t pf_next_ = 0;
+  std::unordered_set<int64_t> pf_pending_;
+  int64_t pf_inflight_ = -1;
+  size_t pf_reserve_ = 0;
+  bool pf_stop_ = false;
+  int64_t pf_maps_ = 0, pf_access_ = 0, pf_errors_ = 0;
+  double pf_map_us_ = 0, pf_access_us_ = 0;
+  void pf_loop();
+  void pf_stop();
   CUmemAllocationProp prop_{};
   CUmemAccessDesc access_{};
   std::vector<int64_t> run_begin_, run_end_;  // pending cuMemSetAccess page runs per buffer
@@ -447,6 +465,61 @@ Manager::Manager(const vattn_config& c) {
   init_wall_us_ = now_us() - t0;
 
   bg_thread_ = std::thread([this] { bg_loop(); });
+  if (real() && (prefetch_tokens_ > 0 || prefetch_slots_ > 0)) pf_thread_ = std::thread([this] { pf_loop(); });
+}
+
+void Manager::pf_stop() {
+  {
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    pf_stop_ = true;
+  }
+  pf_cv_.notify_all();
+  if (pf_thread_.joinable()) pf_thread_.join();
+}
+
+void Manager::pf_loop() {
+  const Driver& d = driver();
+  if (d.CtxSetCurrent(ctx_) != CUDA_SUCCESS) return;
+  std::unique_lock<std::mutex> lk(pf_mu_);
+  for (;;) {
+    pf_cv_.wait(lk, [&] { return pf_stop_ || pf_next_ < pf_targets_.size(); });
+    if (pf_stop_) return;
+    const int64_t key = pf_targets_[pf_next_++];
+    if (!pf_pending_.erase(key) || spec_.count(key)) continue;   // claimed by a logical map meanwhile
+    if (phys_free_.size() <= pf_reserve_) {                       // keep handles for the reference path
+      pf_next_ = pf_targets_.size();
+      pf_pending_.clear();
+      continue;
+    }
+    const auto h = phys_free_.back();
+    phys_free_.pop_back();
+    pf_inflight_ = key;
+    lk.unlock();
+    const int64_t b = key / buffer_size_, off = key % buffer_size_;
+    const double t0 = now_us();
+    bool ok = d.MemMap(va_[b] + off, (size_t)t_, 0, h, 0) == CUDA_SUCCESS;
+    const double t1 = now_us();
+    if (ok && d.MemSetAccess(va_[b] + off, (size_t)t_, &access_, 1) != CUDA_SUCCESS) {
+      d.MemUnmap(va_[b] + off, (size_t)t_);
+      ok = false;
+    }
+    const double t2 = now_us();
+    lk.lock();
+    pf_inflight_ = -1;
+    pf_map_us_ += t1 - t0;
+    pf_access_us_ += t2 - t1;
+    if (ok) {
+      pf_maps_ += 1;
+      pf_access_ += 1;
+      spec_[key] = h;
+      spec_order_.push_back(key);
+      spec_maps_ += 1;
+    } else {
+      pf_errors_ += 1;
+      phys_free_.push_back(h);
+    }
+    pf_cv_.notify_all();
+  }
 }
 
 Manager::~Manager() {
@@ -457,6 +530,7 @@ Manager::~Manager() {
   }
   bg_cv_.notify_all();
   if (bg_thread_.joinable()) bg_thread_.join();
+  pf_stop();
   if (!real()) return;
   const Driver& d = driver();
   d.CtxSetCurrent(ctx_);
@@ -528,6 +602,7 @@ double Manager::dev_precreate(int64_t count) {
       check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
       real_create_us_ += now_us() - t0;
       real_creates_ += 1;
+      std::lock_guard<std::mutex> lk(pf_mu_);
       phys_free_.push_back(h);
     }
   }
@@ -553,14 +628,19 @@ double Manager::dev_map(int32_t b, int64_t off, int64_t hid) {
   if (off < 0 || off + t_ > buffer_size_) throw Fail(VATTN_MAPPING_ERROR, "offset out of range");
   if (buf_maps_[b].count(off)) throw Fail(VATTN_MAPPING_ERROR, "offset already backed");
   if (real()) {
-    auto sp = spec_.find((int64_t)b * buffer_size_ + off);
+    const int64_t key = (int64_t)b * buffer_size_ + off;
+    std::unique_lock<std::mutex> lk(pf_mu_);
+    pf_pending_.erase(key);                                     // the worker must not map it now
+    pf_cv_.wait(lk, [&] { return pf_inflight_ != key; });       // unless it already is
+    auto sp = spec_.find(key);
     if (sp != spec_.end()) {            // prefetched: already mapped and accessible, adopt it
       if (h.real) phys_free_.push_back(h.real);
       h.real = sp->second;
       spec_.erase(sp);
       spec_hits_ += 1;
     } else {
-      if (!h.real) h.real = steal_spec();
+      if (!h.real) h.real = steal_spec_locked(lk);
+      lk.unlock();
       real_map(b, off, h.real);
     }
   }
@@ -595,28 +675,46 @@ double Manager::dev_unmap_release(int32_t b, int64_t off) {
 // An unattached physical handle for a shadow handle; 0 = "all of them are holding speculative
 // pages": resolved in dev_map (adopt the page if it is the one being mapped, else steal one).
 CUmemGenericAllocationHandle Manager::take_unattached() {
+  std::lock_guard<std::mutex> lk(pf_mu_);
   if (!phys_free_.empty()) {
     auto h = phys_free_.back();
     phys_free_.pop_back();
     return h;
   }
-  if (spec_.empty()) throw Fail(VATTN_BAD_STATE, "physical pool accounting error");
+  if (spec_.empty() && pf_inflight_ < 0) throw Fail(VATTN_BAD_STATE, "physical pool accounting error");
   return 0;
 }
 
 CUmemGenericAllocationHandle Manager::steal_spec() {
-  while (!spec_order_.empty()) {
-    const int64_t key = spec_order_.front();
-    spec_order_.pop_front();
-    auto it = spec_.find(key);
-    if (it == spec_.end()) continue;   // already adopted
-    const auto h = it->second;
-    spec_.erase(it);
-    real_unmap((int32_t)(key / buffer_size_), key % buffer_size_);
-    spec_steals_ += 1;
-    return h;
+  std::unique_lock<std::mutex> lk(pf_mu_);
+  return steal_spec_locked(lk);
+}
+
+// Take a speculative page's handle back for the reference path (unmapping it); waits for the
+// worker's page in flight when it holds the last one.  Called and returns with `lk` held.
+CUmemGenericAllocationHandle Manager::steal_spec_locked(std::unique_lock<std::mutex>& lk) {
+  for (;;) {
+    if (!phys_free_.empty()) {        // a failed prefetch may have returned one meanwhile
+      auto h = phys_free_.back();
+      phys_free_.pop_back();
+      return h;
+    }
+    while (!spec_order_.empty()) {
+      const int64_t key = spec_order_.front();
+      spec_order_.pop_front();
+      auto it = spec_.find(key);
+      if (it == spec_.end()) continue;   // already adopted
+      const auto h = it->second;
+      spec_.erase(it);
+      spec_steals_ += 1;
+      lk.unlock();
+      real_unmap((int32_t)(key / buffer_size_), key % buffer_size_);
+      lk.lock();
+      return h;
+    }
+    if (pf_inflight_ < 0) throw Fail(VATTN_BAD_STATE, "no speculative page to steal");
+    pf_cv_.wait(lk, [&] { return pf_inflight_ < 0; });
   }
-  throw Fail(VATTN_BAD_STATE, "no speculative page to steal");
 }
 
 // Physical prefetch (B200 addition, not in the reference): map the pages each active slot will
@@ -626,33 +724,26 @@ CUmemGenericAllocationHandle Manager::steal_spec() {
 // group's worth of handles free so the reference path rarely has to steal.
 void Manager::prefetch() {
   if (!real() || (prefetch_tokens_ <= 0 && prefetch_slots_ <= 0)) return;
-  const size_t reserve = (size_t)(2 * buffer_count_);
-  // map [g0, g1) of slot r speculatively; false = stop (pool reserve reached or cancelled)
-  auto spec_range = [&](int32_t r, int64_t g0, int64_t g1) {
+  // Runs inside a bg window (state owned): choose the pages, hand them to the worker, return.
+  // (urgency, key): pages are mapped soonest-needed first — decode growth by the tokens left
+  // before the row reaches the page, then the speculative-eager slots in alloc_reqid order
+  std::vector<std::pair<int64_t, int64_t>> targets;
+  const int64_t tokens_per_group = t_ / per_buffer_token_bytes_;
+  auto spec_range = [&](int32_t r, int64_t g0, int64_t g1, int64_t urgency0, int64_t ctx) {
     for (int64_t g = g0; g < g1; ++g) {
       const int64_t off = slot_offset(r, g);
-      for (int64_t b = 0; b < buffer_count_; ++b) {
-        const int64_t key = b * buffer_size_ + off;
-        if (spec_.count(key) || buf_maps_[b].count(off)) continue;
-        if (phys_free_.size() <= reserve || prefetch_cancel_.load(std::memory_order_relaxed)) return false;
-        const auto h = phys_free_.back();
-        phys_free_.pop_back();
-        real_map((int32_t)b, off, h);
-        flush_access();                 // per page: a join waits for at most one driver call
-        spec_[key] = h;
-        spec_order_.push_back(key);
-        spec_maps_ += 1;
-      }
+      const int64_t urgency = urgency0 + (ctx >= 0 ? g * tokens_per_group - ctx : g);
+      for (int64_t b = 0; b < buffer_count_; ++b)
+        if (!buf_maps_[b].count(off)) targets.emplace_back(urgency, b * buffer_size_ + off);
     }
-    return true;
   };
   // 1. decode growth of active slots within prefetch_tokens_ more tokens
   if (prefetch_tokens_ > 0)
     for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
       const Slot& s = slots_[r];
       if (!s.active) continue;
-      const int64_t target = std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_);
-      if (!spec_range(r, s.mapped_groups, target)) { flush_access(); return; }
+      spec_range(r, s.mapped_groups, std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_),
+                 0, s.context_len);
     }
   // 2. speculative eager: the slots alloc_reqid would hand out next (eager slot first, then by
   //    (mapped_groups, -req_id), manager.py:166-174) up to prefetch_slot_tokens_ of prompt
@@ -667,13 +758,30 @@ void Manager::prefetch() {
     });
     const int64_t target = std::min(groups_required(prefetch_slot_tokens_), groups_per_slot_);
     for (size_t i = 0; i < cand.size() && (int64_t)i < prefetch_slots_; ++i)
-      if (!spec_range(cand[i], slots_[cand[i]].mapped_groups, target)) break;
+      spec_range(cand[i], slots_[cand[i]].mapped_groups, target, (int64_t)(1 + i) << 40, -1);
   }
-  flush_access();
+  std::stable_sort(targets.begin(), targets.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  {
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    pf_reserve_ = (size_t)(2 * buffer_count_);   // one group's worth of handles stays free
+    pf_targets_.clear();
+    pf_pending_.clear();
+    for (const auto& t : targets)
+      if (!spec_.count(t.second) && t.second != pf_inflight_ && pf_pending_.insert(t.second).second)
+        pf_targets_.push_back(t.second);
+    pf_next_ = 0;
+  }
+  pf_cv_.notify_all();
 }
 
 CUmemGenericAllocationHandle Manager::real_create() {
-  if (!phys_free_.empty() || !spec_.empty()) return take_unattached();
+  bool none_unattached;
+  {
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    none_unattached = phys_free_.empty() && spec_.empty() && pf_inflight_ < 0;
+  }
+  if (!none_unattached) return take_unattached();
   CUmemGenericAllocationHandle h = 0;
   const double t0 = now_us();
   check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
@@ -683,7 +791,11 @@ CUmemGenericAllocationHandle Manager::real_create() {
 }
 
 void Manager::real_release(CUmemGenericAllocationHandle h) {
-  if (!release_physical_) { phys_free_.push_back(h); return; }
+  if (!release_physical_) {
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    phys_free_.push_back(h);
+    return;
+  }
   check_cu(driver().MemRelease(h), "cuMemRelease");
   real_releases_ += 1;
 }
@@ -1143,15 +1255,16 @@ void Manager::counters(vattn_counters* o) const {
   o->next_handle_id = next_hid_;
   o->init_us = init_us_;
   o->charged_us = charged_total();
-  o->real_maps = real_maps_;
+  std::lock_guard<std::mutex> lk(pf_mu_);
+  o->real_maps = real_maps_ + pf_maps_;
   o->real_unmaps = real_unmaps_;
-  o->real_set_access_calls = real_access_;
+  o->real_set_access_calls = real_access_ + pf_access_;
   o->real_creates = real_creates_;
   o->real_releases = real_releases_;
-  o->real_map_wall_us = real_map_us_;
+  o->real_map_wall_us = real_map_us_ + pf_map_us_;
   o->real_unmap_wall_us = real_unmap_us_;
   o->real_create_wall_us = real_create_us_;
-  o->real_set_access_wall_us = real_access_us_;
+  o->real_set_access_wall_us = real_access_us_ + pf_access_us_;
   o->init_wall_us = init_wall_us_;
   o->spec_maps = spec_maps_;
   o->spec_hits = spec_hits_;
