@@ -110,11 +110,21 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("VATTN_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         dist.init_process_group(backend=backend)
+    if os.environ.get("VATTN_BENCH_ONE_GPU"):   # test harness: every rank on cuda:0 (gloo backend)
+        local = 0
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
     return world, rank, local
+
+
+def _reduce_device():
+    import torch
+    import torch.distributed as dist
+
+    nccl = dist.is_initialized() and dist.get_backend() == "nccl"
+    return torch.device("cuda") if nccl else torch.device("cpu")
 
 
 def barrier():
@@ -130,8 +140,7 @@ def max_over_ranks(x: float) -> float:
 
     if not (dist.is_available() and dist.is_initialized()):
         return x
-    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -400,7 +409,7 @@ def head_gather_compare(mgr, q, out, pos, idx, splits, world, local, iters=20):
         hg = HeadGather.create(B, hq * world, d, device=local)
     except Exception as e:          # report, but every rank must agree before timing
         err = repr(e)[:200]
-    ok = torch.tensor([0 if err else 1], device=q.device)
+    ok = torch.tensor([0 if err else 1], device=_reduce_device())
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
 
     def timed(fn):
@@ -416,15 +425,20 @@ def head_gather_compare(mgr, q, out, pos, idx, splits, world, local, iters=20):
         torch.cuda.synchronize()
         return max_over_ranks(e0.elapsed_time(e1) / iters * 1e3)
 
-    res = {"layer_decode_us": timed(lambda: decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits)),
-           "nccl_us": timed(lambda: gather_heads(decode_attention(mgr, 0, q[0], pos, idx, out=out[0],
-                                                                  num_splits=splits)))}
+    res = {"layer_decode_us": timed(lambda: decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits))}
+    nccl = dist.get_backend() == "nccl"
+    if nccl:
+        res["nccl_us"] = timed(lambda: gather_heads(decode_attention(mgr, 0, q[0], pos, idx, out=out[0],
+                                                                     num_splits=splits)))
     if int(ok.item()) == 1:
         res["fused_us"] = timed(lambda: decode_attention_gather(mgr, 0, q[0], hg, pos, idx, num_splits=splits))
-        ref = gather_heads(decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits))
         got = decode_attention_gather(mgr, 0, q[0], hg, pos, idx, num_splits=splits)
+        mine = decode_attention(mgr, 0, q[0], pos, idx, out=out[0], num_splits=splits)
         torch.cuda.synchronize()
-        res["fused_equals_nccl"] = bool(torch.equal(ref, got))
+        r0 = dist.get_rank() * hq
+        res["fused_rows_equal_local"] = bool(torch.equal(got[:, r0:r0 + hq], mine))
+        if nccl:
+            res["fused_equals_nccl"] = bool(torch.equal(gather_heads(mine), got))
         res["timed_out_ranks"] = hg.timed_out_ranks()
     else:
         res["fused_error"] = err or "a peer rank failed to set up the gather"

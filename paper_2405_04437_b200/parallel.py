@@ -98,15 +98,26 @@ class HeadGather:
         dev = torch.cuda.current_device() if device is None else device
         h = C.c_void_p()
         buf = (C.c_char * IPC_HANDLE_BYTES)()
-        check(lib().vattn_gather_create(dev, rank, world, cls._out_bytes(max_batch, hq_total, head_dim),
-                                        C.byref(h), buf))
-        self = cls(h, rank, world, max_batch, hq_total, head_dim, dev)
+        self, err = None, None
         try:
-            blobs = exchange_handles(bytes(buf), group)
-            allh = (C.c_char * (IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(blobs))
+            check(lib().vattn_gather_create(dev, rank, world, cls._out_bytes(max_batch, hq_total, head_dim),
+                                            C.byref(h), buf))
+            self = cls(h, rank, world, max_batch, hq_total, head_dim, dev)
+        except Exception as e:      # still take part in the exchange, so no peer blocks in it
+            err = e
+        # byte 0: this rank's setup status, then its IPC handle
+        blobs = exchange_handles((b"\1" if err is None else b"\0") + bytes(buf), group)
+        failed = [r for r, b in enumerate(blobs) if b[0] != 1]
+        try:
+            if err is not None:
+                raise err
+            if failed:
+                raise RuntimeError(f"HeadGather: ranks {failed} failed to create their buffers")
+            allh = (C.c_char * (IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(b[1:] for b in blobs))
             check(lib().vattn_gather_open(h, allh))
         except Exception:
-            self.close()
+            if self is not None:
+                self.close()
             raise
         return self
 

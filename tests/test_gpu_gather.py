@@ -147,3 +147,68 @@ def test_wait_times_out_when_a_rank_skips_its_launch(monkeypatch):
     assert g0.timed_out_ranks() == [1]
     g0.close()
     g1.close()
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import sys
+
+    from conftest import ROOT
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2405_04437_b200.attention import decode_attention_gather_raw
+        from paper_2405_04437_b200.parallel import HeadGather
+
+        dev = torch.device("cuda", 0)        # both ranks on one GPU: same IPC + signalling path
+        torch.cuda.set_device(dev)
+        B, hq, hkv, d, lens = 4, 16, 4, 128, [700, 1, 64, 2049]
+        gen = torch.Generator().manual_seed(3)
+        k = _rand((B, 2112, hkv, d), gen)
+        v = _rand((B, 2112, hkv, d), gen)
+        qq = _rand((B, hq, d), gen)
+        seq = torch.tensor(lens, dtype=torch.int32)
+        ref = decode_ref(qq, k, v, seq)
+        hg = HeadGather.create(B, hq, d, device=0)
+        hk, hh = hkv // world, hq // world
+        kc = k[:, :, rank * hk:(rank + 1) * hk].contiguous().to(dev)
+        vc = v[:, :, rank * hk:(rank + 1) * hk].contiguous().to(dev)
+        qr = qq[:, rank * hh:(rank + 1) * hh].contiguous().to(dev)
+        for _ in range(3):
+            out = decode_attention_gather_raw(qr, kc, vc, hg, seq.to(dev))
+        torch.cuda.synchronize()
+        err = max_rel_err(out.cpu(), ref)
+        bad = hg.timed_out_ranks()
+        dist.barrier()
+        hg.close()
+        q.put((rank, "ok" if err <= TOL and not bad else f"err={err} timed_out={bad}"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)[:300]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_gather_through_cuda_ipc():
+    """Two processes (ranks) share one GPU: the CUDA IPC handle exchange, peer mapping and
+    cross-process flag signalling of HeadGather.create run exactly as on two GPUs."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    _cuda()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, "ok"), (1, "ok")], res

@@ -66,13 +66,14 @@ def _worker(rank, world, port, q):
         from paper_2405_04437_b200.parallel import HeadGather, exchange_handles
         blobs = exchange_handles(bytes([rank + 1]) * 64)
         assert blobs == [bytes([r + 1]) * 64 for r in range(world)]
-        try:
+        try:      # every rank fails (no GPU) but still completes the exchange: no rank hangs
             HeadGather.create(4, full.q_heads_total, 128, device=0)
             raise AssertionError("HeadGather.create succeeded without a GPU")
         except AssertionError:
             raise
         except Exception:
             pass
+        dist.barrier()
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
