@@ -96,6 +96,11 @@ typedef struct vattn_config {
    * `prefetch_slot_tokens` tokens of prompt (speculative eager; logical state untouched) */
   int32_t prefetch_slots;
   int32_t prefetch_slot_tokens;
+  /* B200 addition: a trimmed or reclaimed page-group stays physically mapped as a speculative
+   * page (logically released exactly as the reference does); the driver unmap happens only if
+   * its handle is needed elsewhere, or never when the slot grows back over it.  Needs
+   * release_physical = 0. */
+  int32_t lazy_unmap;
 } vattn_config;
 
 typedef struct vattn_t vattn_t;
@@ -120,6 +125,7 @@ typedef struct vattn_counters {
   double real_map_wall_us, real_unmap_wall_us, real_create_wall_us, real_set_access_wall_us;
   double init_wall_us;
   int64_t spec_maps, spec_hits, spec_steals, spec_pages;   /* physical prefetch */
+  int64_t lazy_unmaps;         /* logical unmaps that kept the page mapped (lazy_unmap) */
 } vattn_counters;
 
 typedef struct vattn_bg_result {
@@ -201,6 +207,18 @@ vattn_status vattn_buffer_mappings(vattn_t* h, int32_t buffer_id, int64_t* offse
 /* drain the event log: triples (0=map|1=unmap, buffer_id, offset) */
 vattn_status vattn_events(vattn_t* h, int64_t* triples, int64_t cap_entries, int64_t* n);
 vattn_status vattn_buffer_base(vattn_t* h, int32_t buffer_id, uint64_t* dptr);
+
+/* ---- admission-aware prefetch (B200 addition; logical state untouched) --------------------
+ * The next `k` slots consecutive alloc_reqid calls would return now (eager slot first, then by
+ * (mapped_groups, -req_id) with plan credits, manager.py:163-178); out[k], *n = how many. */
+vattn_status vattn_predict_alloc(vattn_t* h, int32_t k, int32_t* out, int32_t* n);
+/* Ask the prefetch worker to back rows [0, tokens[i]) of slots[i] physically (queued prompts
+ * about to be admitted there); replaces the previous hint set; used by the next background job
+ * submitted with VATTN_BG_PREFETCH. */
+vattn_status vattn_prefetch_hint(vattn_t* h, const int32_t* slots, const int64_t* tokens, int32_t n);
+/* *ready = 1 when every page-group of rows [0, tokens) of `slot` is mapped in every buffer,
+ * logically or speculatively (a step to that length then needs no driver call). */
+vattn_status vattn_slot_ready(vattn_t* h, int32_t slot, int64_t tokens, int32_t* ready);
 
 /* Table 2 analog measured on this device: mean µs per call at `page_bytes` (out[10]: reserve,
  * create, map, set_access, unmap, release, address_free, set_access-per-page batched by `run`,

@@ -37,7 +37,7 @@ class Config(C.Structure):
         ("backend", c_i32), ("device", c_i32), ("release_physical", c_i32),
         ("log_events", c_i32), ("batch_set_access", c_i32),
         ("latency", C.POINTER(LatencyEntry)), ("n_latency", c_i32), ("prefetch_tokens", c_i32),
-        ("prefetch_slots", c_i32), ("prefetch_slot_tokens", c_i32),
+        ("prefetch_slots", c_i32), ("prefetch_slot_tokens", c_i32), ("lazy_unmap", c_i32),
     ]
 
 
@@ -54,7 +54,7 @@ class Counters(C.Structure):
             "real_maps", "real_unmaps", "real_set_access_calls", "real_creates", "real_releases")] + [
         (n, c_f64) for n in ("real_map_wall_us", "real_unmap_wall_us", "real_create_wall_us",
                              "real_set_access_wall_us", "init_wall_us")] + [
-        (n, c_i64) for n in ("spec_maps", "spec_hits", "spec_steals", "spec_pages")]
+        (n, c_i64) for n in ("spec_maps", "spec_hits", "spec_steals", "spec_pages", "lazy_unmaps")]
 
 
 class BgResult(C.Structure):
@@ -104,6 +104,9 @@ SIGNATURES = {
     "vattn_buffer_mappings": (c_i32, [c_vp, c_i32, P_i64, P_i64, c_i64, P_i64]),
     "vattn_events": (c_i32, [c_vp, P_i64, c_i64, P_i64]),
     "vattn_buffer_base": (c_i32, [c_vp, c_i32, C.POINTER(c_u64)]),
+    "vattn_predict_alloc": (c_i32, [c_vp, c_i32, P_i32, P_i32]),
+    "vattn_prefetch_hint": (c_i32, [c_vp, P_i32, P_i64, c_i32]),
+    "vattn_slot_ready": (c_i32, [c_vp, c_i32, c_i64, P_i32]),
     "vattn_kv_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "vattn_decode": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
     "vattn_decode_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),

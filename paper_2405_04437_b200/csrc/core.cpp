@@ -164,6 +164,9 @@ struct Slot {  // manager.py:66-75
   int64_t freed_seq = 0;
 };
 
+// alloc_reqid's ranking key (see Manager::alloc_reqid): mapped groups minus plan credits
+static inline int64_t ranked(const Slot& s, int64_t credit) { return s.mapped_groups - credit; }
+
 struct Handle {  // vmm.py:130-138 plus the real driver handle
   bool mapped = false;
   int32_t buf = -1;
@@ -241,6 +244,9 @@ class Manager {
   void real_release(CUmemGenericAllocationHandle hnd);
  public:
   void prefetch();
+  std::vector<int32_t> predict_alloc(int32_t k) const;
+  void prefetch_hint(const int32_t* slots, const int64_t* tokens, int32_t n);
+  bool slot_ready(int32_t slot, int64_t tokens) const;
  private:
   CUmemGenericAllocationHandle steal_spec_locked(std::unique_lock<std::mutex>& lk);
   void real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle hnd);
@@ -301,6 +307,9 @@ class Manager {
   std::deque<int64_t> spec_order_;
   int64_t prefetch_tokens_ = 0;
   int64_t prefetch_slots_ = 0, prefetch_slot_tokens_ = 0;   // speculative eager for likely-next slots
+  bool lazy_unmap_ = false;
+  int64_t lazy_unmaps_ = 0;
+  std::vector<std::pair<int32_t, int64_t>> pf_hints_;       // (slot, tokens) of queued prompts (pf_mu_)
   std::atomic<bool> prefetch_cancel_{false};   // legacy; the detached worker never blocks a join
   int64_t spec_maps_ = 0, spec_hits_ = 0, spec_steals_ = 0;
   // Detached prefetch worker: maps the speculative pages the bg thread chose, holding no state
@@ -384,6 +393,7 @@ Manager::Manager(const vattn_config& c) {
   prefetch_tokens_ = std::max<int64_t>(0, c.prefetch_tokens);
   prefetch_slots_ = std::max<int64_t>(0, c.prefetch_slots);
   prefetch_slot_tokens_ = std::max<int64_t>(0, c.prefetch_slot_tokens);
+  lazy_unmap_ = c.lazy_unmap != 0 && c.release_physical == 0;
 
   lat_ = LatencyTable::table2();
   if (c.latency && c.n_latency > 0) {
@@ -465,7 +475,7 @@ Manager::Manager(const vattn_config& c) {
   init_wall_us_ = now_us() - t0;
 
   bg_thread_ = std::thread([this] { bg_loop(); });
-  if (real() && (prefetch_tokens_ > 0 || prefetch_slots_ > 0)) pf_thread_ = std::thread([this] { pf_loop(); });
+  if (real()) pf_thread_ = std::thread([this] { pf_loop(); });
 }
 
 void Manager::pf_stop() {
@@ -660,8 +670,16 @@ double Manager::dev_unmap_release(int32_t b, int64_t off) {
   const int64_t hid = it->second;
   Handle h = handles_[hid];
   if (real()) {
-    real_unmap(b, off);
-    real_release(h.real);
+    if (lazy_unmap_) {     // keep it mapped as a speculative page: no driver call now
+      std::lock_guard<std::mutex> lk(pf_mu_);
+      const int64_t key = (int64_t)b * buffer_size_ + off;
+      spec_[key] = h.real;
+      spec_order_.push_back(key);
+      lazy_unmaps_ += 1;
+    } else {
+      real_unmap(b, off);
+      real_release(h.real);
+    }
   }
   buf_maps_[b].erase(it);
   handles_.erase(hid);
@@ -722,8 +740,50 @@ CUmemGenericAllocationHandle Manager::steal_spec_locked(std::unique_lock<std::mu
 // shadow considers unattached.  Logical state (slots, counters, events) is untouched; when the
 // reference logic maps such a page later it adopts the mapping with no driver call.  Keeps one
 // group's worth of handles free so the reference path rarely has to steal.
+std::vector<int32_t> Manager::predict_alloc(int32_t k) const {
+  std::vector<int32_t> out;
+  std::vector<char> taken(slots_.size(), 0);
+  if (k > 0 && eager_slot_ >= 0 && !slots_[eager_slot_].active) {
+    out.push_back((int32_t)eager_slot_);
+    taken[eager_slot_] = 1;
+  }
+  while ((int32_t)out.size() < k) {
+    int32_t rid = -1;
+    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+      if (slots_[r].active || taken[r]) continue;
+      if (rid < 0 || ranked(slots_[r], plan_credit_[r]) > ranked(slots_[rid], plan_credit_[rid])) rid = r;
+    }
+    if (rid < 0) break;
+    out.push_back(rid);
+    taken[rid] = 1;
+  }
+  return out;
+}
+
+void Manager::prefetch_hint(const int32_t* slots, const int64_t* tokens, int32_t n) {
+  std::lock_guard<std::mutex> lk(pf_mu_);
+  pf_hints_.clear();
+  for (int32_t i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= (int32_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "hint slot out of range");
+    if (tokens[i] < 0 || tokens[i] > max_context_) throw Fail(VATTN_VALUE_ERROR, "hint tokens out of range");
+    pf_hints_.emplace_back(slots[i], tokens[i]);
+  }
+}
+
+bool Manager::slot_ready(int32_t slot, int64_t tokens) const {
+  if (slot < 0 || slot >= (int32_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "slot out of range");
+  const int64_t need = std::min(groups_required(tokens), groups_per_slot_);
+  std::lock_guard<std::mutex> lk(pf_mu_);
+  for (int64_t g = 0; g < need; ++g) {
+    const int64_t off = slot_offset(slot, g);
+    for (int64_t b = 0; b < buffer_count_; ++b)
+      if (!buf_maps_[b].count(off) && !(real() && spec_.count(b * buffer_size_ + off))) return false;
+  }
+  return true;
+}
+
 void Manager::prefetch() {
-  if (!real() || (prefetch_tokens_ <= 0 && prefetch_slots_ <= 0)) return;
+  if (!real()) return;
   // Runs inside a bg window (state owned): choose the pages, hand them to the worker, return.
   // (urgency, key): pages are mapped soonest-needed first — decode growth by the tokens left
   // before the row reaches the page, then the speculative-eager slots in alloc_reqid order
@@ -759,6 +819,17 @@ void Manager::prefetch() {
     const int64_t target = std::min(groups_required(prefetch_slot_tokens_), groups_per_slot_);
     for (size_t i = 0; i < cand.size() && (int64_t)i < prefetch_slots_; ++i)
       spec_range(cand[i], slots_[cand[i]].mapped_groups, target, (int64_t)(1 + i) << 40, -1);
+  }
+  // 3. prompts queued for admission, at the slots they are predicted to get (after growth)
+  std::vector<std::pair<int32_t, int64_t>> hints;
+  {
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    hints = pf_hints_;
+  }
+  for (size_t i = 0; i < hints.size(); ++i) {
+    const auto& hs = hints[i];
+    if (slots_[hs.first].active) continue;
+    spec_range(hs.first, 0, std::min(groups_required(hs.second), groups_per_slot_), ((int64_t)1 << 38) + ((int64_t)i << 20), -1);
   }
   std::stable_sort(targets.begin(), targets.end(),
                    [](const auto& a, const auto& b) { return a.first < b.first; });
@@ -879,7 +950,6 @@ int32_t Manager::best_inactive() const {  // max over inactive of (mapped_groups
 // alloc_reqid's choice as the reference makes it: admission precedes execute_plan
 // (simulator.py:395-418), so a plan executed early (during the previous iteration's compute)
 // must not influence which inactive slot is reused.  Credits undo its effect on the ranking.
-static inline int64_t ranked(const Slot& s, int64_t credit) { return s.mapped_groups - credit; }
 
 int32_t Manager::alloc_reqid() {  // manager.py:163-178
   int32_t rid;
@@ -1270,6 +1340,7 @@ void Manager::counters(vattn_counters* o) const {
   o->spec_hits = spec_hits_;
   o->spec_steals = spec_steals_;
   o->spec_pages = (int64_t)spec_.size();
+  o->lazy_unmaps = lazy_unmaps_;
 }
 
 void Manager::slot_state(int64_t* out) const {
@@ -1609,6 +1680,30 @@ vattn_status vattn_events(vattn_t* h, int64_t* trip, int64_t cap, int64_t* n) {
   return api_call(h, [&](Manager& m) {
     const int64_t k = m.drain_events(trip, cap);
     if (n) *n = k;
+  });
+}
+
+vattn_status vattn_predict_alloc(vattn_t* h, int32_t k, int32_t* out, int32_t* n) {
+  return api_call(h, [&](Manager& m) {
+    if (!out || !n) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    const auto v = m.predict_alloc(k);
+    std::copy(v.begin(), v.end(), out);
+    *n = (int32_t)v.size();
+  });
+}
+
+vattn_status vattn_prefetch_hint(vattn_t* h, const int32_t* slots, const int64_t* tokens, int32_t n) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    if (n > 0 && (!slots || !tokens)) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    h->m->prefetch_hint(slots, tokens, n);
+  });
+}
+
+vattn_status vattn_slot_ready(vattn_t* h, int32_t slot, int64_t tokens, int32_t* ready) {
+  return api_call(h, [&](Manager& m) {
+    if (!ready) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    *ready = m.slot_ready(slot, tokens) ? 1 : 0;
   });
 }
 

@@ -195,7 +195,7 @@ class KVCacheManager:
     def __init__(self, geometry, config, *, backend: str | None = None, device: int | None = None,
                  log_events: bool | None = None, release_physical: bool = False,
                  batch_set_access: bool = True, prefetch_tokens: int = 0, prefetch_slots: int = 0,
-                 prefetch_slot_tokens: int = 0):
+                 prefetch_slot_tokens: int = 0, lazy_unmap: bool = False):
         g = as_geometry(geometry)
         if g.max_batch < 1:
             raise ValueError("geometry.max_batch must be >= 1 to serve requests")
@@ -229,6 +229,7 @@ class KVCacheManager:
         cfg.prefetch_tokens = int(prefetch_tokens)
         cfg.prefetch_slots = int(prefetch_slots)
         cfg.prefetch_slot_tokens = int(prefetch_slot_tokens)
+        cfg.lazy_unmap = int(bool(lazy_unmap))
         lat, n_lat = _latency_entries(getattr(config, "latency_model", None))
         if lat is not None:
             cfg.latency, cfg.n_latency = C.cast(lat[0], C.POINTER(_abi.LatencyEntry)), n_lat
@@ -439,7 +440,30 @@ class KVCacheManager:
     def driver_stats(self, peek: bool = False) -> dict:
         """Measured real-driver cost (CUDA backend)."""
         c = self.peek_counters() if peek else self._counters()
-        return {k: getattr(c, k) for k, _ in _abi.Counters._fields_ if k.startswith(("real_", "init_wall", "spec_"))}
+        return {k: getattr(c, k) for k, _ in _abi.Counters._fields_
+                if k.startswith(("real_", "init_wall", "spec_", "lazy_"))}
+
+    # -- admission-aware prefetch (B200 addition; logical state untouched) ------------------------
+    def predict_alloc(self, k: int) -> list[int]:
+        """The next k slots consecutive alloc_reqid() calls would return now."""
+        out = (C.c_int32 * max(1, k))()
+        n = C.c_int32()
+        check(lib().vattn_predict_alloc(self._h, int(k), out, C.byref(n)))
+        return list(out[:n.value])
+
+    def prefetch_hint(self, slots, tokens) -> None:
+        """Back rows [0, tokens[i]) of slots[i] physically ahead of admission (queued prompts);
+        replaces the previous hints; picked up by the next bg_submit(prefetch=True)."""
+        n = len(slots)
+        sa = (C.c_int32 * max(1, n))(*[int(x) for x in slots])
+        ta = (C.c_int64 * max(1, n))(*[int(x) for x in tokens])
+        check(lib().vattn_prefetch_hint(self._h, sa, ta, n))
+
+    def slot_ready(self, slot: int, tokens: int) -> bool:
+        """True when a step growing `slot` to `tokens` rows needs no driver call."""
+        r = C.c_int32()
+        check(lib().vattn_slot_ready(self._h, int(slot), int(tokens), C.byref(r)))
+        return bool(r.value)
 
     # -- virtual tensors (Table 3 `init` returns the KV cache tensors, PAPER.md:434-437) ---------
     def _view(self, layer: int, kind: int):

@@ -242,8 +242,16 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         backend: str | None = None, defer: bool | None = None, observer=None,
         max_iterations: int | None = None, model: SyntheticModel | None = None,
         manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
-        prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0) -> ServingMetrics:
-    """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31)."""
+        prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0,
+        lazy_unmap: bool = False, stage_admission: bool = False, stage_max_iters: int = 8) -> ServingMetrics:
+    """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31).
+
+    B200 additions (wall clock, CUDA backend; the allocator's logical state stays the
+    reference's for the calls made): `lazy_unmap` keeps trimmed/reclaimed pages mapped until
+    their handle is needed; `stage_admission` holds an arrived request at the head of the queue
+    (FIFO kept) until the slot alloc_reqid will give it has its prompt pages mapped by the
+    prefetch worker, for at most `stage_max_iters` iterations and never while the batch is
+    empty, so prompt mapping overlaps the running batch's compute instead of stalling it."""
     if mode not in ("sync", "overlapped"):
         raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
     if clock not in ("model", "wall"):
@@ -261,7 +269,9 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
                                 reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
                                 sliced=sliced, pre_create_fraction=pre_create_fraction),
         backend=backend or ("cuda" if wall else "shadow"), prefetch_tokens=prefetch_tokens,
-        prefetch_slots=prefetch_slots, prefetch_slot_tokens=prefetch_slot_tokens)
+        prefetch_slots=prefetch_slots, prefetch_slot_tokens=prefetch_slot_tokens, lazy_unmap=lazy_unmap)
+    stage = bool(stage_admission) and wall and mode == "overlapped"
+    staged_iters: dict[int, int] = {}     # record index -> iterations held at the queue head
     if wall and model is None:
         model = SyntheticModel(mgr, geometry, max(p for _, p, _ in records) if records else 1,
                                dense_model=dense_proxy)
@@ -297,6 +307,14 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         # -- admit (Algorithm 1 lines 6-11) --
         t_exp = time.perf_counter()
         while pending and pending[0][1][0] * 1000 <= clock_us:
+            if stage and running:
+                head_index, head_rec = pending[0]
+                pred = mgr.predict_alloc(1)
+                if pred and not mgr.slot_ready(pred[0], head_rec[1]):
+                    waited = staged_iters.get(head_index, 0)
+                    if waited < stage_max_iters:
+                        staged_iters[head_index] = waited + 1
+                        break
             try:
                 rid = mgr.alloc_reqid()
             except BatchFullError:
@@ -370,8 +388,15 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             for rid in running:
                 next_seq[rid] = min(seq_lens[rid] + 1, geometry.max_context)
             plan = mgr.plan_overlap(next_seq)
+            if stage:
+                # prompts that have arrived -> the slots alloc_reqid would give them now; the
+                # prefetch worker backs them during these kernels (state is owned here: no join)
+                now_ms = (time.perf_counter() - t_start) * 1e3
+                arrived = [rec for _, rec in list(pending)[:geometry.max_batch] if rec[0] <= now_ms]
+                slots = mgr.predict_alloc(len(arrived)) if arrived else []
+                mgr.prefetch_hint(slots, [rec[1] for rec in arrived[:len(slots)]])
             # maps run on the bg thread during the kernels (+ physical prefetch further ahead)
-            mgr.bg_submit(plan, credit=True, prefetch=prefetch_tokens > 0 or prefetch_slots > 0)
+            mgr.bg_submit(plan, credit=True, prefetch=prefetch_tokens > 0 or prefetch_slots > 0 or stage)
         if wall and batch:
             torch.cuda.synchronize()
             kernel_ms = (time.perf_counter() - t_k) * 1e3

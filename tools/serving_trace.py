@@ -24,6 +24,8 @@ ap.add_argument("--prefetch", type=int, default=0, help="physical prefetch looka
 ap.add_argument("--spec-slots", type=int, default=0, help="speculative eager: slots to pre-map physically")
 ap.add_argument("--spec-tokens", type=int, default=0, help="speculative eager: prompt tokens per slot")
 ap.add_argument("--out", default=None)
+ap.add_argument("--lazy-unmap", action="store_true", help="keep trimmed/reclaimed pages mapped until needed")
+ap.add_argument("--stage", type=int, default=0, help="staged admission: max iterations a prompt waits for its pages")
 ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel dense-layer time on the GPU")
 a = ap.parse_args()
 rows = load_trace_csv(Path("tests/golden/trace_config5.csv"))[: a.requests]
@@ -37,15 +39,24 @@ else:
             eager_groups=eager if a.mode == "overlapped" else 0, reclaim_threshold=0.10,
             preemption_cap=100_000, defer=not a.no_defer,
             dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch,
-            prefetch_slots=a.spec_slots, prefetch_slot_tokens=a.spec_tokens)
+            prefetch_slots=a.spec_slots, prefetch_slot_tokens=a.spec_tokens, lazy_unmap=a.lazy_unmap,
+            stage_admission=a.stage > 0, stage_max_iters=a.stage)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
-          "dense_proxy": a.dense_proxy, "prefetch": a.prefetch})
+          "dense_proxy": a.dense_proxy, "prefetch": a.prefetch, "lazy_unmap": a.lazy_unmap, "stage": a.stage})
+if a.mode != "paged":
+    its = m.iterations
+    s["exposed_map_ms_median"] = sorted(r.exposed_ms for r in its)[len(its) // 2] if its else 0.0
+    s["exposed_breakdown_ms"] = {k: sum(getattr(r, k) for r in its) for k in
+                                 ("t_admit_ms", "t_bgwait_ms", "t_step_ms", "t_retire_ms")}
+    s["driver_set_access_ms_total"] = sum(r.drv_set_access_ms for r in its)
+    s["driver_maps_total"] = sum(r.drv_maps for r in its)
 print(json.dumps(s))
 if a.out:
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     tag = (a.mode + ("_dense" if a.dense_proxy else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
-           + (f"_ss{a.spec_slots}x{a.spec_tokens}" if a.spec_slots else ""))
+           + (f"_ss{a.spec_slots}x{a.spec_tokens}" if a.spec_slots else "") + ("_lazy" if a.lazy_unmap else "")
+           + (f"_stage{a.stage}" if a.stage else ""))
     m.write_iterations_csv(a.out + f"_{tag}.csv")
     with open(a.out + f"_{tag}.json", "w") as fh:
         json.dump(s, fh, indent=1)
