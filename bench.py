@@ -732,6 +732,11 @@ def extra_serving(local, requests=48):
         # 256 tokens ahead + speculative eager pre-mapping of the 4 likely-next slots
         "overlapped_prefetch": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
                                     prefetch_slot_tokens=3072),
+        # + lazy unmap of trimmed/reclaimed pages + staged admission (a prompt waits at the
+        # queue head, up to 32 iterations, until the prefetch worker backed its predicted slot)
+        "overlapped_staged": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
+                                  prefetch_slot_tokens=3072, lazy_unmap=True, stage_admission=True,
+                                  stage_max_iters=32),
     }
     for mode, kw in variants.items():
         m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,

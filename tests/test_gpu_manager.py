@@ -127,8 +127,8 @@ def test_decode_through_manager_l8_shape_with_growth():
     mgr.close()
 
 
-@pytest.mark.parametrize("spec_slots", [0, 2])
-def test_physical_prefetch_keeps_logical_state_and_data(spec_slots):
+@pytest.mark.parametrize("spec_slots,lazy", [(0, False), (2, False), (0, True), (2, True)])
+def test_physical_prefetch_keeps_logical_state_and_data(spec_slots, lazy):
     """Prefetch (and speculative eager) maps pages ahead of the reference schedule; the logical
     state must equal the oracle's after every call and kernels must read/write the adopted pages
     correctly."""
@@ -143,7 +143,7 @@ def test_physical_prefetch_keeps_logical_state_and_data(spec_slots):
     g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
     pool = 24 * 4 * MB2
     mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool), prefetch_tokens=1500,
-                         prefetch_slots=spec_slots, prefetch_slot_tokens=1800)
+                         prefetch_slots=spec_slots, prefetch_slot_tokens=1800, lazy_unmap=lazy)
     om = OracleManager(Geometry(2, 8, 128, 2, 4096, 4), MB2, pool_bytes=pool)
     rng = random.Random(0)
     gen = torch.Generator().manual_seed(9)
@@ -195,6 +195,57 @@ def test_physical_prefetch_keeps_logical_state_and_data(spec_slots):
             lens[r] = 0
     ds = mgr.driver_stats()
     assert ds["spec_maps"] > 0 and ds["spec_hits"] > 0
+    if lazy:
+        assert ds["lazy_unmaps"] > 0 and ds["real_unmaps"] < ds["lazy_unmaps"]
+    mgr.close()
+
+
+def test_prefetch_hint_backs_the_predicted_slot_before_admission():
+    """Staged admission: hint a queued prompt at the slot alloc_reqid will return; once the
+    prefetch worker reports it ready, admitting it and stepping to the prompt length maps every
+    page-group without a single driver call (all adopted), and the data path works."""
+    _cuda()
+    import time
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention, kv_append
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(4, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=96 * MB2, eager_groups=0),
+                         lazy_unmap=True)
+    r0 = mgr.alloc_reqid()
+    assert mgr.step([1500 if i == r0 else 0 for i in range(4)]).ok
+    pred = mgr.predict_alloc(2)
+    assert len(pred) == 2 and r0 not in pred
+    mgr.prefetch_hint(pred[:1], [3000])
+    assert not mgr.slot_ready(pred[0], 3000)
+    mgr.bg_submit(execute_plan=False, prefetch=True)
+    t0 = time.time()
+    while not mgr.slot_ready(pred[0], 3000):
+        assert time.time() - t0 < 60, "prefetch worker did not back the hinted slot"
+        time.sleep(0.01)
+    before = mgr.driver_stats()
+    r1 = mgr.alloc_reqid()
+    assert r1 == pred[0]
+    lens = [0] * 4
+    lens[r0], lens[r1] = 1500, 3000
+    assert mgr.step(lens).ok
+    after = mgr.driver_stats()
+    assert after["real_maps"] == before["real_maps"]          # every page adopted
+    assert after["spec_hits"] - before["spec_hits"] == 3 * 8   # 3 groups x 8 buffers
+    gen = torch.Generator().manual_seed(4)
+    kn = torch.randn(1, 3000, 8, 128, generator=gen).to(torch.bfloat16)
+    kv_append(mgr, 3, kn.to(dev), kn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+              torch.tensor([r1], dtype=torch.int32, device=dev))
+    q = torch.randn(1, 32, 128, generator=gen).to(torch.bfloat16)
+    out = decode_attention(mgr, 3, q.to(dev), torch.tensor([3000], dtype=torch.int32, device=dev),
+                           torch.tensor([r1], dtype=torch.int32, device=dev))
+    host = torch.zeros(4, 4096, 8, 128, dtype=torch.bfloat16)
+    host[r1, :3000] = kn[0]
+    ref = decode_ref(q, host, host, torch.tensor([3000], dtype=torch.int32), torch.tensor([r1], dtype=torch.int32))
+    torch.cuda.synchronize()
+    assert max_rel_err(out.cpu(), ref) <= 2e-2
     mgr.close()
 
 
