@@ -233,20 +233,13 @@ def bench_decode(args, world, rank, local):
         from paper_2405_04437_b200.parallel import HeadGather
         hg = HeadGather.create(B, hq * world, d, device=local)
 
-    def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out, pre_layer=None, post_layer=None):
-        nxt = list(state["seq"])
-        for r in rids:
-            nxt[r] += 1
-        t_h = time.perf_counter()
-        r = mgr.step(nxt)                       # joins the bg window, maps any shortfall
-        exposed = time.perf_counter() - t_h
-        assert r.ok
+    def launch_layers(dec_events, q_, kn_, vn_, out_, st, pre_layer=None, post_layer=None):
         p = state["pos"]
         for layer in range(N):
             if pre_layer is not None:
                 pre_layer(layer)
             if dec_events is not None:
-                dec_events[layer][0].record(stream)
+                dec_events[layer][0].record(st)
             if hg is not None:      # fused decode + head all-gather over peer memory
                 decode_attention_gather(mgr, layer, q_[layer], hg, p, idx, k_new=kn_[layer], v_new=vn_[layer],
                                         num_splits=splits)
@@ -261,10 +254,23 @@ def bench_decode(args, world, rank, local):
                 decode_attention_append(mgr, layer, q_[layer], kn_[layer], vn_[layer], p, idx,
                                         out=out_[layer], num_splits=splits)
             if dec_events is not None:
-                dec_events[layer][1].record(stream)
+                dec_events[layer][1].record(st)
             if post_layer is not None:
                 post_layer(layer)
-        p.add_(1)
+
+    def one_step(dec_events=None, q_=q, kn_=kn, vn_=vn, out_=out, pre_layer=None, post_layer=None, graph=None):
+        nxt = list(state["seq"])
+        for r in rids:
+            nxt[r] += 1
+        t_h = time.perf_counter()
+        r = mgr.step(nxt)                       # joins the bg window, maps any shortfall
+        exposed = time.perf_counter() - t_h
+        assert r.ok
+        if graph is not None:
+            graph.replay()                      # layers + position update, one host call
+        else:
+            launch_layers(dec_events, q_, kn_, vn_, out_, stream, pre_layer, post_layer)
+            state["pos"].add_(1)
         state["seq"] = nxt
         nn = list(nxt)
         for rr in rids:
@@ -276,17 +282,36 @@ def bench_decode(args, world, rank, local):
     for _ in range(warm):
         one_step()
     torch.cuda.synchronize()
+    use_graph = not args.eager and args.gather != "nccl"   # NCCL stays eager
+    if use_graph:
+        # One CUDA graph per timed step (the 32 fused append+decode launches, the per-layer
+        # timing events as external record nodes, and the row-position update), so the timed
+        # step costs one replay on the host.  Captured, not executed: state is unchanged.
+        mgr.bg_wait()
+        ev = [[(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+               for _ in range(N)] for _ in range(steps)]
+        cap = torch.cuda.Stream(device=dev)
+        graphs = []
+        for i in range(steps):
+            gr = torch.cuda.CUDAGraph()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
+                launch_layers(ev[i], q, kn, vn, out, torch.cuda.current_stream())
+                state["pos"].add_(1)
+            graphs.append(gr)
+        torch.cuda.synchronize()
+    else:
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(N)] for _ in range(steps)]
     barrier()
     torch.cuda.synchronize()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(N)] for _ in range(steps)]
     clocks = ClockSampler(local)
     clocks.start()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     exposed = []
     s0.record(stream)
     for i in range(steps):
-        exposed.append(one_step(ev[i]))
+        exposed.append(one_step(ev[i], graph=graphs[i] if use_graph else None))
     s1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -866,6 +891,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip prefill / paged / serving sub-benches")
     ap.add_argument("--unfused", action="store_true", help="separate kv_append + decode launches per layer")
+    ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (no CUDA graph)")
     ap.add_argument("--gather", choices=["none", "fused", "nccl"], default="none",
                     help="N>1: all-gather the output heads every layer (fused peer-memory kernel or NCCL)")
     args = ap.parse_args(argv)

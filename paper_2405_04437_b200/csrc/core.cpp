@@ -929,7 +929,14 @@ void Manager::real_unmap(int32_t b, int64_t off) {
 
 void Manager::mark_use(cudaStream_t st) {
   if (!real()) return;
-  check_rt(cudaEventRecord(use_event_, st), "cudaEventRecord(use)");
+  // Inside a CUDA-graph capture a plain record only expresses a cross-stream dependency; an
+  // external record becomes a graph node, so every replay re-arms the unmap fence.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  check_rt(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+  if (cs == cudaStreamCaptureStatusActive)
+    check_rt(cudaEventRecordWithFlags(use_event_, st, cudaEventRecordExternal), "cudaEventRecord(use, graph)");
+  else
+    check_rt(cudaEventRecord(use_event_, st), "cudaEventRecord(use)");
   use_recorded_ = true;
 }
 
@@ -1786,7 +1793,6 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
     const vattn::GatherSink s = vattn::gather_sink(g, hq, batch, v.d);
     vattn::launch_decode(h->m->ks, layer, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new, &s);
-    vattn::gather_commit(g, s, batch);
     h->m->mark_use((cudaStream_t)stream);
   });
 }

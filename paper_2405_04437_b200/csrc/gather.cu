@@ -35,13 +35,12 @@ struct vattn_gather {
   void* base = nullptr;        // own buffer (owned)
   void* peer[vattn::kMaxGatherRanks] = {};
   bool opened[vattn::kMaxGatherRanks] = {};   // peer[r] came from cudaIpcOpenMemHandle
-  uint32_t epoch = 0;          // launches issued (every rank issues the same sequence)
 };
 
 namespace vattn {
 namespace {
 
-constexpr int64_t kSigBytes = 512;   // flags[8] @0, counter @256, error @384
+constexpr int64_t kSigBytes = 512;   // flags[8] @0, counter @256, epoch @320, error @384
 constexpr uint64_t kWaitTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
 uint32_t* flags_of(void* buf, int64_t sig_off) {
@@ -50,16 +49,21 @@ uint32_t* flags_of(void* buf, int64_t sig_off) {
 uint32_t* counter_of(void* buf, int64_t sig_off) {
   return reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + sig_off + 256);
 }
+uint32_t* epoch_of(void* buf, int64_t sig_off) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + sig_off + 320);
+}
 uint32_t* error_of(void* buf, int64_t sig_off) {
   return reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + sig_off + 384);
 }
 
-// One thread per source rank: wait until rank r's flag in our signal area reached `epoch`.
-// Bounded: after kWaitTimeoutNs it records a timeout instead of hanging the device.
-__global__ void gather_wait_kernel(const uint32_t* flags, int world, uint32_t epoch, uint32_t* err,
+// One thread per source rank: wait until rank r's flag in our signal area reached our own
+// launch count (advanced by our last gathered launch, earlier on this stream).  Bounded: after
+// timeout_ns it records a timeout instead of hanging the device.
+__global__ void gather_wait_kernel(const uint32_t* flags, int world, const uint32_t* epoch_ptr, uint32_t* err,
                                    uint64_t timeout_ns) {
   const int r = threadIdx.x;
   if (r >= world) return;
+  const uint32_t epoch = *epoch_ptr;
   uint64_t t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while (true) {
@@ -106,16 +110,12 @@ GatherSink gather_sink(vattn_gather* g, int hq_local, int batch, int head_dim) {
     s.flags[r] = flags_of(g->peer[r], g->sig_off);
   }
   s.counter = counter_of(g->base, g->sig_off);
+  s.epoch = epoch_of(g->base, g->sig_off);
   s.n_ranks = g->world;
   s.rank = g->rank;
   s.hq_total = hq_local * g->world;
   s.head_off = g->rank * hq_local;
-  s.epoch = g->epoch + 1;   // committed by gather_commit once the launch went out
   return s;
-}
-
-void gather_commit(vattn_gather* g, const GatherSink& s, int batch) {
-  if (batch > 0) g->epoch = s.epoch;   // batch 0 launches nothing, so nothing will signal
 }
 
 }  // namespace vattn
@@ -211,11 +211,11 @@ vattn_status vattn_gather_output(vattn_gather_t* g, uint64_t* dptr) {
 vattn_status vattn_gather_wait(vattn_gather_t* g, void* stream) {
   return gguard([&] {
     if (!g) throw Fail(VATTN_VALUE_ERROR, "null gather handle");
-    if (g->epoch == 0) return;
     uint64_t timeout = vattn::kWaitTimeoutNs;
     if (const char* e = getenv("VATTN_GATHER_TIMEOUT_MS")) timeout = (uint64_t)std::max(1L, atol(e)) * 1000000ull;
     vattn::gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
-        vattn::flags_of(g->base, g->sig_off), g->world, g->epoch, vattn::error_of(g->base, g->sig_off), timeout);
+        vattn::flags_of(g->base, g->sig_off), g->world, vattn::epoch_of(g->base, g->sig_off),
+        vattn::error_of(g->base, g->sig_off), timeout);
     vattn::check_rt(cudaGetLastError(), "gather wait launch");
   });
 }
@@ -249,7 +249,6 @@ vattn_status vattn_decode_gather_raw(const vattn_cache_desc* c, const void* q, c
     const vattn::GatherSink s = vattn::gather_sink(g, hq, batch, v.d);
     vattn::launch_decode(nullptr, -1, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale, num_splits, ws,
                          ws_bytes, (cudaStream_t)stream, k_new, v_new, &s);
-    vattn::gather_commit(g, s, batch);
   });
 }
 

@@ -79,14 +79,14 @@ struct GatherSink {
   void* dst[kMaxGatherRanks];          // rank r's full output (peer-mapped; own included)
   uint32_t* flags[kMaxGatherRanks];    // rank r's signal words, indexed by the writing rank
   uint32_t* counter;                   // this rank's CTA-completion counter (reset by the last CTA)
+  uint32_t* epoch;                     // this rank's launch count, advanced on the device by the
+                                       // last CTA (graph-replay safe: no host-side epoch)
   int32_t n_ranks, rank, hq_total, head_off;
-  uint32_t epoch;
 };
 
-// gather.cu: sink for the next launch through `g` (epoch = last + 1) and its commit after the
-// launch succeeded (every rank must issue the same sequence of gathered launches).
+// gather.cu: sink for a launch through `g` (every rank must issue the same sequence of
+// gathered launches; the epoch lives on the device).
 GatherSink gather_sink(vattn_gather_t* g, int hq_local, int batch, int head_dim);
-void gather_commit(vattn_gather_t* g, const GatherSink& s, int batch);
 
 // Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
 void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,

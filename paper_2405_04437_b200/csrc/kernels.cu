@@ -138,8 +138,10 @@ __device__ __forceinline__ void sink_signal(const GatherSink& s, uint32_t total_
     const uint32_t prev = atomicAdd(s.counter, 1u);
     if (prev == total_ctas - 1) {
       __threadfence_system();
+      const uint32_t e = *s.epoch + 1;   // launches are stream-ordered: nobody else writes it now
+      *s.epoch = e;
       for (int r = 0; r < s.n_ranks; ++r)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(s.flags[r] + s.rank), "r"(s.epoch) : "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(s.flags[r] + s.rank), "r"(e) : "memory");
       atomicExch(s.counter, 0u);
     }
   }

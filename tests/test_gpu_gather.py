@@ -212,3 +212,68 @@ def test_two_processes_gather_through_cuda_ipc():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, "ok"), (1, "ok")], res
+
+
+def test_gather_and_manager_decode_replay_from_a_cuda_graph():
+    """The gather epoch lives on the device and mark_use records an external event node, so a
+    captured step (manager-backed fused decode + fused gather of 2 simulated ranks) replays
+    correctly many times."""
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention_append, decode_attention_gather_raw
+    from paper_2405_04437_b200.geometry import ModelGeometry
+    from paper_2405_04437_b200.parallel import HeadGather
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(5)
+    # manager-backed fused decode, captured
+    g = ModelGeometry(2, 8, 128, 2, max_context=2048, max_batch=2, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=2 << 20, pool_bytes=64 << 20), backend="cuda",
+                         device=dev.index or 0)
+    rids = [mgr.alloc_reqid(), mgr.alloc_reqid()]
+    assert mgr.step([1100, 1100]).ok
+    q = _rand((2, 32, 128), gen).to(dev)
+    kn = _rand((2, 8, 128), gen).to(dev)
+    idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+    pos = torch.tensor([1000, 1000], dtype=torch.int32, device=dev)
+    out = torch.empty_like(q)
+    # 2 simulated gather ranks over caller-owned caches
+    k = _rand((3, 256, 4, 64), gen).to(dev)
+    qg = _rand((3, 8, 64), gen).to(dev)
+    seq = torch.tensor([200, 17, 256], dtype=torch.int32, device=dev)
+    gs = HeadGather.local_group(2, 3, 8, 64, device=dev.index or 0)
+    shards = [(k[:, :, 2 * r:2 * r + 2].contiguous(), qg[:, 4 * r:4 * r + 4].contiguous()) for r in range(2)]
+
+    def body():
+        decode_attention_append(mgr, 1, q, kn, kn, pos, idx, out=out)
+        pos.add_(1)
+        for r in range(2):
+            decode_attention_gather_raw(shards[r][1], shards[r][0], shards[r][0], gs[r], seq, wait=False)
+        for r in range(2):
+            gs[r].wait()
+
+    body()                       # warm-up (workspace, tensor maps)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s, capture_error_mode="thread_local"):
+        body()
+    for _ in range(5):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert pos.tolist() == [1006, 1006]
+    got_dec = out.clone()
+    assert all(x.timed_out_ranks() == [] for x in gs)
+    # eager reference of the last replay: rows 1005 appended, attention over 1006 rows
+    ref = decode_attention_append(mgr, 1, q, kn, kn, pos - 1, idx)
+    torch.cuda.synchronize()
+    assert torch.equal(got_dec, ref)
+    from paper_2405_04437_b200.attention import decode_attention_raw
+    full = gs[1].output(3).clone()
+    for r in range(2):
+        loc = decode_attention_raw(shards[r][1], shards[r][0], shards[r][0], seq)
+        torch.cuda.synchronize()
+        assert torch.equal(full[:, 4 * r:4 * r + 4], loc.cpu().to(full.device))
+    for x in gs:
+        x.close()
+    mgr.close()
