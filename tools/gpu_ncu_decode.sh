@@ -2,7 +2,7 @@
 # one ncu --set full capture of the fused decode kernel inside the default bench (1 GPU)
 mkdir -p gpurun_out
 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 100 -c 1 \
-    -o gpurun_out/prof_decode_fused python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_decode.log 2>&1
+    -o gpurun_out/prof_decode_fused python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --eager > gpurun_out/ncu_decode.log 2>&1
 tail -1 gpurun_out/ncu_decode.log
 ncu --set full --clock-control none --import-source on -k regex:kv_append -s 0 -c 1 \
     -o gpurun_out/prof_append python -c "
