@@ -931,6 +931,20 @@ def main(argv=None):
                 except Exception as e:   # an extra must not void the headline line
                     extras[name] = {"error": repr(e)[:300]}
             line["extras"] = extras
+            # the BASELINE metric "exposed map ms/iter" in one place: steady decode (headline run),
+            # decode growth across page-groups, and the config-5 serving trace
+            g, sv = extras.get("decode_growth", {}), extras.get("serving", {})
+            line["exposed_map_ms_per_iter_summary"] = {
+                "steady_decode": line.get("exposed_map_ms_per_iter"),
+                "decode_growth_sync": g.get("sync", {}).get("exposed_map_ms_per_iter"),
+                "decode_growth_reference_overlap": g.get("overlapped", {}).get("exposed_map_ms_per_iter"),
+                "decode_growth_prefetch_worker": g.get("overlapped_prefetch64", {}).get("exposed_map_ms_per_iter"),
+                "serving_sync": sv.get("sync", {}).get("exposed_map_ms_per_iter"),
+                "serving_reference_overlap": sv.get("overlapped", {}).get("exposed_map_ms_per_iter"),
+                "serving_staged": sv.get("overlapped_staged", {}).get("exposed_map_ms_per_iter"),
+                "serving_staged_p99": sv.get("overlapped_staged", {}).get("exposed_map_ms_p99"),
+                "serving_paged_layout_host": sv.get("paged_bs16", {}).get("exposed_map_ms_per_iter"),
+            }
         print(json.dumps(line), flush=True)
     return 0
 
