@@ -35,13 +35,19 @@ constexpr int kD = 128;            // head dim (Yi-6B / Llama / Yi-34B)
 constexpr int kStages = 2;         // K/V ring depth
 constexpr int kThreads = 320;
 constexpr int kHalf = kBN * 128;               // one 64-column half of a 128-row tile (16 KB)
-constexpr int kTileBytes = 2 * kHalf;          // 128 rows x 128 bf16 (32 KB)
-constexpr int kQOff = 0;                       // Q_A, Q_B
-constexpr int kKOff = 2 * kTileBytes;          // K stages
-constexpr int kVOff = kKOff + kStages * kTileBytes;
-constexpr int kBarOff = kVOff + kStages * kTileBytes;
-constexpr int kSmemBytes = kBarOff + 256 + 1024;
 constexpr float kRescaleThreshold = 8.0f;      // log2 domain: rescale O when max grows > 2^8
+
+// Shared-memory layout for head dim D (64 or 128): every 128-row tile is D/64 swizzled 64-column
+// halves of 16 KB.
+template <int D>
+struct PfL {
+  static constexpr int kTile = (D / 64) * kHalf;
+  static constexpr int kQOff = 0;                               // Q_A, Q_B
+  static constexpr int kKOff = 2 * kTile;                       // K stages
+  static constexpr int kVOff = kKOff + kStages * kTile;
+  static constexpr int kBarOff = kVOff + kStages * kTile;
+  static constexpr int kSmem = kBarOff + 256 + 1024;
+};
 
 struct Params {
   __nv_bfloat16* out;      // [n_q, hq, D]
@@ -232,13 +238,14 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
-template <int POLY, bool PAGED = false>
+template <int POLY, bool PAGED = false, int D = 128>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, Params p) {
+  using L = PfL<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;            // [kStages]
   uint64_t* v_full = bars + 3;            // [kStages]
@@ -286,25 +293,25 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       ptx::prefetch_tmap(&qmap);
       ptx::prefetch_tmap(&kmap);
       ptx::prefetch_tmap(&vmap);
-      ptx::mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
+      ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        ptx::tma_load_3d(smem + kQOff + h * kHalf, &qmap, q_full, h * 64, head, q0A);
-        ptx::tma_load_3d(smem + kQOff + kTileBytes + h * kHalf, &qmap, q_full, h * 64, head, q0B);
+      for (int h = 0; h < D / 64; ++h) {
+        ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q0A);
+        ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q0B);
       }
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % kStages;
         if (j >= kStages) ptx::mbar_wait(&kv_empty[s], ((j / kStages) - 1) & 1);
-        ptx::mbar_arrive_expect_tx(&k_full[s], kTileBytes);
+        ptx::mbar_arrive_expect_tx(&k_full[s], L::kTile);
         if constexpr (!PAGED) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            ptx::tma_load_3d(smem + kKOff + s * kTileBytes + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
+          for (int h = 0; h < D / 64; ++h)
+            ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
                              j * kBN);
-          ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+          ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            ptx::tma_load_3d(smem + kVOff + s * kTileBytes + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
+          for (int h = 0; h < D / 64; ++h)
+            ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
                              j * kBN);
         } else {
           // PagedAttention layout: one TMA box per KV block (4-D map over [D, Hkv, block, n_blocks])
@@ -314,18 +321,18 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int blk = __ldg(p.block_table + min(tok / p.block_size, last_blk));
             const int within = tok % p.block_size;
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-              ptx::tma_load_4d(smem + kKOff + s * kTileBytes + h * kHalf + sub * p.box_tokens * 128, &kmap,
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_4d(smem + L::kKOff + s * L::kTile + h * kHalf + sub * p.box_tokens * 128, &kmap,
                                &k_full[s], h * 64, kvh, within, blk);
           }
-          ptx::mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+          ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
           for (int sub = 0; sub < kBN / p.box_tokens; ++sub) {
             const int tok = j * kBN + sub * p.box_tokens;
             const int blk = __ldg(p.block_table + min(tok / p.block_size, last_blk));
             const int within = tok % p.block_size;
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-              ptx::tma_load_4d(smem + kVOff + s * kTileBytes + h * kHalf + sub * p.box_tokens * 128, &vmap,
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_4d(smem + L::kVOff + s * L::kTile + h * kHalf + sub * p.box_tokens * 128, &vmap,
                                &v_full[s], h * 64, kvh, within, blk);
           }
         }
@@ -334,17 +341,17 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   } else if (warp == 9) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0 && n_kv > 0) {
-      const uint32_t id_qk = idesc(false), id_pv = idesc(true);
+      const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
       const uint32_t sbase = ptx::smem_u32(smem);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
       const int nX[2] = {nA, nB};
       auto issue_s = [&](int x, int j) {   // S_x(j) = Q_x K_j^T
         const int s = j % kStages;
-        const uint32_t qa = sbase + kQOff + x * kTileBytes;
-        const uint32_t kb = sbase + kKOff + s * kTileBytes;
+        const uint32_t qa = sbase + L::kQOff + x * L::kTile;
+        const uint32_t kb = sbase + L::kKOff + s * L::kTile;
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
+        for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
           mma_ss(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
         }
@@ -352,7 +359,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
         const int s = j % kStages;
-        const uint32_t vb = sbase + kVOff + s * kTileBytes;
+        const uint32_t vb = sbase + L::kVOff + s * L::kTile;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
           mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
@@ -397,7 +404,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const int qpos = q0 + row;
     const uint32_t lane_base = tmem + (((warp % 4) * 32) << 16);
     const uint32_t tS = lane_base + x * 128;
-    const uint32_t tO = lane_base + 256 + x * 128;
+    const uint32_t tO = lane_base + 256 + x * D;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n; ++j) {
       if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
@@ -439,7 +446,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const float f = ptx::fast_exp2(m_run - m_new);
             if (j > 0) {
 #pragma unroll 1
-              for (int c0 = 0; c0 < 128; c0 += 32) {
+              for (int c0 = 0; c0 < D; c0 += 32) {
                 uint32_t o[32];
                 TMEM_LD32(tO + c0, o);
                 tmem_wait_ld();
@@ -510,7 +517,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         if (j > 0 && __any_sync(0xffffffffu, f != 1.f)) {
           // O_x(j-1) is complete: S_x(j) was issued after PV_x(j-1) and has retired
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = 0; c0 < D; c0 += 32) {
             uint32_t o[32];
             TMEM_LD32(tO + c0, o);
             tmem_wait_ld();
@@ -542,10 +549,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       fence_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * kD;
+    __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
     const bool live = qpos < p.n_q;
 #pragma unroll
-    for (int c0 = 0; c0 < 128; c0 += 32) {
+    for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];
       if (n > 0) {
         TMEM_LD32(tO + c0, o);
@@ -595,7 +602,8 @@ static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const 
 
 void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* out, int n_q, int hq,
                     int slot, int kv_len, float scale, bool causal, cudaStream_t st) {
-  if (v.d != pf::kD) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 128");
+  if (v.d != 128 && v.d != 64) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 64 and 128");
+  const int D = v.d;
   if (hq % v.hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
   if (slot < 0 || slot >= v.n_slots) throw Fail(VATTN_VALUE_ERROR, "slot out of range");
   if (kv_len < 0 || kv_len > v.slot_tokens) throw Fail(VATTN_VALUE_ERROR, "kv_len out of range");
@@ -605,13 +613,13 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   // Per-call maps: the K/V token extent is exactly kv_len, so rows past it are zero-filled by
   // TMA instead of being read from (possibly stale or unmapped) pages.
   const int kvl = std::max(kv_len, 1);
-  cuuint64_t qd[3] = {(cuuint64_t)pf::kD, (cuuint64_t)hq, (cuuint64_t)n_q};
-  cuuint64_t qs[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)hq * pf::kD * 2};
+  cuuint64_t qd[3] = {(cuuint64_t)D, (cuuint64_t)hq, (cuuint64_t)n_q};
+  cuuint64_t qs[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
   cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
   const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
   // 3-D map rooted at the request's slot: [D, Hkv, kv_len] (the slot index is folded into the base)
-  cuuint64_t kd[3] = {(cuuint64_t)pf::kD, (cuuint64_t)v.hkv, (cuuint64_t)kvl};
-  cuuint64_t ks[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)v.token_stride};
+  cuuint64_t kd[3] = {(cuuint64_t)D, (cuuint64_t)v.hkv, (cuuint64_t)kvl};
+  cuuint64_t ks[2] = {(cuuint64_t)D * 2, (cuuint64_t)v.token_stride};
   cuuint32_t kb[3] = {64, 1, (cuuint32_t)pf::kBN};
   const uint64_t slot_off = (uint64_t)slot * (uint64_t)v.slot_stride;
   const CUtensorMap kmap = make_map(reinterpret_cast<void*>(v.k_base + slot_off), 3, kd, ks, kb);
@@ -626,22 +634,33 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
   p.q_off = kv_len - n_q;
   p.causal = causal ? 1 : 0;
-  if (scale <= 0.f) scale = 1.f / sqrtf((float)pf::kD);
+  if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(p.n_pairs, hq);
+  if (D == 64) {
+    static bool attr64 = false;
+    if (!attr64) {
+      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    pf::PfL<64>::kSmem), "smem attr");
+      attr64 = true;
+    }
+    pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, p);
+    check_rt(cudaGetLastError(), "prefill launch");
+    return;
+  }
   static int poly = -1;
   if (poly < 0) {
     const char* e = getenv("VATTN_PF_POLY");   // share of exp2 on the FMA pipe, in quarters
     poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
+    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
   }
-  dim3 grid(p.n_pairs, hq);
-  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
-  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
-  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
-  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
+  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
+  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
+  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
@@ -681,11 +700,11 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
   static bool attr = false;
   if (!attr) {
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  pf::kSmemBytes), "smem attr");
+                                  pf::PfL<128>::kSmem), "smem attr");
     attr = true;
   }
   dim3 grid(p.n_pairs, hq);
-  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(qmap, kmap, vmap, p);
+  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
 }
 

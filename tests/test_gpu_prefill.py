@@ -29,19 +29,20 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("d", [128, 64])
 @pytest.mark.parametrize("case", CASES, ids=[str(i) for i in range(len(CASES))])
-def test_prefill_raw_matches_oracle(case):
+def test_prefill_raw_matches_oracle(case, d):
     from paper_2405_04437_b200.attention import prefill_attention_raw
 
     dev = _cuda()
     n_q, kv_len, hq, hkv, causal, slot, slots = case
     gen = torch.Generator().manual_seed(11)
     L = (kv_len + 127) // 128 * 128 + 128
-    k = torch.randn(slots, L, hkv, 128, generator=gen).to(torch.bfloat16)
-    v = torch.randn(slots, L, hkv, 128, generator=gen).to(torch.bfloat16)
+    k = torch.randn(slots, L, hkv, d, generator=gen).to(torch.bfloat16)
+    v = torch.randn(slots, L, hkv, d, generator=gen).to(torch.bfloat16)
     k[:, kv_len:] = float("nan")          # rows past kv_len must never be read into the result
     v[:, kv_len:] = float("nan")
-    q = torch.randn(n_q, hq, 128, generator=gen).to(torch.bfloat16)
+    q = torch.randn(n_q, hq, d, generator=gen).to(torch.bfloat16)
     ref = prefill_ref(q, k[slot, :kv_len], v[slot, :kv_len], causal=causal)
     out = prefill_attention_raw(q.to(dev), k.to(dev), v.to(dev), slot, kv_len, causal=causal)
     torch.cuda.synchronize()
@@ -143,3 +144,17 @@ def test_prefill_max_jumps_take_the_rescale_paths():
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
     assert max_rel_err(out.cpu(), ref) <= TOL
+
+
+def test_tiny_config_serving_loop_on_gpu():
+    """BASELINE config 1 geometry (1 layer, 8 Q / 2 KV heads, D 64, 2 MiB pages) through the
+    wall-clock Algorithm-1 loop: prefill (tcgen05, D 64) + fused decode on the virtual cache."""
+    _cuda()
+    from paper_2405_04437_b200.geometry import tiny
+    from paper_2405_04437_b200.serving import run
+
+    g = tiny()
+    recs = [(0, 128, 5), (0, 400, 3), (1, 300, 4), (2, 200, 2)]
+    m = run(recs, g, mode="overlapped", clock="wall", pool_bytes=64 << 20, eager_groups=1)
+    s = m.summary()
+    assert s["completed_requests"] == 4 and s["generated_tokens"] == 14
