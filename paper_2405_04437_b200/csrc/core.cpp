@@ -217,6 +217,7 @@ class Manager {
   uint64_t buffer_base(int32_t b) const;
   const std::vector<int64_t>& last_plan() const { return last_plan_; }
   CacheView layer_view(int32_t layer) const;
+  void check_decode_tiling() const;
   bool real() const { return backend_ == VATTN_BACKEND_CUDA; }
   int64_t max_batch() const { return (int64_t)slots_.size(); }
   int32_t hq_local() const { return hq_local_; }
@@ -1396,6 +1397,16 @@ uint64_t Manager::buffer_base(int32_t b) const {
   return (uint64_t)va_[b];
 }
 
+// The decode kernels stream 64-token TMA boxes (kernels.cu kTile); a box that starts below a
+// row's length must end inside its mapped page-groups, which holds for every length only when a
+// page-group spans a whole number of 64-token tiles.
+void Manager::check_decode_tiling() const {
+  if (t_ % (64 * per_buffer_token_bytes_) != 0)
+    throw Fail(VATTN_UNSUPPORTED, "decode kernels need page-groups of a whole number of 64-token tiles (page-group " +
+                                      std::to_string(t_) + " B, token row " + std::to_string(per_buffer_token_bytes_) +
+                                      " B); prefill and append have no such constraint");
+}
+
 CacheView Manager::layer_view(int32_t layer) const {
   if (!real()) throw Fail(VATTN_BAD_STATE, "kernels need the CUDA backend");
   if (layer < 0 || layer >= n_layers_) throw Fail(VATTN_VALUE_ERROR, "layer out of range");
@@ -1736,6 +1747,7 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
                           int32_t num_splits, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
+    h->m->check_decode_tiling();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
@@ -1758,6 +1770,7 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
                                  int32_t num_splits, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
+    h->m->check_decode_tiling();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
@@ -1780,6 +1793,7 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
                                  int32_t num_splits, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
+    h->m->check_decode_tiling();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);

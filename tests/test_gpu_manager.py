@@ -258,7 +258,7 @@ def test_sliced_layout_kernels():
     from paper_2405_04437_b200.attention import decode_attention_append, kv_append, prefill_attention
 
     dev = torch.device("cuda")
-    g = ModelGeometry(3, 4, 128, 2, max_context=2048, max_batch=3, n_q_heads_total=16)
+    g = ModelGeometry(4, 4, 128, 2, max_context=2048, max_batch=3, n_q_heads_total=16)
     mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, sliced=True))
     assert mgr.buffer_count == 2
     r = mgr.alloc_reqid()
@@ -267,7 +267,7 @@ def test_sliced_layout_kernels():
     lens[r] = S + 1
     assert mgr.step(lens).ok
     gen = torch.Generator().manual_seed(4)
-    for layer in range(3):
+    for layer in range(4):
         kn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
         vn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
         q = torch.randn(S, 16, 128, generator=gen).to(torch.bfloat16)
@@ -291,6 +291,18 @@ def test_sliced_layout_kernels():
         # the view sees the sliced strides
         assert torch.equal(mgr.k_cache(layer)[r, :S].cpu(), kn[0])
     mgr.close()
+    # 3 layers: a 3 KiB token row does not tile a 2 MiB page-group into 64-token boxes, so a decode
+    # box could reach an unmapped page; the decode entry points refuse it instead of faulting
+    from paper_2405_04437_b200.attention import decode_attention
+    from paper_2405_04437_b200.errors import UnsupportedError
+    g3 = ModelGeometry(3, 4, 128, 2, max_context=2048, max_batch=3, n_q_heads_total=16)
+    m3 = KVCacheManager(g3, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, sliced=True))
+    r3 = m3.alloc_reqid()
+    assert m3.step([100 if i == r3 else 0 for i in range(3)]).ok
+    with pytest.raises(UnsupportedError):
+        decode_attention(m3, 0, torch.zeros(1, 16, 128, dtype=torch.bfloat16, device=dev),
+                         torch.tensor([100], dtype=torch.int32, device=dev), torch.tensor([r3], dtype=torch.int32, device=dev))
+    m3.close()
 
 
 def test_bounds_guard_raises_instead_of_faulting(monkeypatch):
