@@ -672,6 +672,57 @@ def extra_y34_shards(local):
     return out
 
 
+def extra_l8_shards(local, steps=20):
+    """The headline workload's per-rank step at the KV-head shard shapes of a G = 1/2/4/8 job,
+    each run on this GPU: manager + 32 fused append+decode launches replayed from one CUDA graph
+    per step (as in the timed region).  Ranks share nothing on this path, so the job's tokens/s
+    at G GPUs is B / (per-rank step time); this is the single-GPU prediction the torchrun
+    scaling run (N = 2/4/8) checks."""
+    import torch
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention_append
+    from paper_2405_04437_b200.geometry import llama3_8b
+
+    dev = torch.device("cuda", local)
+    out = {}
+    base = None
+    for G in (1, 2, 4, 8):
+        g = llama3_8b(max_context=8192, max_batch=64).with_tp(G)
+        B, N, hq, hkv, d = g.max_batch, g.n_layers, g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
+        groups = math.ceil((4096 + steps + 8) * g.per_token_layer_bytes / MB2)
+        mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=(groups + 1) * 2 * N * B * MB2,
+                                              eager_groups=0, reclaim_threshold=0.0), backend="cuda", device=local)
+        rids = [mgr.alloc_reqid() for _ in range(B)]
+        assert mgr.step([4096 + steps + 4] * B).ok
+        gen = torch.Generator(device=dev).manual_seed(G)
+        q = torch.randn(N, B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+        kn = torch.randn(N, B, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+        o = torch.empty_like(q)
+        idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+        pos = torch.full((B,), 4096, dtype=torch.int32, device=dev)
+
+        def body():
+            for layer in range(N):
+                decode_attention_append(mgr, layer, q[layer], kn[layer], kn[layer], pos, idx, out=o[layer])
+
+        body()
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
+            body()
+        ms = _time_ms(gr.replay, iters=steps)
+        del gr
+        mgr.close()
+        tok = B / (ms / 1e3)
+        base = base or tok
+        out[f"G{G}"] = {"hq": hq, "hkv": hkv, "ms_per_step": ms, "job_tokens_per_s": tok,
+                        "scaling_efficiency_vs_G1": tok / (base * G)}
+    return out
+
+
 def extra_decode_growth(local, steps=96, warm=8):
     """Exposed map ms/iter (BASELINE metric) while decode contexts GROW across page-group
     boundaries: Llama-3-8B shape, 32 layers, B 64, contexts staggered 3584 + 16*b (mean ~4.1K)
@@ -924,7 +975,8 @@ def main(argv=None):
             extras = {}
             for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
                              ("paged_vs_contiguous", extra_paged),
-                             ("y34_shards", extra_y34_shards), ("libraries", extra_libraries),
+                             ("y34_shards", extra_y34_shards), ("l8_shards", extra_l8_shards),
+                             ("libraries", extra_libraries),
                              ("serving", extra_serving)):
                 try:
                     extras[name] = fn(local)

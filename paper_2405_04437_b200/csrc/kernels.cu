@@ -647,7 +647,9 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
       const char* e = getenv("VATTN_DEC_STAGES");
       return e ? atoi(e) : 0;
     }();
-    const int stages = forced ? forced : (batch * hkv * p.num_splits >= 2 * num_sms() ? 3 : 4);
+    // more CTAs than SMs: 2 CTAs/SM (3 stages) so a grid of up to 2 x 148 runs in one wave
+    // (L8 at G = 2: 256 CTAs; measured 6.26 vs 6.12 TB/s with 4 stages in two waves)
+    const int stages = forced ? forced : (batch * hkv * p.num_splits > num_sms() ? 3 : 4);
     if (paged) {   // same rule, so the paged comparison differs from the contiguous path only in layout
       if (stages == 3) run_decode<128, 3, true>(km, vm, p, batch, hkv, st);
       else run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
