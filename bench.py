@@ -109,13 +109,13 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not dist.is_initialized():
-        backend = os.environ.get("VATTN_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
-        dist.init_process_group(backend=backend)
     if os.environ.get("VATTN_BENCH_ONE_GPU"):   # test harness: every rank on cuda:0 (gloo backend)
         local = 0
     if torch.cuda.is_available():
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(local)             # before NCCL binds its communicator to a device
+    if world > 1 and not dist.is_initialized():
+        backend = os.environ.get("VATTN_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend=backend)
     return world, rank, local
 
 
