@@ -252,6 +252,21 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
                                  const void* v_new, void* out, int32_t batch,
                                  const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
                                  float scale, int32_t num_splits, void* stream);
+/* Rotary embedding for the fused append+decode (flash_attn_with_kvcache rotary_cos / rotary_sin /
+ * rotary_interleaved, as the paper's kernels use it): q and k_new are rotated at
+ * position cache_seqlens[b] before attention, and k is cached rotated.  Tables fp32
+ * [positions, rotary_dim / 2]; rotary_dim a multiple of 16, <= head_dim. */
+typedef struct vattn_rotary {
+  const float* cos;
+  const float* sin;
+  int32_t rotary_dim;
+  int32_t interleaved;         /* 0: GPT-NeoX halves, 1: GPT-J adjacent pairs */
+} vattn_rotary;
+vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q, const void* k_new,
+                                        const void* v_new, void* out, int32_t batch,
+                                        const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                                        float scale, int32_t num_splits, const vattn_rotary* rotary,
+                                        void* stream);
 /* causal (bottom-right) prefill of q [n_q, Hq, D] against slot rows [0, kv_len). */
 vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                            int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
@@ -284,6 +299,11 @@ vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, c
                                      const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
                                      float scale, int32_t num_splits, void* workspace,
                                      int64_t workspace_bytes, void* stream);
+vattn_status vattn_decode_append_rotary_raw(const vattn_cache_desc* c, const void* q, const void* k_new,
+                                            const void* v_new, void* out, int32_t batch, int32_t n_q_heads,
+                                            const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
+                                            float scale, int32_t num_splits, const vattn_rotary* rotary,
+                                            void* workspace, int64_t workspace_bytes, void* stream);
 /* Paged-layout comparison kernel (PagedAttention block table; PAPER.md:602 block sizes):
  * pools [num_blocks, block_size, Hkv, D], block_table [batch, max_blocks] int32. */
 vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,

@@ -97,3 +97,26 @@ def max_rel_err(out, ref) -> float:
     ref = ref.float()
     denom = ref.abs().max().item()
     return (out.float() - ref).abs().max().item() / max(denom, 1e-30)
+
+
+def rotary_ref(x, cos, sin, positions, interleaved=False):
+    """Rotary embedding of x [B, H, D] at per-row positions [B] (fp32 result).
+
+    cos/sin: [positions, rotary_dim/2]; dims >= rotary_dim pass through.  Non-interleaved =
+    GPT-NeoX halves (x[i], x[i + rd/2]); interleaved = GPT-J pairs (x[2i], x[2i+1]).  This is
+    flash-attn's apply_rotary_emb as flash_attn_with_kvcache applies it to q and k at
+    cache_seqlens (the kernels the paper uses; not vendored in the reference).
+    """
+    x = x.float().clone()
+    rd = 2 * cos.shape[1]
+    c = cos.float()[positions.long()].unsqueeze(1)      # [B, 1, rd/2]
+    s = sin.float()[positions.long()].unsqueeze(1)
+    if interleaved:
+        x1, x2 = x[..., 0:rd:2].clone(), x[..., 1:rd:2].clone()
+        x[..., 0:rd:2] = x1 * c - x2 * s
+        x[..., 1:rd:2] = x1 * s + x2 * c
+    else:
+        x1, x2 = x[..., : rd // 2].clone(), x[..., rd // 2: rd].clone()
+        x[..., : rd // 2] = x1 * c - x2 * s
+        x[..., rd // 2: rd] = x1 * s + x2 * c
+    return x

@@ -68,6 +68,10 @@ class CacheDesc(C.Structure):
                 ("n_kv_heads", c_i32), ("head_dim", c_i32)]
 
 
+class RotaryC(C.Structure):
+    _fields_ = [("cos", c_vp), ("sin", c_vp), ("rotary_dim", c_i32), ("interleaved", c_i32)]
+
+
 class IterationResult(C.Structure):
     _fields_ = [("ok", c_i32), ("deferred", c_i32), ("sync_us", c_f64), ("eager_us", c_f64),
                 ("reclaim_us", c_f64), ("reclaimed_groups", c_i64), ("bg_wait_us", c_f64),
@@ -112,6 +116,10 @@ SIGNATURES = {
     "vattn_decode_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
     "vattn_decode_append_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                         c_f32, c_i32, c_vp, c_i64, c_vp]),
+    "vattn_decode_append_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32,
+                                           C.POINTER(RotaryC), c_vp]),
+    "vattn_decode_append_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                               c_f32, c_i32, C.POINTER(RotaryC), c_vp, c_i64, c_vp]),
     "vattn_prefill": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_f32, c_i32, c_vp]),
     "vattn_kv_append_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "vattn_decode_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_f32,

@@ -107,10 +107,30 @@ def decode_attention(mgr, layer: int, q, cache_seqlens, cache_batch_idx=None, so
     return out
 
 
+def _rotary(rotary_cos, rotary_sin, rotary_interleaved):
+    """fp32 tables [positions, rotary_dim / 2] -> (descriptor, keep-alive tensors)."""
+    if rotary_cos is None and rotary_sin is None:
+        return None, None
+    if rotary_cos is None or rotary_sin is None:
+        raise ValueError("rotary_cos and rotary_sin go together")
+    _need_cuda(rotary_cos, rotary_sin)
+    if rotary_cos.shape != rotary_sin.shape or rotary_cos.dim() != 2:
+        raise ValueError("rotary_cos / rotary_sin must both be [positions, rotary_dim / 2]")
+    cos = rotary_cos.to(torch.float32).contiguous()
+    sin = rotary_sin.to(torch.float32).contiguous()
+    r = _abi.RotaryC()
+    r.cos, r.sin = cos.data_ptr(), sin.data_ptr()
+    r.rotary_dim, r.interleaved = 2 * cos.shape[1], int(bool(rotary_interleaved))
+    return r, (cos, sin)
+
+
 def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cache_batch_idx=None,
-                            softmax_scale=None, out=None, num_splits: int = 0, stream=None):
+                            softmax_scale=None, out=None, num_splits: int = 0, stream=None,
+                            rotary_cos=None, rotary_sin=None, rotary_interleaved: bool = False):
     """Fused KV-append + decode (flash_attn_with_kvcache k=/v=): k_new/v_new [B, Hkv, D] are
-    written at row cache_seqlens[b] (the length before the token) and attended to, one launch."""
+    written at row cache_seqlens[b] (the length before the token) and attended to, one launch.
+    rotary_cos / rotary_sin [positions, rotary_dim / 2]: q and k_new are rotated at position
+    cache_seqlens[b] first and k is cached rotated (flash-attn's rotary semantics)."""
     _need_cuda(q, k_new, v_new)
     q, k_new, v_new = _bf16(q, "q"), _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     if out is None:
@@ -120,6 +140,12 @@ def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cac
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx, extra_rows=1)
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_decode_append_rotary(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
+                                               q.shape[0], _ptr(seq), _ptr(idx), float(scale), int(num_splits),
+                                               C.byref(rot), C.c_void_p(_stream(stream))))
+        return out
     check(lib().vattn_decode_append(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), q.shape[0],
                                     _ptr(seq), _ptr(idx), float(scale), int(num_splits), C.c_void_p(_stream(stream))))
     return out
@@ -228,7 +254,8 @@ def decode_attention_raw(q, k_cache, v_cache, cache_seqlens, cache_batch_idx=Non
 
 
 def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx=None,
-                                softmax_scale=None, out=None, num_splits: int = 0, stream=None):
+                                softmax_scale=None, out=None, num_splits: int = 0, stream=None,
+                                rotary_cos=None, rotary_sin=None, rotary_interleaved: bool = False):
     desc = cache_desc(k_cache, v_cache)
     q, k_new, v_new = _bf16(q, "q"), _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     out = torch.empty_like(q) if out is None else out
@@ -237,6 +264,12 @@ def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens
     b, hq, d = q.shape
     ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0))
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_decode_append_rotary_raw(C.byref(desc), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), b,
+                                                   hq, _ptr(seq), _ptr(idx), float(scale), int(num_splits),
+                                                   C.byref(rot), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
+        return out
     check(lib().vattn_decode_append_raw(C.byref(desc), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), b, hq,
                                         _ptr(seq), _ptr(idx), float(scale), int(num_splits), _ptr(ws), ws.numel(),
                                         C.c_void_p(_stream(stream))))

@@ -1787,6 +1787,31 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
   });
 }
 
+vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q, const void* k_new,
+                                        const void* v_new, void* out, int32_t batch,
+                                        const int32_t* cache_seqlens, const int32_t* batch_idx, float scale,
+                                        int32_t num_splits, const vattn_rotary* rotary, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    h->m->check_decode_tiling();
+    const vattn::CacheView v = h->m->layer_view(layer);
+    const int hq = h->m->hq_local();
+    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
+    if (need > h->workspace_bytes) {
+      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
+      h->workspace = nullptr;
+      h->workspace_bytes = 0;
+      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
+      h->workspace_bytes = need;
+    }
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale, num_splits,
+                         h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
 vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const void* k_new,
                                  const void* v_new, vattn_gather_t* g, int32_t batch,
                                  const int32_t* cache_seqlens, const int32_t* batch_idx, float scale,

@@ -74,6 +74,15 @@ void kernel_state_free(KernelState*);
 // straight into each rank's full [batch, Hq_total, D] buffer over NVLink peer memory (P2P
 // stores) at head offset rank*Hq_local, then the last CTA to finish raises this rank's flag in
 // every peer's signal array.  n_ranks = 0 disables it (plain local output).
+// Rotary embedding applied by the fused append+decode kernel to q and the new k at the token's
+// position (flash_attn_with_kvcache rotary_cos / rotary_sin / rotary_interleaved semantics).
+struct Rotary {
+  const float* cos = nullptr;   // [positions, rotary_dim / 2] fp32; nullptr = no rotary
+  const float* sin = nullptr;
+  int32_t dim = 0;              // rotary_dim: even, multiple of 16, <= head_dim
+  int32_t interleaved = 0;      // 0: GPT-NeoX halves (i, i + dim/2); 1: GPT-J pairs (2i, 2i + 1)
+};
+
 constexpr int kMaxGatherRanks = 8;
 struct GatherSink {
   void* dst[kMaxGatherRanks];          // rank r's full output (peer-mapped; own included)
@@ -96,7 +105,7 @@ void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const voi
                    int batch, int hq, const int32_t* seqlens, const int32_t* batch_idx,
                    float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st,
                    const void* k_new = nullptr, const void* v_new = nullptr,
-                   const GatherSink* sink = nullptr);
+                   const GatherSink* sink = nullptr, const Rotary* rot = nullptr);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
                     cudaStream_t st);

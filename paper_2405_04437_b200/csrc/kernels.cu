@@ -114,7 +114,40 @@ struct DecodeParams {
   __nv_bfloat16* v_cache;
   int64_t slot_stride, token_stride;
   GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
+  Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
 };
+
+// Rotate one 16-byte chunk (8 bf16, dims [8c, 8c+8)) at the position whose tables start at
+// cosr / sinr.  `partner` is the chunk holding the other element of each pair in the NeoX layout
+// (c -/+ dim/16); GPT-J pairs sit inside the chunk.  fp32 math, one bf16 rounding.
+__device__ __forceinline__ uint4 rotary_chunk(uint4 own, uint4 partner, int c, const float* cosr,
+                                              const float* sinr, int dim, bool interleaved) {
+  if (c * 8 >= dim) return own;
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&own);
+  const __nv_bfloat16* y = reinterpret_cast<const __nv_bfloat16*>(&partner);
+  uint4 out;
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
+  const int half = dim / 2;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int d = c * 8 + e;
+    float r;
+    if (interleaved) {
+      const int i = d >> 1;
+      const float cs = __ldg(cosr + i), sn = __ldg(sinr + i);
+      const float x1 = __bfloat162float(x[e & ~1]), x2 = __bfloat162float(x[e | 1]);
+      r = (e & 1) ? x1 * sn + x2 * cs : x1 * cs - x2 * sn;
+    } else if (d < half) {
+      const float cs = __ldg(cosr + d), sn = __ldg(sinr + d);
+      r = __bfloat162float(x[e]) * cs - __bfloat162float(y[e]) * sn;
+    } else {
+      const float cs = __ldg(cosr + d - half), sn = __ldg(sinr + d - half);
+      r = __bfloat162float(y[e]) * sn + __bfloat162float(x[e]) * cs;
+    }
+    o[e] = __float2bfloat16(r);
+  }
+  return out;
+}
 
 // ---- fused head all-gather epilogue (gather.cu owns the buffers and the wait) ----
 // Output row (b, local head h) goes to row (b, head_off + h) of every rank's full output: one
@@ -231,12 +264,23 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
   }
 
   // ===== consumers: 4 warps x 16 tokens of every tile =====
-  // Q rows of this GQA group -> smem (rows >= group are zero padding of the m16 tile)
+  // Q rows of this GQA group -> smem (rows >= group are zero padding of the m16 tile), rotated
+  // at the new token's position when rotary tables are given
+  const bool rotary = fused && p.rot.cos != nullptr;
+  const int rhalf_chunks = p.rot.dim / 16;
   for (int i = threadIdx.x; i < 16 * (D / 8); i += kConsumerWarps * 32) {
     const int r = i / (D / 8), c = i % (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < p.group)
-      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.hq + kvh * p.group + r) * D + c * 8);
+    if (r < p.group) {
+      const __nv_bfloat16* qrow = p.q + ((int64_t)b * p.hq + kvh * p.group + r) * D;
+      v = *reinterpret_cast<const uint4*>(qrow + c * 8);
+      if (rotary && c * 8 < p.rot.dim) {
+        const int pc = p.rot.interleaved ? c : (c < rhalf_chunks ? c + rhalf_chunks : c - rhalf_chunks);
+        const uint4 w = *reinterpret_cast<const uint4*>(qrow + pc * 8);
+        const int64_t t = (int64_t)pos_new * (p.rot.dim / 2);
+        v = rotary_chunk(v, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
+      }
+    }
     *reinterpret_cast<uint4*>(qs + r * L::kQStride + c * 8) = v;
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
@@ -271,7 +315,13 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
                           (int64_t)kvh * D * 2;
       for (int c = lane % 16; c < D / 8; c += 16) {
         const bool is_v = lane >= 16;
-        const uint4 val = *reinterpret_cast<const uint4*>((is_v ? p.v_new : p.k_new) + src + c * 8);
+        uint4 val = *reinterpret_cast<const uint4*>((is_v ? p.v_new : p.k_new) + src + c * 8);
+        if (rotary && !is_v && c * 8 < p.rot.dim) {   // k is cached rotated (flash-attn semantics)
+          const int pc = p.rot.interleaved ? c : (c < rhalf_chunks ? c + rhalf_chunks : c - rhalf_chunks);
+          const uint4 w = *reinterpret_cast<const uint4*>(p.k_new + src + pc * 8);
+          const int64_t t = (int64_t)pos_new * (p.rot.dim / 2);
+          val = rotary_chunk(val, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
+        }
         const uint32_t a = ptx::swz128((is_v ? vs : ks) + (c >> 3) * L::kHalfBytes, r, c & 7);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(val.x), "r"(val.y), "r"(val.z),
                      "r"(val.w));
@@ -598,7 +648,8 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
                           const int32_t* batch_idx, const int32_t* block_table, int max_blocks,
                           int block_size, int box_tokens, float scale, int num_splits,
                           int max_len, void* ws, int64_t ws_bytes, bool paged, cudaStream_t st,
-                          const FusedAppend* fa = nullptr, const GatherSink* sink = nullptr) {
+                          const FusedAppend* fa = nullptr, const GatherSink* sink = nullptr,
+                          const Rotary* rot = nullptr) {
   if (hq % hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
   const int group = hq / hkv;
   if (group > 16) throw Fail(VATTN_UNSUPPORTED, "GQA group larger than 16");
@@ -626,6 +677,12 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
     p.v_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->v_base);
     p.slot_stride = fa->view->slot_stride;
     p.token_stride = fa->view->token_stride;
+  }
+  if (rot && rot->cos) {
+    if (!fa) throw Fail(VATTN_VALUE_ERROR, "rotary embedding needs the fused append (k_new / v_new)");
+    if (!rot->sin || rot->dim <= 0 || rot->dim % 16 || rot->dim > d)
+      throw Fail(VATTN_VALUE_ERROR, "rotary_dim must be a positive multiple of 16 and <= head_dim");
+    p.rot = *rot;
   }
   if (sink && sink->n_ranks) {
     if (sink->n_ranks > kMaxGatherRanks || sink->hq_total < hq * sink->n_ranks)
@@ -667,7 +724,7 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
 void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void* out, int batch,
                    int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
                    int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st, const void* k_new,
-                   const void* v_new, const GatherSink* sink) {
+                   const void* v_new, const GatherSink* sink, const Rotary* rot) {
   check_view(v);
   // Token extent = every row inside the slot stride, so a 64-row tile that starts below seqlen
   // never takes TMA's out-of-bounds path (which faults on VMM-backed maps when the box
@@ -678,7 +735,7 @@ void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void
   const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
   FusedAppend fa{k_new, v_new, &v};
   decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
-                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr, sink);
+                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr, sink, rot);
 }
 
 }  // namespace vattn
@@ -751,6 +808,20 @@ vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, c
     const vattn::CacheView v = vattn::view_from_desc(c);
     vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
+  });
+}
+
+vattn_status vattn_decode_append_rotary_raw(const vattn_cache_desc* c, const void* q, const void* k_new,
+                                            const void* v_new, void* out, int32_t batch, int32_t hq,
+                                            const int32_t* cache_seqlens, const int32_t* batch_idx, float scale,
+                                            int32_t num_splits, const vattn_rotary* rotary, void* ws,
+                                            int64_t ws_bytes, void* stream) {
+  return kguard([&] {
+    if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    const vattn::CacheView v = vattn::view_from_desc(c);
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, cache_seqlens, batch_idx, scale, num_splits, ws,
+                         ws_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
   });
 }
 

@@ -112,3 +112,51 @@ def test_prefill_matches_flash_attn(n_q, kv_len, causal):
     ours = prefill_attention_raw(q, kc, vc, slot, kv_len, causal=causal)
     torch.cuda.synchronize()
     assert max_rel_err(ours.float().cpu(), ref.float().cpu()) <= TOL
+
+
+@pytest.mark.parametrize("interleaved", [False, True])
+def test_rotary_fused_decode_matches_flash_attn_on_the_vmm_cache(interleaved):
+    """Manager-backed fused append+decode with rotary vs flash_attn_with_kvcache(k=, v=,
+    rotary_cos=, rotary_sin=, rotary_interleaved=) on two copies of the same VMM-backed cache."""
+    fa = _fa()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import decode_attention_append, kv_append
+    from paper_2405_04437_b200.geometry import ModelGeometry
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(n_layers=2, kv_heads_total=8, head_dim=128, bytes_per_elem=2, max_context=4096,
+                      max_batch=4, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=1 << 30))
+    try:
+        gen = torch.Generator().manual_seed(12)
+        rids = [mgr.alloc_reqid() for _ in range(3)]
+        lens = [0] * 4
+        for rid, n in zip(rids, (100, 1023, 2500)):
+            lens[rid] = n + 1
+        assert mgr.step(lens).ok
+        for layer in range(2):      # layer 0 = ours, layer 1 = flash-attn; same history
+            gl = torch.Generator().manual_seed(13)
+            for rid in rids:
+                n = lens[rid] - 1
+                kv_append(mgr, layer, _rand((1, n, 8, 128), gl, dev), _rand((1, n, 8, 128), gl, dev),
+                          torch.zeros(1, dtype=torch.int32, device=dev),
+                          torch.tensor([rid], dtype=torch.int32, device=dev))
+        idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+        seq = torch.tensor([lens[r] - 1 for r in rids], dtype=torch.int32, device=dev)
+        q = _rand((3, 32, 128), gen, dev)
+        kn, vn = _rand((3, 8, 128), gen, dev), _rand((3, 8, 128), gen, dev)
+        ang = torch.arange(4096, dtype=torch.float32)[:, None] / (10000 ** (torch.arange(0, 128, 2) / 128))[None, :]
+        cos, sin = ang.cos().to(dev), ang.sin().to(dev)
+        ours = decode_attention_append(mgr, 0, q, kn, vn, seq, idx, rotary_cos=cos, rotary_sin=sin,
+                                       rotary_interleaved=interleaved)
+        ref = fa.flash_attn_with_kvcache(q.unsqueeze(1), mgr.k_cache(1), mgr.v_cache(1), k=kn.unsqueeze(1),
+                                         v=vn.unsqueeze(1), rotary_cos=cos.to(torch.bfloat16),
+                                         rotary_sin=sin.to(torch.bfloat16), cache_seqlens=seq,
+                                         cache_batch_idx=idx, rotary_interleaved=interleaved).squeeze(1)
+        torch.cuda.synchronize()
+        assert max_rel_err(ours.float().cpu(), ref.float().cpu()) <= TOL
+        for i, r in enumerate(rids):   # both caches hold the rotated new k (bf16 tables on the flash-attn side)
+            p = lens[r] - 1
+            assert torch.allclose(mgr.k_cache(0)[r, p].float(), mgr.k_cache(1)[r, p].float(), rtol=2e-2, atol=2e-2)
+    finally:
+        mgr.close()

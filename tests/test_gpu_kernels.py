@@ -173,3 +173,40 @@ def test_kv_append_paged_bit_exact():
     kd, vd = kp.to(dev), vp.to(dev)
     kv_append_paged(kd, vd, kn.to(dev), vn.to(dev), table.to(dev), seq.to(dev))
     assert torch.equal(kd.cpu(), kr) and torch.equal(vd.cpu(), vr)
+
+
+@pytest.mark.parametrize("d,rd,inter,splits", [(128, 128, False, 0), (128, 64, False, 3), (128, 128, True, 0),
+                                               (64, 32, True, 2), (64, 64, False, 0)])
+def test_fused_decode_rotary_matches_oracle(d, rd, inter, splits):
+    """Rotary at append (flash_attn_with_kvcache rotary_cos/sin): q and k_new rotated at position
+    cache_seqlens[b]; k cached rotated; attention over the rotated cache."""
+    from oracle.attention import rotary_ref
+    from paper_2405_04437_b200.attention import decode_attention_append_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(7)
+    B, hq, hkv, L = 4, 16, 4, 1024
+    lens = [0, 63, 500, 1000]
+    k, v = _mk_cache(B, L, hkv, d, gen)
+    q = _rand((B, hq, d), gen)
+    kn, vn = _rand((B, hkv, d), gen), _rand((B, hkv, d), gen)
+    pos = torch.arange(L, dtype=torch.float32)
+    inv = 1.0 / (10000 ** (torch.arange(0, rd, 2, dtype=torch.float32) / rd))
+    ang = pos[:, None] * inv[None, :]
+    cos, sin = ang.cos(), ang.sin()
+    seq = torch.tensor(lens, dtype=torch.int32)
+    qr = rotary_ref(q, cos, sin, seq, inter).to(torch.bfloat16)
+    kr = rotary_ref(kn, cos, sin, seq, inter).to(torch.bfloat16)
+    k_ref, v_ref = k.clone(), v.clone()
+    for b, n in enumerate(lens):
+        k_ref[b, n], v_ref[b, n] = kr[b], vn[b]
+    ref = decode_ref(qr, k_ref, v_ref, seq + 1)
+    kd, vd = k.to(dev), v.to(dev)
+    out = decode_attention_append_raw(q.to(dev), kd, vd, kn.to(dev), vn.to(dev), seq.to(dev), num_splits=splits,
+                                      rotary_cos=cos.to(dev), rotary_sin=sin.to(dev), rotary_interleaved=inter)
+    torch.cuda.synchronize()
+    assert max_rel_err(out.cpu(), ref) <= TOL
+    got = kd.cpu()
+    for b, n in enumerate(lens):      # the cached row is the rotated k (one bf16 rounding of fp32 math)
+        assert torch.allclose(got[b, n].float(), kr[b].float(), rtol=1e-2, atol=1e-2)
+        assert torch.equal(vd.cpu()[b, n], vn[b])
