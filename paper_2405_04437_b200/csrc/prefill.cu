@@ -378,7 +378,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         for (int x = 0; x < 2; ++x) {
           if (j >= nX[x]) continue;
           PF_TRACE(2 + x, j, 0);
-          ptx::mbar_wait(&p_full[x], j & 1);
+          // polled without a suspend hint: the issuer wakes sooner (measured 1229 vs 1220 TF)
+          ptx::mbar_wait_poll(&p_full[x], j & 1);
           PF_TRACE(2 + x, j, 1);
           fence_after();
           issue_pv(x, j);
