@@ -1,14 +1,17 @@
 """Benchmark of the vAttention hot path on B200 (driver contract: one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload l8_decode|y34_decode|y6_prefill]
+                    [--workload l8_decode|y34_decode] [--gather none|fused|nccl] [--eager]
 
 Default workload = BASELINE config 2 (Llama-3-8B-shaped decode: 32 layers, 32 Q / 8 KV heads,
 D 128, batch 64, context 4K, bf16, 2 MiB pages).  One step = one decode iteration of the whole
 KV cache: allocator `step` (+ the background thread mapping the next iteration's pages), then
-per layer KV-append of the new token and split-K decode attention over it.  `value` is decode
-tokens/s with inputs resident in HBM; `e2e` is the same through the public API with the inputs
-copied H2D from pinned host memory and the outputs read back D2H every step.
+per layer one fused launch that appends the new token's K/V and runs decode attention over the
+row (timed steps replay one CUDA graph each; `--eager` launches them one by one).  `value` is
+decode tokens/s with inputs resident in HBM; `e2e` is the same through the public API with the
+inputs copied H2D from pinned host memory and the outputs read back D2H every step.  Extras
+(N = 1): decode growth across page-groups, Yi-6B prefill, paged-layout comparisons, shard
+shapes, flash-attn / cuDNN, and the config-5 serving trace.
 
 Multi-GPU (torchrun, one process per GPU): KV heads are sharded (geometry.with_tp(N)); every
 rank runs an independent allocator + kernels over its heads, no data-path collective; the whole
