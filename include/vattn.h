@@ -267,6 +267,16 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
                                         const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
                                         float scale, int32_t num_splits, const vattn_rotary* rotary,
                                         void* stream);
+/* Rotary at append / prefill (same tables and layouts): kv_append rotates each new k row at its
+ * position cache_seqlens[b] + i before caching it; prefill rotates query row i at position
+ * kv_len - n_q + i inside the tcgen05 kernel (in shared memory, before the first MMA). */
+vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new, const void* v_new,
+                                    int32_t batch, int32_t n_new, const int32_t* cache_seqlens,
+                                    const int32_t* cache_batch_idx, const vattn_rotary* rotary,
+                                    void* stream);
+vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
+                                  int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
+                                  const vattn_rotary* rotary, void* stream);
 /* causal (bottom-right) prefill of q [n_q, Hq, D] against slot rows [0, kv_len). */
 vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                            int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
@@ -304,6 +314,13 @@ vattn_status vattn_decode_append_rotary_raw(const vattn_cache_desc* c, const voi
                                             const int32_t* cache_seqlens, const int32_t* cache_batch_idx,
                                             float scale, int32_t num_splits, const vattn_rotary* rotary,
                                             void* workspace, int64_t workspace_bytes, void* stream);
+vattn_status vattn_kv_append_rotary_raw(const vattn_cache_desc* c, const void* k_new, const void* v_new,
+                                        int32_t batch, int32_t n_new, const int32_t* cache_seqlens,
+                                        const int32_t* cache_batch_idx, const vattn_rotary* rotary,
+                                        void* stream);
+vattn_status vattn_prefill_rotary_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
+                                      int32_t n_q_heads, int32_t req_slot, int32_t kv_len, float scale,
+                                      int32_t causal, const vattn_rotary* rotary, void* stream);
 /* Paged-layout comparison kernel (PagedAttention block table; PAPER.md:602 block sizes):
  * pools [num_blocks, block_size, Hkv, D], block_table [batch, max_blocks] int32. */
 vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,

@@ -116,6 +116,13 @@ SIGNATURES = {
     "vattn_decode_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),
     "vattn_decode_append_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                         c_f32, c_i32, c_vp, c_i64, c_vp]),
+    "vattn_kv_append_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, C.POINTER(RotaryC), c_vp]),
+    "vattn_kv_append_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                           C.POINTER(RotaryC), c_vp]),
+    "vattn_prefill_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_f32, c_i32,
+                                     C.POINTER(RotaryC), c_vp]),
+    "vattn_prefill_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_f32,
+                                         c_i32, C.POINTER(RotaryC), c_vp]),
     "vattn_decode_append_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32,
                                            C.POINTER(RotaryC), c_vp]),
     "vattn_decode_append_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,

@@ -74,10 +74,12 @@ def check_bounds(mgr, cache_seqlens, cache_batch_idx=None, extra_rows: int = 0) 
 
 
 # ------------------------------------------------------------------ manager-backed ops
-def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None):
+def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None,
+              rotary_cos=None, rotary_sin=None, rotary_interleaved: bool = False):
     """Write k_new/v_new [B, T, Hkv, D] (or [B, Hkv, D] for one token) at rows
     cache_seqlens[b] .. +T of slot cache_batch_idx[b].  The rows must be backed (call
-    mgr.step with the grown lengths first)."""
+    mgr.step with the grown lengths first).  With rotary tables, k row i is cached rotated at
+    position cache_seqlens[b] + i."""
     _need_cuda(k_new, v_new)
     if k_new.dim() == 3:
         k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
@@ -86,6 +88,11 @@ def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx, extra_rows=k_new.shape[1])
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_kv_append_rotary(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
+                                           _ptr(seq), _ptr(idx), C.byref(rot), C.c_void_p(_stream(stream))))
+        return
     check(lib().vattn_kv_append(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
                                 _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
 
@@ -179,9 +186,11 @@ def decode_attention_gather(mgr, layer: int, q, gather, cache_seqlens, cache_bat
 
 
 def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None, causal=True,
-                      softmax_scale=None, out=None, stream=None):
+                      softmax_scale=None, out=None, stream=None, rotary_cos=None, rotary_sin=None,
+                      rotary_interleaved: bool = False):
     """Causal (bottom-right aligned) attention of q [S, Hq, D] over rows [0, kv_len) of slot
-    req_id (default kv_len = S, i.e. the prompt just appended)."""
+    req_id (default kv_len = S, i.e. the prompt just appended).  With rotary tables, query row i
+    is rotated at position kv_len - S + i inside the kernel (append k with the same tables)."""
     _need_cuda(q)
     q = _bf16(q, "q")
     if out is None:
@@ -190,6 +199,11 @@ def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, [kv_len], [req_id])
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_prefill_rotary(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
+                                         float(scale), int(bool(causal)), C.byref(rot), C.c_void_p(_stream(stream))))
+        return out
     check(lib().vattn_prefill(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
                               float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
     return out
@@ -215,13 +229,20 @@ def cache_desc(k_cache, v_cache) -> _abi.CacheDesc:
     return desc
 
 
-def kv_append_raw(k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None):
+def kv_append_raw(k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx=None, stream=None,
+                  rotary_cos=None, rotary_sin=None, rotary_interleaved: bool = False):
     desc = cache_desc(k_cache, v_cache)
     if k_new.dim() == 3:
         k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
     k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_kv_append_rotary_raw(C.byref(desc), _ptr(k_new), _ptr(v_new), k_new.shape[0],
+                                               k_new.shape[1], _ptr(seq), _ptr(idx), C.byref(rot),
+                                               C.c_void_p(_stream(stream))))
+        return
     check(lib().vattn_kv_append_raw(C.byref(desc), _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
                                     _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
 
@@ -323,12 +344,19 @@ def decode_num_splits(batch: int, n_kv_heads: int, max_seqlen: int) -> int:
 
 
 def prefill_attention_raw(q, k_cache, v_cache, req_slot: int, kv_len: int, causal=True,
-                          softmax_scale=None, out=None, stream=None):
+                          softmax_scale=None, out=None, stream=None, rotary_cos=None, rotary_sin=None,
+                          rotary_interleaved: bool = False):
     desc = cache_desc(k_cache, v_cache)
     q = _bf16(q, "q")
     out = torch.empty_like(q) if out is None else out
     n_q, hq, d = q.shape
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
+    rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    if rot is not None:
+        check(lib().vattn_prefill_rotary_raw(C.byref(desc), _ptr(q), _ptr(out), n_q, hq, int(req_slot), int(kv_len),
+                                             float(scale), int(bool(causal)), C.byref(rot),
+                                             C.c_void_p(_stream(stream))))
+        return out
     check(lib().vattn_prefill_raw(C.byref(desc), _ptr(q), _ptr(out), n_q, hq, int(req_slot), int(kv_len),
                                   float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
     return out

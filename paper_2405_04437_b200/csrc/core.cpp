@@ -1787,6 +1787,34 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
   });
 }
 
+vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new, const void* v_new,
+                                    int32_t batch, int32_t n_new, const int32_t* seqlens,
+                                    const int32_t* batch_idx, const vattn_rotary* rotary, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    const vattn::CacheView v = h->m->layer_view(layer);
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
+                            (cudaStream_t)stream, &rot);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
+vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
+                                  int32_t slot, int32_t kv_len, float scale, int32_t causal,
+                                  const vattn_rotary* rotary, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    const vattn::CacheView v = h->m->layer_view(layer);
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
+                          causal != 0, (cudaStream_t)stream, &rot);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
 vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q, const void* k_new,
                                         const void* v_new, void* out, int32_t batch,
                                         const int32_t* cache_seqlens, const int32_t* batch_idx, float scale,

@@ -100,7 +100,7 @@ GatherSink gather_sink(vattn_gather_t* g, int hq_local, int batch, int head_dim)
 // Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
 void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,
                       const void* v_new, int batch, int n_new, const int32_t* seqlens,
-                      const int32_t* batch_idx, cudaStream_t st);
+                      const int32_t* batch_idx, cudaStream_t st, const Rotary* rot = nullptr);
 void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                    int batch, int hq, const int32_t* seqlens, const int32_t* batch_idx,
                    float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st,
@@ -108,6 +108,6 @@ void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const voi
                    const GatherSink* sink = nullptr, const Rotary* rot = nullptr);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
-                    cudaStream_t st);
+                    cudaStream_t st, const Rotary* rot = nullptr);
 
 }  // namespace vattn

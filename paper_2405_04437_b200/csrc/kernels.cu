@@ -24,6 +24,7 @@
 
 namespace vattn {
 
+
 // ------------------------------------------------------------------------------ KV append
 // One 16-byte chunk per thread-iteration; rows are contiguous in both source and destination
 // so warps issue fully coalesced 128-bit loads and stores.
@@ -37,6 +38,8 @@ struct AppendParams {
   int64_t slot_stride, token_stride;
   int32_t n_new, chunks_per_row;
   int64_t total_chunks;  // batch * n_new * chunks_per_row
+  Rotary rot;            // rotary of k at its position (cos == nullptr: plain copy)
+  int32_t d;             // head dim (chunks per head = d / 8)
 };
 
 __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
@@ -56,6 +59,16 @@ __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
                  : "l"(p.v_src + c));
+    if (p.rot.cos) {
+      const int cc = within % (p.d / 8);          // chunk within this head
+      if (cc * 8 < p.rot.dim) {
+        const int half = p.rot.dim / 16;
+        const int pc = p.rot.interleaved ? cc : (cc < half ? cc + half : cc - half);
+        const uint4 w = __ldg(p.k_src + c - cc + pc);
+        const int64_t t = pos * (p.rot.dim / 2);
+        kv = ptx::rotary_chunk(kv, w, cc, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
+      }
+    }
     *reinterpret_cast<uint4*>(p.k_dst + dst) = kv;
     *reinterpret_cast<uint4*>(p.v_dst + dst) = vv;
   }
@@ -117,37 +130,6 @@ struct DecodeParams {
   Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
 };
 
-// Rotate one 16-byte chunk (8 bf16, dims [8c, 8c+8)) at the position whose tables start at
-// cosr / sinr.  `partner` is the chunk holding the other element of each pair in the NeoX layout
-// (c -/+ dim/16); GPT-J pairs sit inside the chunk.  fp32 math, one bf16 rounding.
-__device__ __forceinline__ uint4 rotary_chunk(uint4 own, uint4 partner, int c, const float* cosr,
-                                              const float* sinr, int dim, bool interleaved) {
-  if (c * 8 >= dim) return own;
-  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&own);
-  const __nv_bfloat16* y = reinterpret_cast<const __nv_bfloat16*>(&partner);
-  uint4 out;
-  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
-  const int half = dim / 2;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int d = c * 8 + e;
-    float r;
-    if (interleaved) {
-      const int i = d >> 1;
-      const float cs = __ldg(cosr + i), sn = __ldg(sinr + i);
-      const float x1 = __bfloat162float(x[e & ~1]), x2 = __bfloat162float(x[e | 1]);
-      r = (e & 1) ? x1 * sn + x2 * cs : x1 * cs - x2 * sn;
-    } else if (d < half) {
-      const float cs = __ldg(cosr + d), sn = __ldg(sinr + d);
-      r = __bfloat162float(x[e]) * cs - __bfloat162float(y[e]) * sn;
-    } else {
-      const float cs = __ldg(cosr + d - half), sn = __ldg(sinr + d - half);
-      r = __bfloat162float(y[e]) * sn + __bfloat162float(x[e]) * cs;
-    }
-    o[e] = __float2bfloat16(r);
-  }
-  return out;
-}
 
 // ---- fused head all-gather epilogue (gather.cu owns the buffers and the wait) ----
 // Output row (b, local head h) goes to row (b, head_off + h) of every rank's full output: one
@@ -278,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
         const int pc = p.rot.interleaved ? c : (c < rhalf_chunks ? c + rhalf_chunks : c - rhalf_chunks);
         const uint4 w = *reinterpret_cast<const uint4*>(qrow + pc * 8);
         const int64_t t = (int64_t)pos_new * (p.rot.dim / 2);
-        v = rotary_chunk(v, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
+        v = ptx::rotary_chunk(v, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
       }
     }
     *reinterpret_cast<uint4*>(qs + r * L::kQStride + c * 8) = v;
@@ -320,7 +302,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant_
           const int pc = p.rot.interleaved ? c : (c < rhalf_chunks ? c + rhalf_chunks : c - rhalf_chunks);
           const uint4 w = *reinterpret_cast<const uint4*>(p.k_new + src + pc * 8);
           const int64_t t = (int64_t)pos_new * (p.rot.dim / 2);
-          val = rotary_chunk(val, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
+          val = ptx::rotary_chunk(val, w, c, p.rot.cos + t, p.rot.sin + t, p.rot.dim, p.rot.interleaved != 0);
         }
         const uint32_t a = ptx::swz128((is_v ? vs : ks) + (c >> 3) * L::kHalfBytes, r, c & 7);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(val.x), "r"(val.y), "r"(val.z),
@@ -579,11 +561,17 @@ static void check_view(const CacheView& v) {
 
 void launch_kv_append(KernelState*, int, const CacheView& v, const void* k_new, const void* v_new,
                       int batch, int n_new, const int32_t* seqlens, const int32_t* batch_idx,
-                      cudaStream_t st) {
+                      cudaStream_t st, const Rotary* rot) {
   check_view(v);
   if (batch <= 0 || n_new <= 0) return;
   const int64_t row_bytes = (int64_t)v.hkv * v.d * 2;
-  AppendParams p;
+  AppendParams p{};
+  p.d = v.d;
+  if (rot && rot->cos) {
+    if (!rot->sin || rot->dim <= 0 || rot->dim % 16 || rot->dim > v.d)
+      throw Fail(VATTN_VALUE_ERROR, "rotary_dim must be a positive multiple of 16 and <= head_dim");
+    p.rot = *rot;
+  }
   p.k_src = reinterpret_cast<const uint4*>(k_new);
   p.v_src = reinterpret_cast<const uint4*>(v_new);
   p.k_dst = reinterpret_cast<char*>(v.k_base);
@@ -808,6 +796,17 @@ vattn_status vattn_decode_append_raw(const vattn_cache_desc* c, const void* q, c
     const vattn::CacheView v = vattn::view_from_desc(c);
     vattn::launch_decode(nullptr, -1, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
+  });
+}
+
+vattn_status vattn_kv_append_rotary_raw(const vattn_cache_desc* c, const void* k_new, const void* v_new,
+                                        int32_t batch, int32_t n_new, const int32_t* seqlens,
+                                        const int32_t* batch_idx, const vattn_rotary* rotary, void* stream) {
+  return kguard([&] {
+    if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_kv_append(nullptr, -1, vattn::view_from_desc(c), k_new, v_new, batch, n_new, seqlens,
+                            batch_idx, (cudaStream_t)stream, &rot);
   });
 }
 

@@ -58,6 +58,10 @@ struct Params {
   // paged comparison variant: K/V tiles gathered block by block through a block table
   const int32_t* block_table;
   int block_size, box_tokens;
+  // rotary of the query rows at their absolute positions q_off + i (k is rotated at append)
+  const float* rot_cos;
+  const float* rot_sin;
+  int rot_dim, rot_inter;
 };
 
 // ---- tcgen05 wrappers -------------------------------------------------------------------
@@ -253,6 +257,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   uint64_t* s_full = bars + 7;            // [2] tiles A, B
   uint64_t* p_full = bars + 9;            // [2]
   uint64_t* o_final = bars + 11;          // [2]
+  uint64_t* q_ready = bars + 13;          // rotary: both Q tiles rotated in shared memory
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -275,6 +280,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       ptx::mbar_init(&p_full[x], kBM);
       ptx::mbar_init(&o_final[x], 1);
     }
+    ptx::mbar_init(q_ready, 2 * kBM);
     ptx::fence_mbar_init();
   }
   if (warp == 9) {
@@ -365,6 +371,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
           mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
       };
       ptx::mbar_wait(q_full, 0);
+      if (p.rot_cos) ptx::mbar_wait(q_ready, 0);
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % kStages;
         ptx::mbar_wait(&k_full[s], (j / kStages) & 1);
@@ -407,6 +414,33 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const uint32_t tS = lane_base + x * 128;
     const uint32_t tO = lane_base + 256 + x * D;
     float m_run = -INFINITY, l_run = 0.f;
+    if (p.rot_cos && n_kv > 0) {
+      // rotary: each thread rotates its own query row of tile x in the swizzled smem tile, then
+      // hands the tiles to the async proxy (tcgen05.mma reads Q from smem) and signals the issuer
+      ptx::mbar_wait(q_full, 0);
+      if (qpos < p.n_q) {
+        const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
+        const int64_t t = (int64_t)(qpos + p.q_off) * (p.rot_dim / 2);
+        const int nch = p.rot_dim / 8, half = p.rot_dim / 16;
+        for (int cc = 0; cc < nch; ++cc) {
+          if (!p.rot_inter && cc >= half) break;     // NeoX: the first-half chunk rotates both
+          const int pc = p.rot_inter ? cc : cc + half;
+          const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
+          const uint32_t a1 = ptx::swz128(qt + (pc >> 3) * kHalf, row, pc & 7);
+          uint4 v0, v1;
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(a0));
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(a1));
+          const uint4 r0 = ptx::rotary_chunk(v0, v1, cc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, p.rot_inter != 0);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(r0.x), "r"(r0.y), "r"(r0.z), "r"(r0.w));
+          if (!p.rot_inter) {
+            const uint4 r1 = ptx::rotary_chunk(v1, v0, pc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, false);
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(r1.x), "r"(r1.y), "r"(r1.z), "r"(r1.w));
+          }
+        }
+      }
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive(q_ready);
+    }
     for (int j = 0; j < n; ++j) {
       if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
       ptx::mbar_wait(&s_full[x], j & 1);
@@ -602,7 +636,7 @@ static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const 
 }
 
 void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* out, int n_q, int hq,
-                    int slot, int kv_len, float scale, bool causal, cudaStream_t st) {
+                    int slot, int kv_len, float scale, bool causal, cudaStream_t st, const Rotary* rot) {
   if (v.d != 128 && v.d != 64) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 64 and 128");
   const int D = v.d;
   if (hq % v.hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
@@ -625,7 +659,15 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   const uint64_t slot_off = (uint64_t)slot * (uint64_t)v.slot_stride;
   const CUtensorMap kmap = make_map(reinterpret_cast<void*>(v.k_base + slot_off), 3, kd, ks, kb);
   const CUtensorMap vmap = make_map(reinterpret_cast<void*>(v.v_base + slot_off), 3, kd, ks, kb);
-  pf::Params p;
+  pf::Params p{};
+  if (rot && rot->cos) {
+    if (!rot->sin || rot->dim <= 0 || rot->dim % 16 || rot->dim > D)
+      throw Fail(VATTN_VALUE_ERROR, "rotary_dim must be a positive multiple of 16 and <= head_dim");
+    p.rot_cos = rot->cos;
+    p.rot_sin = rot->sin;
+    p.rot_dim = rot->dim;
+    p.rot_inter = rot->interleaved;
+  }
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.n_q = n_q;
   p.hq = hq;
@@ -735,6 +777,24 @@ extern "C" int vattn_debug_prefill_trace(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, vattn::pf::g_pf_trace, sizeof(vattn::pf::g_pf_trace));
 }
 #endif
+
+extern "C" vattn_status vattn_prefill_rotary_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
+                                                 int32_t hq, int32_t slot, int32_t kv_len, float scale,
+                                                 int32_t causal, const vattn_rotary* rotary, void* stream) {
+  try {
+    if (!rotary) throw vattn::Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    vattn::launch_prefill(nullptr, -1, vattn::view_from_desc(c), q, out, n_q, hq, slot, kv_len, scale,
+                          causal != 0, (cudaStream_t)stream, &rot);
+    return VATTN_OK;
+  } catch (const vattn::Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
+}
 
 extern "C" vattn_status vattn_prefill_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                           int32_t hq, int32_t slot, int32_t kv_len, float scale,

@@ -119,5 +119,37 @@ __device__ __forceinline__ uint32_t swz128(uint32_t base, int r, int c) {
   return base + r * 128 + ((c ^ (r & 7)) << 4);
 }
 
+// Rotate one 16-byte chunk (8 bf16, dims [8c, 8c+8)) at the position whose tables start at
+// cosr / sinr.  `partner` is the chunk holding the other element of each pair in the NeoX layout
+// (c -/+ dim/16); GPT-J pairs sit inside the chunk.  fp32 math, one bf16 rounding.
+__device__ __forceinline__ uint4 rotary_chunk(uint4 own, uint4 partner, int c, const float* cosr,
+                                              const float* sinr, int dim, bool interleaved) {
+  if (c * 8 >= dim) return own;
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&own);
+  const __nv_bfloat16* y = reinterpret_cast<const __nv_bfloat16*>(&partner);
+  uint4 out;
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&out);
+  const int half = dim / 2;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int d = c * 8 + e;
+    float r;
+    if (interleaved) {
+      const int i = d >> 1;
+      const float cs = __ldg(cosr + i), sn = __ldg(sinr + i);
+      const float x1 = __bfloat162float(x[e & ~1]), x2 = __bfloat162float(x[e | 1]);
+      r = (e & 1) ? x1 * sn + x2 * cs : x1 * cs - x2 * sn;
+    } else if (d < half) {
+      const float cs = __ldg(cosr + d), sn = __ldg(sinr + d);
+      r = __bfloat162float(x[e]) * cs - __bfloat162float(y[e]) * sn;
+    } else {
+      const float cs = __ldg(cosr + d - half), sn = __ldg(sinr + d - half);
+      r = __bfloat162float(y[e]) * sn + __bfloat162float(x[e]) * cs;
+    }
+    o[e] = __float2bfloat16(r);
+  }
+  return out;
+}
+
 }  // namespace ptx
 }  // namespace vattn

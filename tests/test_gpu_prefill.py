@@ -158,3 +158,81 @@ def test_tiny_config_serving_loop_on_gpu():
     m = run(recs, g, mode="overlapped", clock="wall", pool_bytes=64 << 20, eager_groups=1)
     s = m.summary()
     assert s["completed_requests"] == 4 and s["generated_tokens"] == 14
+
+
+@pytest.mark.parametrize("d,rd,inter,n_q,kv_len", [(128, 128, False, 1000, 1000), (128, 64, True, 200, 1224),
+                                                   (64, 64, True, 384, 384), (64, 32, False, 129, 700)])
+def test_rotary_append_and_prefill_match_oracle(d, rd, inter, n_q, kv_len):
+    """Rotary at append (k row i cached rotated at cache_seqlens + i) and inside the tcgen05
+    prefill (query row i rotated in shared memory at kv_len - n_q + i) vs the fp32 oracle."""
+    from oracle.attention import rotary_ref
+    from paper_2405_04437_b200.attention import kv_append_raw, prefill_attention_raw
+
+    dev = _cuda()
+    hq, hkv = 16, 4
+    gen = torch.Generator().manual_seed(21)
+    kn = torch.randn(1, kv_len, hkv, d, generator=gen).to(torch.bfloat16)
+    vn = torch.randn(1, kv_len, hkv, d, generator=gen).to(torch.bfloat16)
+    q = torch.randn(n_q, hq, d, generator=gen).to(torch.bfloat16)
+    ang = torch.arange(2048, dtype=torch.float32)[:, None] / (10000 ** (torch.arange(0, rd, 2) / rd))[None, :]
+    cos, sin = ang.cos(), ang.sin()
+    L = (kv_len + 127) // 128 * 128 + 128
+    kc = torch.zeros(2, L, hkv, d, dtype=torch.bfloat16, device=dev)
+    vc = torch.zeros_like(kc)
+    kv_append_raw(kc, vc, kn.to(dev), vn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                  torch.tensor([1], dtype=torch.int32, device=dev), rotary_cos=cos.to(dev), rotary_sin=sin.to(dev),
+                  rotary_interleaved=inter)
+    out = prefill_attention_raw(q.to(dev), kc, vc, 1, kv_len, rotary_cos=cos.to(dev), rotary_sin=sin.to(dev),
+                                rotary_interleaved=inter)
+    torch.cuda.synchronize()
+    pos_k = torch.arange(kv_len, dtype=torch.int32)
+    kr = rotary_ref(kn[0], cos, sin, pos_k, inter).to(torch.bfloat16)        # [kv_len, hkv, d]
+    assert torch.allclose(kc[1, :kv_len].cpu().float(), kr.float(), rtol=1e-2, atol=1e-2)
+    assert torch.equal(vc[1, :kv_len].cpu(), vn[0])
+    qr = rotary_ref(q, cos, sin, torch.arange(kv_len - n_q, kv_len, dtype=torch.int32), inter).to(torch.bfloat16)
+    ref = prefill_ref(qr, kr, vn[0])
+    assert max_rel_err(out.cpu(), ref) <= TOL
+
+
+def test_rotary_manager_backed_prefill_then_decode():
+    """Rotary through the manager (VMM cache): prompt appended rotated, prefill rotates q inside
+    the kernel, then the fused decode appends + rotates the next token; both checked vs oracle."""
+    from oracle.attention import decode_ref, rotary_ref
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention_append, kv_append, prefill_attention
+
+    dev = _cuda()
+    g = ModelGeometry(1, 4, 128, 2, max_context=4096, max_batch=2, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=2 << 20, pool_bytes=64 << 20))
+    r = mgr.alloc_reqid()
+    S = 777
+    lens = [0, 0]
+    lens[r] = S + 1
+    assert mgr.step(lens).ok
+    gen = torch.Generator().manual_seed(22)
+    kn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
+    vn = torch.randn(1, S, 4, 128, generator=gen).to(torch.bfloat16)
+    q = torch.randn(S, 32, 128, generator=gen).to(torch.bfloat16)
+    ang = torch.arange(4096, dtype=torch.float32)[:, None] / (10000 ** (torch.arange(0, 128, 2) / 128))[None, :]
+    cos, sin = ang.cos(), ang.sin()
+    rot = dict(rotary_cos=cos.to(dev), rotary_sin=sin.to(dev))
+    idx = torch.tensor([r], dtype=torch.int32, device=dev)
+    kv_append(mgr, 0, kn.to(dev), vn.to(dev), torch.zeros(1, dtype=torch.int32, device=dev), idx, **rot)
+    out = prefill_attention(mgr, 0, q.to(dev), r, **rot)
+    pos = torch.arange(S, dtype=torch.int32)
+    kr = rotary_ref(kn[0], cos, sin, pos).to(torch.bfloat16)
+    qr = rotary_ref(q, cos, sin, pos).to(torch.bfloat16)
+    torch.cuda.synchronize()
+    assert max_rel_err(out.cpu(), prefill_ref(qr, kr, vn[0])) <= TOL
+    q1 = torch.randn(1, 32, 128, generator=gen).to(torch.bfloat16)
+    k1 = torch.randn(1, 4, 128, generator=gen).to(torch.bfloat16)
+    v1 = torch.randn(1, 4, 128, generator=gen).to(torch.bfloat16)
+    o1 = decode_attention_append(mgr, 0, q1.to(dev), k1.to(dev), v1.to(dev),
+                                 torch.tensor([S], dtype=torch.int32, device=dev), idx, **rot)
+    p1 = torch.tensor([S], dtype=torch.int32)
+    kc = torch.cat([kr, rotary_ref(k1, cos, sin, p1).to(torch.bfloat16)], 0).unsqueeze(0)
+    vc = torch.cat([vn[0], v1], 0).unsqueeze(0)
+    ref = decode_ref(rotary_ref(q1, cos, sin, p1).to(torch.bfloat16), kc, vc, torch.tensor([S + 1], dtype=torch.int32))
+    torch.cuda.synchronize()
+    assert max_rel_err(o1.cpu(), ref) <= TOL
+    mgr.close()
