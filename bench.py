@@ -547,6 +547,44 @@ def extra_prefill(local):
             "map_16k_prompt_ms": map_ms, **paged}
 
 
+def extra_long_prefill(local, lengths=(4096, 16384, 65536, 131072)):
+    """Prefill at growing context (the paper's prefill-throughput figure, PAPER.md:549, 653-660:
+    attention dominates from 16K up, where the non-paged kernel's advantage shows): Yi-6B heads
+    (32 Q / 4 KV, D 128), causal, one layer, the tcgen05 kernel on a contiguous slot vs the same
+    kernel gathering K/V through a block table (blocks of 16 and 256)."""
+    import torch
+
+    from paper_2405_04437_b200.attention import prefill_attention_paged, prefill_attention_raw
+
+    dev = torch.device("cuda", local)
+    out = {}
+    for S in lengths:
+        gen = torch.Generator(device=dev).manual_seed(S)
+        k = torch.randn(1, S, 4, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        v = torch.randn_like(k)
+        q = torch.randn(S, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        o = torch.empty_like(q)
+        it = 10 if S <= 16384 else 3
+        ms = _time_ms(lambda: prefill_attention_raw(q, k, v, 0, S, out=o), iters=it, warm=2)
+        flops = 2.0 * S * S * 128 * 32
+        row = {"ms": ms, "tflops": flops / (ms * 1e-3) / 1e12}
+        for bs in (16, 256):
+            nb = S // bs
+            perm = torch.randperm(nb, device=dev, generator=gen)
+            kp = torch.empty(nb, bs, 4, 128, device=dev, dtype=torch.bfloat16)
+            vp = torch.empty_like(kp)
+            kp[perm] = k[0].view(nb, bs, 4, 128)
+            vp[perm] = v[0].view(nb, bs, 4, 128)
+            bt = perm.to(torch.int32)
+            pms = _time_ms(lambda: prefill_attention_paged(q, kp, vp, bt, S, out=o), iters=it, warm=2)
+            row[f"paged_bs{bs}_slowdown"] = pms / ms
+            del kp, vp
+        out[f"S{S}"] = row
+        del k, v, q, o
+        torch.cuda.empty_cache()
+    return out
+
+
 def extra_paged(local):
     """Contiguous (vAttention) vs paged-layout decode kernel on identical K/V (L8 layer)."""
     import torch
@@ -979,6 +1017,7 @@ def main(argv=None):
         if not args.no_extras and world == 1:
             extras = {}
             for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
+                             ("long_prefill", extra_long_prefill),
                              ("paged_vs_contiguous", extra_paged),
                              ("y34_shards", extra_y34_shards), ("l8_shards", extra_l8_shards),
                              ("libraries", extra_libraries),
