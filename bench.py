@@ -621,6 +621,53 @@ def extra_paged(local):
     return res
 
 
+def extra_long_decode(local, cases=((1, 32768), (1, 131072), (8, 32768), (8, 131072), (16, 65536))):
+    """Decode at long contexts (the paper's decode-attention latency table):
+    Llama-3-8B heads (32 Q / 8 KV, D 128), batch B x context L, contiguous split-K kernel vs the
+    same kernel through a block table (16 / 256).  Four cache copies are cycled so every launch
+    reads HBM.  Latency in µs and HBM GB/s."""
+    import torch
+
+    from paper_2405_04437_b200.attention import decode_attention_paged, decode_attention_raw, decode_num_splits
+
+    dev = torch.device("cuda", local)
+    hq, hkv, d = 32, 8, 128
+    out = {}
+    for B, L in cases:
+        gen = torch.Generator(device=dev).manual_seed(B * 7 + L)
+        ncopy = 2 if B * L >= 8 * 131072 else 4
+        kv = [(torch.randn(B, L, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16),
+               torch.randn(B, L, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)) for _ in range(ncopy)]
+        q = torch.randn(B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+        seq = torch.full((B,), L, dtype=torch.int32, device=dev)
+        byt = 2 * B * L * hkv * d * 2
+        cnt = [0]
+
+        def contiguous():
+            k, v = kv[cnt[0] % ncopy]
+            cnt[0] += 1
+            decode_attention_raw(q, k, v, seq)
+
+        us = _time_ms(contiguous, iters=8) * 1e3
+        row = {"us": us, "gbs": byt / (us * 1e-6) / 1e9, "num_splits": decode_num_splits(B, hkv, L)}
+        for bs in (16, 256):
+            nb = L // bs
+            perm = torch.randperm(B * nb, device=dev, generator=gen)
+            k, v = kv[0]
+            kp = torch.empty_like(k).view(B * nb, bs, hkv, d)
+            vp = torch.empty_like(v).view(B * nb, bs, hkv, d)
+            kp[perm] = k.view(B * nb, bs, hkv, d)
+            vp[perm] = v.view(B * nb, bs, hkv, d)
+            bt = perm.view(B, nb).to(torch.int32)
+            pus = _time_ms(lambda: decode_attention_paged(q, kp, vp, bt, seq), iters=8) * 1e3
+            row[f"paged_bs{bs}_slowdown"] = pus / us
+            del kp, vp
+        out[f"B{B}_L{L}"] = row
+        del kv
+        torch.cuda.empty_cache()
+    return out
+
+
 def extra_libraries(local):
     """Library kernels on identical inputs, for context (not on the product path).
     * flash-attn 2.8.3: the kernels vAttention runs unmodified.
@@ -1018,7 +1065,7 @@ def main(argv=None):
             extras = {}
             for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
                              ("long_prefill", extra_long_prefill),
-                             ("paged_vs_contiguous", extra_paged),
+                             ("paged_vs_contiguous", extra_paged), ("long_decode", extra_long_decode),
                              ("y34_shards", extra_y34_shards), ("l8_shards", extra_l8_shards),
                              ("libraries", extra_libraries),
                              ("serving", extra_serving)):
