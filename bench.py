@@ -621,6 +621,38 @@ def extra_paged(local):
     return res
 
 
+def extra_varlen_prefill(local, cases=((16, 512), (8, 2048), (4, 3072))):
+    """Several prompts' prefill attention (Llama-3-8B heads, causal, one layer): one launch per
+    request vs one varlen launch for all of them (short prompts alone leave most SMs idle)."""
+    import torch
+
+    from paper_2405_04437_b200.attention import prefill_attention_raw, prefill_attention_varlen_raw
+
+    dev = torch.device("cuda", local)
+    out = {}
+    for n_req, S in cases:
+        gen = torch.Generator(device=dev).manual_seed(n_req * S)
+        k = torch.randn(n_req, S, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        v = torch.randn_like(k)
+        q = torch.randn(n_req * S, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        o = torch.empty_like(q)
+        qs = [q[i * S:(i + 1) * S] for i in range(n_req)]
+        os_ = [o[i * S:(i + 1) * S] for i in range(n_req)]
+
+        def per_request():
+            for i in range(n_req):
+                prefill_attention_raw(qs[i], k, v, i, S, out=os_[i])
+
+        t_each = _time_ms(per_request, iters=10)
+        t_var = _time_ms(lambda: prefill_attention_varlen_raw(q, k, v, [S] * n_req, list(range(n_req)), out=o),
+                         iters=10)
+        flops = n_req * 2.0 * S * S * 128 * 32
+        out[f"{n_req}x{S}"] = {"per_request_ms": t_each, "varlen_ms": t_var, "speedup": t_each / t_var,
+                               "varlen_tflops": flops / (t_var * 1e-3) / 1e12}
+        del k, v, q, o
+    return out
+
+
 def extra_long_decode(local, cases=((1, 32768), (1, 131072), (8, 32768), (8, 131072), (16, 65536))):
     """Decode at long contexts (the paper's decode-attention latency table):
     Llama-3-8B heads (32 Q / 8 KV, D 128), batch B x context L, contiguous split-K kernel vs the
@@ -1064,7 +1096,7 @@ def main(argv=None):
         if not args.no_extras and world == 1:
             extras = {}
             for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
-                             ("long_prefill", extra_long_prefill),
+                             ("long_prefill", extra_long_prefill), ("varlen_prefill", extra_varlen_prefill),
                              ("paged_vs_contiguous", extra_paged), ("long_decode", extra_long_decode),
                              ("y34_shards", extra_y34_shards), ("l8_shards", extra_l8_shards),
                              ("libraries", extra_libraries),

@@ -277,6 +277,13 @@ vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new
 vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                                   int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
                                   const vattn_rotary* rotary, void* stream);
+/* Several requests' prefills in one launch (flash_attn_varlen_func-style packed queries): host
+ * arrays of n_req entries; request i's query rows are q[q_start[i] .. + n_q[i]] (packed
+ * [total, Hq, D]), attending causally over rows [0, kv_len[i]) of slot slots[i]; outputs at the
+ * same packed rows.  The per-call schedule is uploaded on `stream` (not graph-capturable). */
+vattn_status vattn_prefill_varlen(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_req,
+                                  const int32_t* q_start, const int32_t* n_q, const int32_t* slots,
+                                  const int32_t* kv_len, float scale, int32_t causal, void* stream);
 /* causal (bottom-right) prefill of q [n_q, Hq, D] against slot rows [0, kv_len). */
 vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                            int32_t req_slot, int32_t kv_len, float scale, int32_t causal,
@@ -321,6 +328,10 @@ vattn_status vattn_kv_append_rotary_raw(const vattn_cache_desc* c, const void* k
 vattn_status vattn_prefill_rotary_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                       int32_t n_q_heads, int32_t req_slot, int32_t kv_len, float scale,
                                       int32_t causal, const vattn_rotary* rotary, void* stream);
+vattn_status vattn_prefill_varlen_raw(const vattn_cache_desc* c, const void* q, void* out,
+                                      int32_t n_q_heads, int32_t n_req, const int32_t* q_start,
+                                      const int32_t* n_q, const int32_t* slots, const int32_t* kv_len,
+                                      float scale, int32_t causal, void* stream);
 /* Paged-layout comparison kernel (PagedAttention block table; PAPER.md:602 block sizes):
  * pools [num_blocks, block_size, Hkv, D], block_table [batch, max_blocks] int32. */
 vattn_status vattn_decode_paged(const void* q, const void* k_pool, const void* v_pool,

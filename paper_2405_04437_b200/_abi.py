@@ -119,6 +119,9 @@ SIGNATURES = {
     "vattn_kv_append_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, C.POINTER(RotaryC), c_vp]),
     "vattn_kv_append_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                            C.POINTER(RotaryC), c_vp]),
+    "vattn_prefill_varlen": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, P_i32, P_i32, P_i32, P_i32, c_f32, c_i32, c_vp]),
+    "vattn_prefill_varlen_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, P_i32, P_i32, P_i32, P_i32,
+                                         c_f32, c_i32, c_vp]),
     "vattn_prefill_rotary": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_f32, c_i32,
                                      C.POINTER(RotaryC), c_vp]),
     "vattn_prefill_rotary_raw": (c_i32, [C.POINTER(CacheDesc), c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_f32,

@@ -209,6 +209,50 @@ def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None
     return out
 
 
+def _varlen_arrays(q, q_lens, req_ids, kv_lens):
+    n = len(q_lens)
+    if len(req_ids) != n or (kv_lens is not None and len(kv_lens) != n):
+        raise ValueError("q_lens, req_ids and kv_lens must have one entry per request")
+    kv_lens = list(q_lens) if kv_lens is None else list(kv_lens)
+    starts, acc = [], 0
+    for m in q_lens:
+        starts.append(acc)
+        acc += int(m)
+    if acc != q.shape[0]:
+        raise ValueError(f"packed q has {q.shape[0]} rows but q_lens sum to {acc}")
+    arr = lambda xs: (C.c_int32 * max(1, n))(*[int(x) for x in xs])  # noqa: E731
+    return n, arr(starts), arr(q_lens), arr(req_ids), arr(kv_lens)
+
+
+def prefill_attention_varlen(mgr, layer: int, q, q_lens, req_ids, kv_lens=None, causal=True, softmax_scale=None,
+                             out=None, stream=None):
+    """Prefill of several requests in ONE launch (flash_attn_varlen_func-style): q [sum(q_lens),
+    Hq, D] packs each request's query rows in order; request i attends (bottom-right causal)
+    over rows [0, kv_lens[i]) of slot req_ids[i] (default kv_lens = q_lens)."""
+    _need_cuda(q)
+    q = _bf16(q, "q")
+    out = torch.empty_like(q) if out is None else out
+    n, st, nq, sl, kl = _varlen_arrays(q, q_lens, req_ids, kv_lens)
+    if CHECK_BOUNDS:
+        check_bounds(mgr, list(kv_lens if kv_lens is not None else q_lens), list(req_ids))
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    check(lib().vattn_prefill_varlen(mgr._h, layer, _ptr(q), _ptr(out), n, st, nq, sl, kl, float(scale),
+                                     int(bool(causal)), C.c_void_p(_stream(stream))))
+    return out
+
+
+def prefill_attention_varlen_raw(q, k_cache, v_cache, q_lens, slots, kv_lens=None, causal=True, softmax_scale=None,
+                                 out=None, stream=None):
+    desc = cache_desc(k_cache, v_cache)
+    q = _bf16(q, "q")
+    out = torch.empty_like(q) if out is None else out
+    n, st, nq, sl, kl = _varlen_arrays(q, q_lens, slots, kv_lens)
+    scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    check(lib().vattn_prefill_varlen_raw(C.byref(desc), _ptr(q), _ptr(out), q.shape[1], n, st, nq, sl, kl,
+                                         float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
+    return out
+
+
 # ------------------------------------------------------------------ standalone ops
 def cache_desc(k_cache, v_cache) -> _abi.CacheDesc:
     """Descriptor of caller-owned token-major caches [slots, tokens, Hkv, D] (any slot/token

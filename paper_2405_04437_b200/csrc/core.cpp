@@ -1801,6 +1801,19 @@ vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new
   });
 }
 
+vattn_status vattn_prefill_varlen(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_req,
+                                  const int32_t* q_start, const int32_t* n_q, const int32_t* slots,
+                                  const int32_t* kv_len, float scale, int32_t causal, void* stream) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] {
+    if (n_req > 0 && (!q_start || !n_q || !slots || !kv_len)) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    const vattn::CacheView v = h->m->layer_view(layer);
+    vattn::launch_prefill_varlen(v, q, out, h->m->hq_local(), n_req, q_start, n_q, slots, kv_len, scale,
+                                 causal != 0, (cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream);
+  });
+}
+
 vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void* out, int32_t n_q,
                                   int32_t slot, int32_t kv_len, float scale, int32_t causal,
                                   const vattn_rotary* rotary, void* stream) {

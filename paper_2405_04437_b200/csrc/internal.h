@@ -106,6 +106,9 @@ void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const voi
                    float scale, int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st,
                    const void* k_new = nullptr, const void* v_new = nullptr,
                    const GatherSink* sink = nullptr, const Rotary* rot = nullptr);
+void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq, int n_req,
+                           const int32_t* q_start, const int32_t* n_q, const int32_t* slots,
+                           const int32_t* kv_len, float scale, bool causal, cudaStream_t st);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
                     cudaStream_t st, const Rotary* rot = nullptr);

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 
@@ -62,6 +64,11 @@ struct Params {
   const float* rot_cos;
   const float* rot_sin;
   int rot_dim, rot_inter;
+  // varlen (several requests per launch): blockIdx.x indexes work = (request, pair), requests
+  // hold (first packed query row, n_q, kv_len), maps hold each request's K and V tensor maps
+  const int4* work;
+  const int4* reqs;
+  const CUtensorMap* maps;
 };
 
 // ---- tcgen05 wrappers -------------------------------------------------------------------
@@ -242,7 +249,7 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
-template <int POLY, bool PAGED = false, int D = 128>
+template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, Params p) {
@@ -261,7 +268,22 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int pair = p.n_pairs - 1 - blockIdx.x;   // heaviest (latest) query rows first
+  int pair = p.n_pairs - 1 - blockIdx.x;   // heaviest (latest) query rows first
+  int q_row0 = 0;                          // packed row of this request's query row 0
+  const CUtensorMap* kmp = &kmap;
+  const CUtensorMap* vmp = &vmap;
+  if constexpr (VARLEN) {                  // work list is sorted heaviest first on the host
+    const int4 w = p.work[blockIdx.x];
+    const int4 r = p.reqs[w.x];
+    pair = w.y;
+    q_row0 = r.x;
+    p.n_q = r.y;
+    p.kv_len = r.z;
+    p.q_off = r.z - r.y;
+    p.out += (int64_t)r.x * p.hq * D;
+    kmp = p.maps + 2 * w.x;
+    vmp = kmp + 1;
+  }
   const int head = blockIdx.y;
   const int kvh = head / p.group;
   const int q0A = pair * 2 * kBM, q0B = q0A + kBM;
@@ -297,13 +319,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     // ===================== TMA producer =====================
     if (lane == 0 && n_kv > 0) {
       ptx::prefetch_tmap(&qmap);
-      ptx::prefetch_tmap(&kmap);
-      ptx::prefetch_tmap(&vmap);
+      ptx::prefetch_tmap(kmp);
+      ptx::prefetch_tmap(vmp);
       ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
 #pragma unroll
       for (int h = 0; h < D / 64; ++h) {
-        ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q0A);
-        ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q0B);
+        ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0A);
+        ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0B);
       }
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % kStages;
@@ -312,12 +334,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         if constexpr (!PAGED) {
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, &kmap, &k_full[s], h * 64, kvh,
+            ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh,
                              j * kBN);
           ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, &vmap, &v_full[s], h * 64, kvh,
+            ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh,
                              j * kBN);
         } else {
           // PagedAttention layout: one TMA box per KV block (4-D map over [D, Hkv, block, n_blocks])
@@ -707,6 +729,102 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
+// Several requests' prefills in one launch (flash_attn_varlen_func-style packing of the query
+// rows): q [total, Hq, D] packed, request i's rows at q_start[i] .. + n_q[i], attending over rows
+// [0, kv_len[i]) of slot slots[i].  The host builds each request's K/V tensor maps (rooted at its
+// slot, extent exactly kv_len) and a work list of (request, 256-row pair) sorted by descending
+// KV tiles, copied to a device buffer on the stream before the launch.
+void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq, int n_req, const int32_t* q_start,
+                           const int32_t* n_q, const int32_t* slots, const int32_t* kv_len, float scale,
+                           bool causal, cudaStream_t st) {
+  if (v.d != 128 && v.d != 64) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 64 and 128");
+  if (hq % v.hkv) throw Fail(VATTN_VALUE_ERROR, "n_q_heads must be a multiple of n_kv_heads");
+  if (n_req <= 0) return;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) % 16)
+    throw Fail(VATTN_UNSUPPORTED, "q/out must be 16-byte aligned");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  check_rt(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+  if (cs != cudaStreamCaptureStatusNone)
+    throw Fail(VATTN_UNSUPPORTED, "varlen prefill uploads a per-call schedule and cannot be graph-captured");
+  const int D = v.d;
+  int total = 0;
+  std::vector<CUtensorMap> maps(2 * (size_t)n_req);
+  std::vector<int4> reqs(n_req);
+  std::vector<std::pair<int, int4>> work;   // (kv tiles, item)
+  for (int i = 0; i < n_req; ++i) {
+    if (slots[i] < 0 || slots[i] >= v.n_slots) throw Fail(VATTN_VALUE_ERROR, "slot out of range");
+    if (kv_len[i] < 0 || kv_len[i] > v.slot_tokens) throw Fail(VATTN_VALUE_ERROR, "kv_len out of range");
+    if (n_q[i] < 0 || q_start[i] < 0) throw Fail(VATTN_VALUE_ERROR, "bad query rows");
+    total = std::max(total, q_start[i] + n_q[i]);
+    const int kvl = std::max(kv_len[i], 1);
+    cuuint64_t kd[3] = {(cuuint64_t)D, (cuuint64_t)v.hkv, (cuuint64_t)kvl};
+    cuuint64_t ks[2] = {(cuuint64_t)D * 2, (cuuint64_t)v.token_stride};
+    cuuint32_t kb[3] = {64, 1, (cuuint32_t)pf::kBN};
+    const uint64_t off = (uint64_t)slots[i] * (uint64_t)v.slot_stride;
+    maps[2 * i] = make_map(reinterpret_cast<void*>(v.k_base + off), 3, kd, ks, kb);
+    maps[2 * i + 1] = make_map(reinterpret_cast<void*>(v.v_base + off), 3, kd, ks, kb);
+    reqs[i] = make_int4(q_start[i], n_q[i], kv_len[i], 0);
+    const int pairs = (n_q[i] + 2 * pf::kBM - 1) / (2 * pf::kBM);
+    for (int pr = 0; pr < pairs; ++pr) {
+      const int q_last = std::min((pr + 1) * 2 * pf::kBM, n_q[i]) - 1;
+      const int last_key = causal ? std::min(kv_len[i] - 1, q_last + kv_len[i] - n_q[i]) : kv_len[i] - 1;
+      work.push_back({last_key < 0 ? 0 : last_key / pf::kBN + 1, make_int4(i, pr, 0, 0)});
+    }
+  }
+  if (work.empty() || total == 0) return;
+  std::stable_sort(work.begin(), work.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  // device copy: [maps (64-B aligned)][reqs][work]
+  const size_t maps_b = maps.size() * sizeof(CUtensorMap), reqs_b = reqs.size() * sizeof(int4),
+               work_b = work.size() * sizeof(int4);
+  std::vector<uint8_t> blob(maps_b + reqs_b + work_b);
+  std::memcpy(blob.data(), maps.data(), maps_b);
+  std::memcpy(blob.data() + maps_b, reqs.data(), reqs_b);
+  for (size_t k = 0; k < work.size(); ++k) std::memcpy(blob.data() + maps_b + reqs_b + k * sizeof(int4), &work[k].second, sizeof(int4));
+  static thread_local void* dbuf = nullptr;
+  static thread_local size_t dcap = 0;
+  if (blob.size() > dcap) {
+    if (dbuf) check_rt(cudaFree(dbuf), "cudaFree(varlen)");
+    dcap = std::max(blob.size(), (size_t)1 << 16);
+    check_rt(cudaMalloc(&dbuf, dcap), "cudaMalloc(varlen)");
+  }
+  // pageable source: the copy is staged before cudaMemcpyAsync returns; stream order keeps the
+  // previous launch's reads of dbuf ahead of this write
+  check_rt(cudaMemcpyAsync(dbuf, blob.data(), blob.size(), cudaMemcpyHostToDevice, st), "varlen params H2D");
+  cuuint64_t qd[3] = {(cuuint64_t)D, (cuuint64_t)hq, (cuuint64_t)total};
+  cuuint64_t qs[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
+  cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
+  const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  pf::Params p{};
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.hq = hq;
+  p.group = hq / v.hkv;
+  p.causal = causal ? 1 : 0;
+  if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.maps = reinterpret_cast<const CUtensorMap*>(dbuf);
+  p.reqs = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b);
+  p.work = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b + reqs_b);
+  dim3 grid((unsigned)work.size(), hq);
+  if (D == 128) {
+    static bool attr = false;
+    if (!attr) {
+      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    pf::PfL<128>::kSmem), "smem attr");
+      attr = true;
+    }
+    pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, p);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    pf::PfL<64>::kSmem), "smem attr");
+      attr = true;
+    }
+    pf::prefill_kernel<0, false, 64, true><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, qmap, qmap, p);
+  }
+  check_rt(cudaGetLastError(), "prefill (varlen) launch");
+}
+
 void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool, int num_blocks,
                           int block_size, int hkv, const int32_t* block_table, int kv_len, void* out,
                           int n_q, int hq, float scale, bool causal, cudaStream_t st) {
@@ -777,6 +895,23 @@ extern "C" int vattn_debug_prefill_trace(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, vattn::pf::g_pf_trace, sizeof(vattn::pf::g_pf_trace));
 }
 #endif
+
+extern "C" vattn_status vattn_prefill_varlen_raw(const vattn_cache_desc* c, const void* q, void* out,
+                                                 int32_t n_q_heads, int32_t n_req, const int32_t* q_start,
+                                                 const int32_t* n_q, const int32_t* slots, const int32_t* kv_len,
+                                                 float scale, int32_t causal, void* stream) {
+  try {
+    vattn::launch_prefill_varlen(vattn::view_from_desc(c), q, out, n_q_heads, n_req, q_start, n_q, slots, kv_len,
+                                 scale, causal != 0, (cudaStream_t)stream);
+    return VATTN_OK;
+  } catch (const vattn::Fail& e) {
+    vattn::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    vattn::set_last_error(e.what());
+    return VATTN_BAD_STATE;
+  }
+}
 
 extern "C" vattn_status vattn_prefill_rotary_raw(const vattn_cache_desc* c, const void* q, void* out, int32_t n_q,
                                                  int32_t hq, int32_t slot, int32_t kv_len, float scale,

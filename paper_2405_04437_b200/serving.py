@@ -190,12 +190,27 @@ class SyntheticModel:
         self.out_dec = torch.empty_like(self.q_dec)
         self.zero = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.dense_model = dense_model
+        self.q_pack = None           # packed queries of an iteration's prompts (varlen prefill)
+        self.out_pack = None
 
     def forward(self, prefills, decodes) -> None:
         """prefills: [(slot, prompt_len)]; decodes: [(slot, ctx)] (ctx includes the new token)."""
-        from .attention import decode_attention_append, kv_append, prefill_attention
+        from .attention import decode_attention_append, kv_append, prefill_attention, prefill_attention_varlen
 
         t = self.t
+        if len(prefills) > 1:   # all new prompts' attention in one varlen launch per layer
+            lens = [n for _, n in prefills]
+            total = sum(lens)
+            if self.q_pack is None or self.q_pack.shape[0] < total:
+                self.q_pack = t.randn(total, self.hq, self.d, device=self.dev, dtype=t.bfloat16)
+                self.out_pack = t.empty_like(self.q_pack)
+            idxs = [t.tensor([slot], dtype=t.int32, device=self.dev) for slot, _ in prefills]
+            for layer in range(self.layers):
+                for (slot, n), idx in zip(prefills, idxs):
+                    kv_append(self.mgr, layer, self.k_pf[:, :n], self.v_pf[:, :n], self.zero, idx)
+                prefill_attention_varlen(self.mgr, layer, self.q_pack[:total], lens, [s_ for s_, _ in prefills],
+                                         out=self.out_pack[:total])
+            prefills = []
         for slot, n in prefills:
             idx = t.tensor([slot], dtype=t.int32, device=self.dev)
             for layer in range(self.layers):
