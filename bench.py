@@ -105,6 +105,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def box_copy_gbs(dev) -> float:
+    """HBM copy bandwidth of THIS GPU, measured the way MEASURED_PEAKS.json's hbm_gbs is
+    (b.copy_(a) over 1 Gi bf16 elements, read + write bytes, best of 10): B200 boxes of the pool
+    differ by ~10 % in HBM throughput, so the line also reports the fraction against this box."""
+    import torch
+
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * (1 << 30) * 2 / (best * 1e-3) / 1e9
+
+
 def dist_setup():
     import torch
     import torch.distributed as dist
@@ -328,6 +349,7 @@ def bench_decode(args, world, rank, local):
     dec_us = statistics.mean(dec_ms) * 1e3
     pk = peaks()
     achieved = dec_bytes / (dec_us * 1e-6) / 1e9
+    box_copy = box_copy_gbs(dev)
     kernel_name = "decode_kernel<128,3,false>" + ("" if args.unfused else " (fused append)")
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
@@ -403,6 +425,7 @@ def bench_decode(args, world, rank, local):
                                       "real_set_access_wall_us", "real_creates", "init_wall_us")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "copy_peak_this_box_gbs": box_copy, "frac_of_this_box_copy_peak": achieved / box_copy,
                      "algorithmic_bytes": dec_bytes, "kernel": kernel_name,
                      "peak_source": pk["source"], "traffic_source": "profiles/ncu_traffic.json (ncu --set full)"},
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
