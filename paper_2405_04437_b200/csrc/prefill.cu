@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <vector>
 #include <cmath>
 #include <cstdlib>
@@ -780,13 +781,17 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   std::memcpy(blob.data(), maps.data(), maps_b);
   std::memcpy(blob.data() + maps_b, reqs.data(), reqs_b);
   for (size_t k = 0; k < work.size(); ++k) std::memcpy(blob.data() + maps_b + reqs_b + k * sizeof(int4), &work[k].second, sizeof(int4));
-  static thread_local void* dbuf = nullptr;
-  static thread_local size_t dcap = 0;
-  if (blob.size() > dcap) {
-    if (dbuf) check_rt(cudaFree(dbuf), "cudaFree(varlen)");
-    dcap = std::max(blob.size(), (size_t)1 << 16);
-    check_rt(cudaMalloc(&dbuf, dcap), "cudaMalloc(varlen)");
+  // one schedule buffer per (thread, device); reused in stream order
+  static thread_local std::map<int, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  check_rt(cudaGetDevice(&dev), "cudaGetDevice");
+  auto& slot = bufs[dev];
+  if (blob.size() > slot.second) {
+    if (slot.first) check_rt(cudaFree(slot.first), "cudaFree(varlen)");
+    slot.second = std::max(blob.size(), (size_t)1 << 16);
+    check_rt(cudaMalloc(&slot.first, slot.second), "cudaMalloc(varlen)");
   }
+  void* dbuf = slot.first;
   // pageable source: the copy is staged before cudaMemcpyAsync returns; stream order keeps the
   // previous launch's reads of dbuf ahead of this write
   check_rt(cudaMemcpyAsync(dbuf, blob.data(), blob.size(), cudaMemcpyHostToDevice, st), "varlen params H2D");
