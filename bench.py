@@ -1057,7 +1057,7 @@ def run_reference(args, world, rank):
         return None
     # the whole job's work (every KV head) on the one host, whatever N is: the host cores do not
     # multiply with the GPU count
-    s = CpuDecodeSample(args.workload, 1)
+    s = CpuDecodeSample(args.workload, 1, batch_frac=8)   # 8 of 64 rows per step keeps the arm to ~1 min
     for _ in range(args.warmup):
         s.step()
     times = [s.step() for _ in range(args.steps)]
