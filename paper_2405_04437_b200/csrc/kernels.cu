@@ -175,7 +175,7 @@ struct DecodeSmem {
 };
 
 template <int D, int STAGES, bool PAGED>
-__global__ void __launch_bounds__(kThreads) decode_kernel(const __grid_constant__ CUtensorMap kmap,
+__global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_constant__ CUtensorMap kmap,
                                                           const __grid_constant__ CUtensorMap vmap,
                                                           DecodeParams p) {
   using L = DecodeSmem<D, STAGES>;

@@ -122,7 +122,7 @@ __device__ __forceinline__ uint32_t swz128(uint32_t base, int r, int c) {
 // Rotate one 16-byte chunk (8 bf16, dims [8c, 8c+8)) at the position whose tables start at
 // cosr / sinr.  `partner` is the chunk holding the other element of each pair in the NeoX layout
 // (c -/+ dim/16); GPT-J pairs sit inside the chunk.  fp32 math, one bf16 rounding.
-__device__ __forceinline__ uint4 rotary_chunk(uint4 own, uint4 partner, int c, const float* cosr,
+static __device__ __noinline__ uint4 rotary_chunk(uint4 own, uint4 partner, int c, const float* cosr,
                                               const float* sinr, int dim, bool interleaved) {
   if (c * 8 >= dim) return own;
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(&own);
