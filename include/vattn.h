@@ -212,6 +212,10 @@ vattn_status vattn_buffer_base(vattn_t* h, int32_t buffer_id, uint64_t* dptr);
  * The next `k` slots consecutive alloc_reqid calls would return now (eager slot first, then by
  * (mapped_groups, -req_id) with plan credits, manager.py:163-178); out[k], *n = how many. */
 vattn_status vattn_predict_alloc(vattn_t* h, int32_t k, int32_t* out, int32_t* n);
+/* Foreground launch window: while active != 0 the prefetch worker makes no new driver call
+ * (cuMemSetAccess holds the kernel driver's lock for up to milliseconds on B200 and would stall
+ * the caller's kernel launches).  Set around an iteration's launch burst. */
+vattn_status vattn_set_foreground(vattn_t* h, int32_t active);
 /* Ask the prefetch worker to back rows [0, tokens[i]) of slots[i] physically (queued prompts
  * about to be admitted there); replaces the previous hint set; used by the next background job
  * submitted with VATTN_BG_PREFETCH. */

@@ -109,6 +109,7 @@ SIGNATURES = {
     "vattn_events": (c_i32, [c_vp, P_i64, c_i64, P_i64]),
     "vattn_buffer_base": (c_i32, [c_vp, c_i32, C.POINTER(c_u64)]),
     "vattn_predict_alloc": (c_i32, [c_vp, c_i32, P_i32, P_i32]),
+    "vattn_set_foreground": (c_i32, [c_vp, c_i32]),
     "vattn_prefetch_hint": (c_i32, [c_vp, P_i32, P_i64, c_i32]),
     "vattn_slot_ready": (c_i32, [c_vp, c_i32, c_i64, P_i32]),
     "vattn_kv_append": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),

@@ -326,6 +326,16 @@ class Manager {
   int64_t pf_inflight_ = -1;
   size_t pf_reserve_ = 0;
   bool pf_stop_ = false;
+  bool pf_hold_ = false;          // foreground launch window: the worker makes no driver call
+ public:
+  void set_foreground(bool on) {
+    {
+      std::lock_guard<std::mutex> lk(pf_mu_);
+      pf_hold_ = on;
+    }
+    pf_cv_.notify_all();
+  }
+ private:
   int64_t pf_maps_ = 0, pf_access_ = 0, pf_errors_ = 0;
   double pf_map_us_ = 0, pf_access_us_ = 0;
   void pf_loop();
@@ -493,7 +503,10 @@ void Manager::pf_loop() {
   if (d.CtxSetCurrent(ctx_) != CUDA_SUCCESS) return;
   std::unique_lock<std::mutex> lk(pf_mu_);
   for (;;) {
-    pf_cv_.wait(lk, [&] { return pf_stop_ || pf_next_ < pf_targets_.size(); });
+    // cuMemMap/cuMemSetAccess take the kernel driver's lock for up to milliseconds; while the
+    // caller is launching an iteration's kernels the worker holds back so launches never queue
+    // behind it
+    pf_cv_.wait(lk, [&] { return pf_stop_ || (!pf_hold_ && pf_next_ < pf_targets_.size()); });
     if (pf_stop_) return;
     const int64_t key = pf_targets_[pf_next_++];
     if (!pf_pending_.erase(key) || spec_.count(key)) continue;   // claimed by a logical map meanwhile
@@ -1699,6 +1712,11 @@ vattn_status vattn_events(vattn_t* h, int64_t* trip, int64_t cap, int64_t* n) {
     const int64_t k = m.drain_events(trip, cap);
     if (n) *n = k;
   });
+}
+
+vattn_status vattn_set_foreground(vattn_t* h, int32_t active) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->set_foreground(active != 0); });
 }
 
 vattn_status vattn_predict_alloc(vattn_t* h, int32_t k, int32_t* out, int32_t* n) {

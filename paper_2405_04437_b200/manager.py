@@ -459,6 +459,11 @@ class KVCacheManager:
         ta = (C.c_int64 * max(1, n))(*[int(x) for x in tokens])
         check(lib().vattn_prefetch_hint(self._h, sa, ta, n))
 
+    def foreground(self, active: bool) -> None:
+        """Mark the caller's kernel-launch window: the prefetch worker makes no driver call while
+        it is active (its cuMemSetAccess calls would otherwise stall the launches)."""
+        check(lib().vattn_set_foreground(self._h, int(bool(active))))
+
     def slot_ready(self, slot: int, tokens: int) -> bool:
         """True when a step growing `slot` to `tokens` rows needs no driver call."""
         r = C.c_int32()

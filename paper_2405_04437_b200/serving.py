@@ -258,7 +258,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         max_iterations: int | None = None, model: SyntheticModel | None = None,
         manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
         prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0,
-        lazy_unmap: bool = False, stage_admission: bool = False, stage_max_iters: int = 8) -> ServingMetrics:
+        lazy_unmap: bool = False, stage_admission: bool = False, stage_max_iters: int = 8,
+        hold_worker: bool = False) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31).
 
     B200 additions (wall clock, CUDA backend; the allocator's logical state stays the
@@ -395,9 +396,13 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         kernel_ms = 0.0
         if wall and batch:
             t_k = time.perf_counter()
+            if hold_worker:
+                mgr.foreground(True)     # no prefetch driver call during the launch burst
             model.forward([(rid, seq_lens[rid]) for rid, r in running.items() if r.produced == 0],
                           [(rid, seq_lens[rid]) for rid, r in running.items() if r.produced > 0])
             mgr.mark_use()
+            if hold_worker:
+                mgr.foreground(False)
         if overlapped:
             next_seq = list(seq_lens)
             for rid in running:

@@ -25,6 +25,7 @@ ap.add_argument("--spec-slots", type=int, default=0, help="speculative eager: sl
 ap.add_argument("--spec-tokens", type=int, default=0, help="speculative eager: prompt tokens per slot")
 ap.add_argument("--out", default=None)
 ap.add_argument("--lazy-unmap", action="store_true", help="keep trimmed/reclaimed pages mapped until needed")
+ap.add_argument("--hold", action="store_true", help="prefetch worker pauses during the launch burst")
 ap.add_argument("--stage", type=int, default=0, help="staged admission: max iterations a prompt waits for its pages")
 ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel dense-layer time on the GPU")
 a = ap.parse_args()
@@ -40,7 +41,7 @@ else:
             preemption_cap=100_000, defer=not a.no_defer,
             dense_proxy=IterationModel() if a.dense_proxy else None, prefetch_tokens=a.prefetch,
             prefetch_slots=a.spec_slots, prefetch_slot_tokens=a.spec_tokens, lazy_unmap=a.lazy_unmap,
-            stage_admission=a.stage > 0, stage_max_iters=a.stage)
+            stage_admission=a.stage > 0, stage_max_iters=a.stage, hold_worker=a.hold)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
           "dense_proxy": a.dense_proxy, "prefetch": a.prefetch, "lazy_unmap": a.lazy_unmap, "stage": a.stage})
@@ -56,7 +57,7 @@ if a.out:
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     tag = (a.mode + ("_dense" if a.dense_proxy else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
            + (f"_ss{a.spec_slots}x{a.spec_tokens}" if a.spec_slots else "") + ("_lazy" if a.lazy_unmap else "")
-           + (f"_stage{a.stage}" if a.stage else ""))
+           + (f"_stage{a.stage}" if a.stage else "") + ("_hold" if a.hold else ""))
     m.write_iterations_csv(a.out + f"_{tag}.csv")
     with open(a.out + f"_{tag}.json", "w") as fh:
         json.dump(s, fh, indent=1)
