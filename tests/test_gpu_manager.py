@@ -331,3 +331,30 @@ def test_bounds_guard_raises_instead_of_faulting(monkeypatch):
         assert torch.isfinite(out.float()).all()
     finally:
         mgr.close()
+
+
+def test_foreground_window_holds_the_prefetch_worker():
+    """vattn_set_foreground: while the caller is in its launch window the worker makes no new
+    driver call; hinted pages appear only after the window closes."""
+    _cuda()
+    import time
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+
+    g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=2, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, eager_groups=0),
+                         lazy_unmap=True)
+    (slot,) = mgr.predict_alloc(1)
+    mgr.foreground(True)
+    mgr.prefetch_hint([slot], [3000])
+    mgr.bg_submit(execute_plan=False, prefetch=True)
+    time.sleep(0.3)
+    assert not mgr.slot_ready(slot, 3000)
+    assert mgr.driver_stats()["spec_maps"] == 0
+    mgr.foreground(False)
+    t0 = time.time()
+    while not mgr.slot_ready(slot, 3000):
+        assert time.time() - t0 < 60
+        time.sleep(0.01)
+    assert mgr.driver_stats()["spec_maps"] == 3 * 4     # 3 groups x 4 buffers
+    mgr.close()
