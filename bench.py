@@ -868,7 +868,7 @@ def extra_l8_shards(local, steps=20):
 
 def extra_decode_growth(local, steps=96, warm=8):
     """Exposed map ms/iter (BASELINE metric) while decode contexts GROW across page-group
-    boundaries: Llama-3-8B shape, 32 layers, B 64, contexts staggered 3584 + 16*b (mean ~4.1K)
+    boundaries: Llama-3-8B shape, 32 layers, B 64, contexts staggered 1024 + 16*b (mean ~1.5K: half the init maps of 4K)
     so a row crosses a 2 MiB group (64 buffers to map) every ~16 steps.  Each step = allocator
     step + 32 fused append+decode launches + a host sync (the token sampling point of a serving
     loop).  Modes: sync (maps inside step), overlapped (the reference's plan_overlap ->
@@ -883,12 +883,12 @@ def extra_decode_growth(local, steps=96, warm=8):
     dev = torch.device("cuda", local)
     g = llama3_8b(max_context=8192, max_batch=64)
     B, N, hq, hkv, d = g.max_batch, g.n_layers, g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
-    ctx0 = [3584 + 16 * b for b in range(B)]
+    ctx0 = [1024 + 16 * b for b in range(B)]
     gen = torch.Generator(device=dev).manual_seed(0)
     q = torch.randn(N, B, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
     kn = torch.randn(N, B, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
     out = torch.empty_like(q)
-    res = {"workload": "llama-3-8b decode b64, ctx 3584+16*b growing, 32 layers, 2 MiB groups",
+    res = {"workload": "llama-3-8b decode b64, ctx 1024+16*b growing, 32 layers, 2 MiB groups",
            "steps": steps}
     for mode, pf in (("sync", 0), ("overlapped", 0), ("overlapped_prefetch64", 64)):
         tok = g.per_token_layer_bytes
