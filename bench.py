@@ -955,7 +955,7 @@ def extra_serving(local, requests=48):
         # queue head, up to 32 iterations, until the prefetch worker backed its predicted slot)
         "overlapped_staged": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
                                   prefetch_slot_tokens=3072, lazy_unmap=True, stage_admission=True,
-                                  stage_max_iters=32),
+                                  stage_max_iters=32, hold_worker=True),
     }
     for mode, kw in variants.items():
         m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
