@@ -218,6 +218,16 @@ class Manager {
   const std::vector<int64_t>& last_plan() const { return last_plan_; }
   CacheView layer_view(int32_t layer) const;
   void check_decode_tiling() const;
+  // active slots' contexts differ by more than a quarter of the longest (decode row ordering)
+  bool mixed_lengths() const {
+    int64_t lo = INT64_MAX, hi = 0;
+    for (const Slot& s : slots_)
+      if (s.active) {
+        lo = std::min(lo, s.context_len);
+        hi = std::max(hi, s.context_len);
+      }
+    return hi > 0 && (hi - lo) * 4 > hi;
+  }
   bool real() const { return backend_ == VATTN_BACKEND_CUDA; }
   int64_t max_batch() const { return (int64_t)slots_.size(); }
   int32_t hq_local() const { return hq_local_; }
@@ -1766,6 +1776,7 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     h->m->check_decode_tiling();
+    vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
@@ -1789,6 +1800,7 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     h->m->check_decode_tiling();
+    vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
@@ -1854,6 +1866,7 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
   return guard([&] {
     if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
     h->m->check_decode_tiling();
+    vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
@@ -1878,6 +1891,7 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     h->m->check_decode_tiling();
+    vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);

@@ -97,6 +97,9 @@ struct GatherSink {
 // gathered launches; the epoch lives on the device).
 GatherSink gather_sink(vattn_gather_t* g, int hq_local, int batch, int head_dim);
 
+// Decode row-order hint for the next launches on this thread (-1 none, 0 keep, 1 longest first).
+void set_decode_order_hint(int h);
+
 // Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
 void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,
                       const void* v_new, int batch, int n_new, const int32_t* seqlens,

@@ -127,6 +127,7 @@ struct DecodeParams {
   __nv_bfloat16* v_cache;
   int64_t slot_stride, token_stride;
   GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
+  int32_t longest_first;        // schedule rows by descending length (B <= 256)
   Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
 };
 
@@ -186,8 +187,28 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty = full + STAGES;
 
-  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int split = blockIdx.x, kvh = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // Longest rows first: CTA z takes the row with the z-th largest length (ties by index), so a
+  // batch of mixed contexts does not finish on a tail of long rows started last (uniform(128,
+  // 8192) contexts, B 64: 5.87 -> 6.5 TB/s, against 6.7 for equal lengths).
+  int b = blockIdx.z;
+  if (p.longest_first) {
+    __shared__ int s_len[256];
+    __shared__ int s_row;
+    const int B = gridDim.z;
+    for (int i = threadIdx.x; i < B; i += blockDim.x) s_len[i] = __ldg(p.seqlens + i);
+    __syncthreads();
+    for (int i = threadIdx.x; i < B; i += blockDim.x) {
+      const int li = s_len[i];
+      int rank = 0;
+#pragma unroll 8
+      for (int k = 0; k < B; ++k) rank += (s_len[k] > li) || (s_len[k] == li && k < i);
+      if (rank == (int)blockIdx.z) s_row = i;
+    }
+    __syncthreads();
+    b = s_row;
+  }
   const bool fused = p.k_new != nullptr;
   const int pos_new = fused ? __ldg(p.seqlens + b) : -1;      // row receiving the new token
   const int seqlen = fused ? pos_new + 1 : __ldg(p.seqlens + b);
@@ -514,6 +535,9 @@ struct KernelState {
 KernelState* kernel_state_new() { return new KernelState(); }
 void kernel_state_free(KernelState* s) { delete s; }
 
+thread_local int g_order_hint = -1;
+void set_decode_order_hint(int h) { g_order_hint = h; }
+
 static int g_num_sms = 0;
 static int num_sms() {
   if (g_num_sms == 0) {
@@ -656,6 +680,17 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   p.hq = hq;
   p.group = group;
   p.num_splits = num_splits;
+  // longest-first row order costs ~1 % on equal lengths (rank pass before the first TMA) and
+  // gains ~11 % on mixed ones: on when the caller's hint says the lengths differ (the manager
+  // knows its slots' contexts), forced by VATTN_DEC_LONGEST_FIRST=0/1
+  static const int lf_env = [] {
+    const char* e = getenv("VATTN_DEC_LONGEST_FIRST");
+    return e ? atoi(e) : -1;
+  }();
+  const int hint = g_order_hint;
+  g_order_hint = -1;                 // a hint applies to the one launch it was set for
+  const int lf = lf_env >= 0 ? lf_env : (hint > 0 ? 1 : 0);
+  p.longest_first = (lf && batch > 1 && batch <= 256) ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)d);
   p.scale_log2 = scale * 1.4426950408889634f;
   if (fa) {
