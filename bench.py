@@ -218,9 +218,9 @@ def bench_decode(args, world, rank, local):
     B, N = g.max_batch, g.n_layers
     hkv, hq, d = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim
     steps, warm = args.steps, args.warmup
-    # pool: every slot at ctx + the steps we run, + one group per buffer of slack
-    groups = math.ceil((ctx + steps + warm + 1) * g.per_token_layer_bytes / MB2)
-    pool = (groups + 1) * 2 * N * B * MB2
+    # pool: every slot at ctx + all the steps this run takes (warm-up, timed, e2e), + slack
+    groups = math.ceil((ctx + steps + warm + 1 + max(3, min(steps, 20)) + 2) * g.per_token_layer_bytes / MB2)
+    pool = (groups * B + B // 8 + 1) * 2 * N * MB2   # every slot's groups + a little slack (fewer cuMemCreate at init)
     mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool, eager_groups=0,
                                           reclaim_threshold=0.0), backend="cuda", device=local)
     t0 = time.perf_counter()
