@@ -262,7 +262,8 @@ def bench_decode(args, world, rank, local):
         for layer in range(N):
             if pre_layer is not None:
                 pre_layer(layer)
-            if dec_events is not None:
+            timed = dec_events is not None and dec_events[layer] is not None
+            if timed:
                 dec_events[layer][0].record(st)
             if hg is not None:      # fused decode + head all-gather over peer memory
                 decode_attention_gather(mgr, layer, q_[layer], hg, p, idx, k_new=kn_[layer], v_new=vn_[layer],
@@ -277,7 +278,7 @@ def bench_decode(args, world, rank, local):
             else:   # one launch: append the new token at row p and attend over p + 1 rows
                 decode_attention_append(mgr, layer, q_[layer], kn_[layer], vn_[layer], p, idx,
                                         out=out_[layer], num_splits=splits)
-            if dec_events is not None:
+            if timed:
                 dec_events[layer][1].record(st)
             if post_layer is not None:
                 post_layer(layer)
@@ -312,8 +313,11 @@ def bench_decode(args, world, rank, local):
         # timing events as external record nodes, and the row-position update), so the timed
         # step costs one replay on the host.  Captured, not executed: state is unchanged.
         mgr.bg_wait()
+        # timing events are graph nodes and cost ~2.5 % of the step when placed around all 32
+        # launches (measured 12.13K vs 12.42K tok/s at every 4th): time every 4th layer's decode
+        stride = int(os.environ.get("VATTN_BENCH_EVENT_STRIDE", "4"))
         ev = [[(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
-               for _ in range(N)] for _ in range(steps)]
+               if layer % stride == 0 else None for layer in range(N)] for _ in range(steps)]
         cap = torch.cuda.Stream(device=dev)
         graphs = []
         for i in range(steps):
@@ -341,7 +345,7 @@ def bench_decode(args, world, rank, local):
     clk = clocks.stop()
     barrier()
     ms_total = s0.elapsed_time(s1)
-    dec_ms = [a.elapsed_time(b) for row in ev for a, b in row]
+    dec_ms = [a.elapsed_time(b) for row in ev for pair in row if pair is not None for a, b in [pair]]
     ms_step = max_over_ranks(ms_total / steps)
     tokens_s = B / (ms_step / 1e3)
     mean_ctx = ctx + warm + 1 + (steps - 1) / 2
@@ -416,6 +420,7 @@ def bench_decode(args, world, rank, local):
                      "page_group": MB2},
         "decode_kernel_us_mean": dec_us,
         "decode_num_splits": splits,
+        "decode_launches_timed": len(dec_ms),
         "decode_hbm_gbs": achieved,
         "decode_bytes_per_launch": dec_bytes,
         "exposed_map_ms_per_iter": statistics.mean(exposed) * 1e3,
