@@ -89,13 +89,14 @@ def test_decode_ignores_stale_rows_past_seqlen():
         assert max_rel_err(out.cpu(), ref) <= TOL
 
 
+@pytest.mark.parametrize("d", [128, 64])
 @pytest.mark.parametrize("block_size", [16, 64, 256])
-def test_decode_paged_matches_oracle(block_size):
+def test_decode_paged_matches_oracle(block_size, d):
     from paper_2405_04437_b200.attention import decode_attention_paged
 
     dev = _cuda()
     gen = torch.Generator().manual_seed(2)
-    B, hq, hkv, d = 5, 32, 8, 128
+    B, hq, hkv = 5, 32, 8
     lens = [1, 300, 1024, 17, 2049]
     maxb = (max(lens) + block_size - 1) // block_size
     nblocks = B * maxb + 3
