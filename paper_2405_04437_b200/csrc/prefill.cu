@@ -70,7 +70,24 @@ struct Params {
   const int4* work;
   const int4* reqs;
   const CUtensorMap* maps;
+  // grid order: 1 = heads vary fastest (blockIdx.x = head, blockIdx.y = work item), so the
+  // hardware's linear CTA order is heaviest-first across ALL heads and the CTAs of one GQA group
+  // read the same K/V tiles at the same time; 0 = work items fastest (per-head heaviest-first)
+  int head_fast;
 };
+
+static int head_fast_order() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VATTN_PF_HEAD_FAST");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v;
+}
+static dim3 pf_grid(Params& p, unsigned n_work, unsigned hq) {
+  p.head_fast = head_fast_order();
+  return p.head_fast ? dim3(hq, n_work) : dim3(n_work, hq);
+}
 
 // ---- tcgen05 wrappers -------------------------------------------------------------------
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -269,12 +286,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  int pair = p.n_pairs - 1 - blockIdx.x;   // heaviest (latest) query rows first
+  const int witem = p.head_fast ? blockIdx.y : blockIdx.x;
+  int pair = p.n_pairs - 1 - witem;        // heaviest (latest) query rows first
   int q_row0 = 0;                          // packed row of this request's query row 0
   const CUtensorMap* kmp = &kmap;
   const CUtensorMap* vmp = &vmap;
   if constexpr (VARLEN) {                  // work list is sorted heaviest first on the host
-    const int4 w = p.work[blockIdx.x];
+    const int4 w = p.work[witem];
     const int4 r = p.reqs[w.x];
     pair = w.y;
     q_row0 = r.x;
@@ -285,7 +303,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     kmp = p.maps + 2 * w.x;
     vmp = kmp + 1;
   }
-  const int head = blockIdx.y;
+  const int head = p.head_fast ? blockIdx.x : blockIdx.y;
   const int kvh = head / p.group;
   const int q0A = pair * 2 * kBM, q0B = q0A + kBM;
   const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
@@ -702,7 +720,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.causal = causal ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
-  dim3 grid(p.n_pairs, hq);
+  const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
   if (D == 64) {
     static bool attr64 = false;
     if (!attr64) {
@@ -809,7 +827,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   p.maps = reinterpret_cast<const CUtensorMap*>(dbuf);
   p.reqs = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b);
   p.work = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b + reqs_b);
-  dim3 grid((unsigned)work.size(), hq);
+  const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), hq);
   if (D == 128) {
     static bool attr = false;
     if (!attr) {
@@ -869,7 +887,7 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
                                   pf::PfL<128>::kSmem), "smem attr");
     attr = true;
   }
-  dim3 grid(p.n_pairs, hq);
+  const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
   pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
 }
