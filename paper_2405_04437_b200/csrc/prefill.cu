@@ -270,7 +270,7 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
 template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-               const __grid_constant__ CUtensorMap vmap, Params p) {
+               const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
   using L = PfL<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -625,6 +625,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       fence_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    // Full tiles (and any tile of a single-request launch: the map clips rows >= n_q) go out
+    // through shared memory and one TMA store: the tile's Q buffer is free once o_final landed
+    // (every MMA reading it has retired), and whole 128-byte rows reach L2 instead of the
+    // half-sector 16-byte stores of one row per thread.  Varlen tail tiles store directly so
+    // they cannot spill into the next request's rows.
+    const bool via_tma = !VARLEN || q0 + kBM <= p.n_q;
+    const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
     __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
     const bool live = qpos < p.n_q;
 #pragma unroll
@@ -637,16 +644,31 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
         for (int c = 0; c < 32; ++c) o[c] = 0u;
       }
-      if (live) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          uint4 v;
-          v.x = ptx::pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
-          v.y = ptx::pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
-          v.z = ptx::pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
-          v.w = ptx::pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
+      for (int c = 0; c < 32; c += 8) {
+        uint4 v;
+        v.x = ptx::pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
+        v.y = ptx::pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
+        v.z = ptx::pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
+        v.w = ptx::pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
+        if (via_tma) {
+          const int cc = (c0 + c) / 8;
+          const uint32_t a = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+        } else if (live) {
           *reinterpret_cast<uint4*>(dst + c0 + c) = v;
         }
+      }
+    }
+    if (via_tma) {
+      ptx::fence_proxy_async();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");   // the 4 warps of tile x
+      if (warp % 4 == 0 && lane == 0) {
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h)
+          ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, head, q_row0 + q0);
+        ptx::tma_store_commit();
+        ptx::tma_store_wait_read();
       }
     }
   }
@@ -693,6 +715,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   cuuint64_t qs[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
   cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
   const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  const CUtensorMap omap = make_map(out, 3, qd, qs, qb);
   // 3-D map rooted at the request's slot: [D, Hkv, kv_len] (the slot index is folded into the base)
   cuuint64_t kd[3] = {(cuuint64_t)D, (cuuint64_t)v.hkv, (cuuint64_t)kvl};
   cuuint64_t ks[2] = {(cuuint64_t)D * 2, (cuuint64_t)v.token_stride};
@@ -728,7 +751,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
                                     pf::PfL<64>::kSmem), "smem attr");
       attr64 = true;
     }
-    pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, p);
+    pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
     check_rt(cudaGetLastError(), "prefill launch");
     return;
   }
@@ -741,10 +764,10 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
     check_rt(cudaFuncSetAttribute(pf::prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
   }
-  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
-  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
-  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
-  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
+  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
@@ -817,6 +840,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   cuuint64_t qs[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
   cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
   const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  const CUtensorMap omap = make_map(out, 3, qd, qs, qb);
   pf::Params p{};
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.hq = hq;
@@ -835,7 +859,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
                                     pf::PfL<128>::kSmem), "smem attr");
       attr = true;
     }
-    pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, p);
+    pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -843,7 +867,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
                                     pf::PfL<64>::kSmem), "smem attr");
       attr = true;
     }
-    pf::prefill_kernel<0, false, 64, true><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, qmap, qmap, p);
+    pf::prefill_kernel<0, false, 64, true><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
   }
   check_rt(cudaGetLastError(), "prefill (varlen) launch");
 }
@@ -861,6 +885,7 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
   cuuint64_t qs[2] = {(cuuint64_t)pf::kD * 2, (cuuint64_t)hq * pf::kD * 2};
   cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
   const CUtensorMap qmap = make_map(const_cast<void*>(q), 3, qd, qs, qb);
+  const CUtensorMap omap = make_map(out, 3, qd, qs, qb);
   const uint64_t row = (uint64_t)hkv * pf::kD * 2;
   cuuint64_t kd[4] = {(cuuint64_t)pf::kD, (cuuint64_t)hkv, (cuuint64_t)block_size, (cuuint64_t)num_blocks};
   cuuint64_t ks[3] = {(cuuint64_t)pf::kD * 2, row, row * block_size};
@@ -888,7 +913,7 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
     attr = true;
   }
   const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
-  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, p);
+  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
 }
 
