@@ -822,20 +822,35 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   std::memcpy(blob.data(), maps.data(), maps_b);
   std::memcpy(blob.data() + maps_b, reqs.data(), reqs_b);
   for (size_t k = 0; k < work.size(); ++k) std::memcpy(blob.data() + maps_b + reqs_b + k * sizeof(int4), &work[k].second, sizeof(int4));
-  // one schedule buffer per (thread, device); reused in stream order
-  static thread_local std::map<int, std::pair<void*, size_t>> bufs;
+  // Schedule buffers per (thread, device): a ring of pinned host staging slots, each with a
+  // device copy and an event, so a call never waits on the previous launch and the H2D copy is
+  // a true async DMA (a pageable source may make the driver stage or serialise it).
+  constexpr int kSlots = 4;
+  struct Ring {
+    void* host[kSlots] = {};
+    void* dev[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
+    size_t cap[kSlots] = {};
+    int next = 0;
+  };
+  static thread_local std::map<int, Ring> rings;
   int dev = 0;
   check_rt(cudaGetDevice(&dev), "cudaGetDevice");
-  auto& slot = bufs[dev];
-  if (blob.size() > slot.second) {
-    if (slot.first) check_rt(cudaFree(slot.first), "cudaFree(varlen)");
-    slot.second = std::max(blob.size(), (size_t)1 << 16);
-    check_rt(cudaMalloc(&slot.first, slot.second), "cudaMalloc(varlen)");
+  Ring& ring = rings[dev];
+  const int k = ring.next;
+  ring.next = (k + 1) % kSlots;
+  if (ring.done[k]) check_rt(cudaEventSynchronize(ring.done[k]), "varlen slot reuse");   // 4 launches back
+  else check_rt(cudaEventCreateWithFlags(&ring.done[k], cudaEventDisableTiming), "cudaEventCreate(varlen)");
+  if (blob.size() > ring.cap[k]) {
+    if (ring.host[k]) check_rt(cudaFreeHost(ring.host[k]), "cudaFreeHost(varlen)");
+    if (ring.dev[k]) check_rt(cudaFree(ring.dev[k]), "cudaFree(varlen)");
+    ring.cap[k] = std::max(blob.size(), (size_t)1 << 16);
+    check_rt(cudaMallocHost(&ring.host[k], ring.cap[k]), "cudaMallocHost(varlen)");
+    check_rt(cudaMalloc(&ring.dev[k], ring.cap[k]), "cudaMalloc(varlen)");
   }
-  void* dbuf = slot.first;
-  // pageable source: the copy is staged before cudaMemcpyAsync returns; stream order keeps the
-  // previous launch's reads of dbuf ahead of this write
-  check_rt(cudaMemcpyAsync(dbuf, blob.data(), blob.size(), cudaMemcpyHostToDevice, st), "varlen params H2D");
+  std::memcpy(ring.host[k], blob.data(), blob.size());
+  void* dbuf = ring.dev[k];
+  check_rt(cudaMemcpyAsync(dbuf, ring.host[k], blob.size(), cudaMemcpyHostToDevice, st), "varlen params H2D");
   cuuint64_t qd[3] = {(cuuint64_t)D, (cuuint64_t)hq, (cuuint64_t)total};
   cuuint64_t qs[2] = {(cuuint64_t)D * 2, (cuuint64_t)hq * D * 2};
   cuuint32_t qb[3] = {64, 1, (cuuint32_t)pf::kBM};
@@ -870,6 +885,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
     pf::prefill_kernel<0, false, 64, true><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
   }
   check_rt(cudaGetLastError(), "prefill (varlen) launch");
+  check_rt(cudaEventRecord(ring.done[k], st), "varlen slot event");
 }
 
 void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool, int num_blocks,

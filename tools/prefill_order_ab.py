@@ -41,6 +41,14 @@ def inner():
         sl = list(range(n))
         ms = timeit(lambda: prefill_attention_varlen_raw(q, k, v, ql, sl, out=out))
         print(f"V{n}x{L} {2.0 * n * L * L * 128 * 32 / ms / 1e9:.0f}")
+        import time
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(10):
+            prefill_attention_varlen_raw(q, k, v, ql, sl, out=out)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        print(f"H{n}x{L} {(t1 - t0) / 10 * 1e6:.0f}")
 
 
 if __name__ == "__main__":
