@@ -4,14 +4,14 @@ sys.path.insert(0, ".")
 import torch
 from paper_2405_04437_b200.attention import decode_attention_raw, decode_num_splits
 dev = torch.device("cuda")
-for (B, L) in ((1, 32768), (1, 131072), (2, 65536), (4, 32768)):
+for (B, L) in ((1, 32768), (1, 131072), (2, 65536), (4, 32768), (8, 32768)):
     kv = [(torch.randn(B, L, 8, 128, device=dev, dtype=torch.bfloat16),
            torch.randn(B, L, 8, 128, device=dev, dtype=torch.bfloat16)) for _ in range(4)]
     q = torch.randn(B, 32, 128, device=dev, dtype=torch.bfloat16)
     seq = torch.full((B,), L, dtype=torch.int32, device=dev)
     byt = 2 * B * L * 8 * 128 * 2
     res = {}
-    for s in (8, 16, 24, 32, 37, 48, 64):
+    for s in (2, 4, 8, 16, 19, 24, 32, 37, 48, 64):
         for i in range(4):
             decode_attention_raw(q, kv[i][0], kv[i][1], seq, num_splits=s)
         torch.cuda.synchronize()
