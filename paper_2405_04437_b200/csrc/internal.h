@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime_api.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -64,6 +65,20 @@ struct CacheView {
 };
 
 CacheView view_from_desc(const vattn_cache_desc* c);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the kernel in the current device's context, so a process driving several GPUs
+// must set it on each.  Thread-safe (setting it twice is harmless).
+template <auto Kern>
+void ensure_smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  check_rt(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  check_rt(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attribute");
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 // Kernel-side per-handle state (tensor-map cache, split-K workspace); defined in kernels.cu.
 struct KernelState;

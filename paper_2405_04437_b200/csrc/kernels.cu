@@ -631,12 +631,7 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
                        int hkv, cudaStream_t st) {
   using L = DecodeSmem<D, STAGES>;
   auto kern = decode_kernel<D, STAGES, PAGED>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    check_rt(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes),
-             "decode smem attribute");
-    attr_done = true;
-  }
+  ensure_smem_attr<decode_kernel<D, STAGES, PAGED>>(L::kBytes);
   dim3 grid(p.num_splits, hkv, batch);
   kern<<<grid, kThreads, L::kBytes, st>>>(km, vm, p);
   check_rt(cudaGetLastError(), "decode launch");

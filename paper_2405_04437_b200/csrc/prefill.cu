@@ -745,12 +745,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.scale_log2 = scale * 1.4426950408889634f;
   const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
   if (D == 64) {
-    static bool attr64 = false;
-    if (!attr64) {
-      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    pf::PfL<64>::kSmem), "smem attr");
-      attr64 = true;
-    }
+    ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
     check_rt(cudaGetLastError(), "prefill launch");
     return;
@@ -759,15 +754,21 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   if (poly < 0) {
     const char* e = getenv("VATTN_PF_POLY");   // share of exp2 on the FMA pipe, in quarters
     poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::PfL<128>::kSmem), "smem attr");
   }
-  if (poly == 0) pf::prefill_kernel<0><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
-  else if (poly == 1) pf::prefill_kernel<1><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
-  else if (poly == 2) pf::prefill_kernel<2><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
-  else pf::prefill_kernel<3><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+  constexpr int kS = pf::PfL<128>::kSmem;
+  if (poly == 0) {
+    ensure_smem_attr<pf::prefill_kernel<0>>(kS);
+    pf::prefill_kernel<0><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
+  } else if (poly == 1) {
+    ensure_smem_attr<pf::prefill_kernel<1>>(kS);
+    pf::prefill_kernel<1><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
+  } else if (poly == 2) {
+    ensure_smem_attr<pf::prefill_kernel<2>>(kS);
+    pf::prefill_kernel<2><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
+  } else {
+    ensure_smem_attr<pf::prefill_kernel<3>>(kS);
+    pf::prefill_kernel<3><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
+  }
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
@@ -868,20 +869,10 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   p.work = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b + reqs_b);
   const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), hq);
   if (D == 128) {
-    static bool attr = false;
-    if (!attr) {
-      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    pf::PfL<128>::kSmem), "smem attr");
-      attr = true;
-    }
+    ensure_smem_attr<pf::prefill_kernel<0, false, 128, true>>(pf::PfL<128>::kSmem);
     pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, false, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    pf::PfL<64>::kSmem), "smem attr");
-      attr = true;
-    }
+    ensure_smem_attr<pf::prefill_kernel<0, false, 64, true>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64, true><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
   }
   check_rt(cudaGetLastError(), "prefill (varlen) launch");
@@ -922,12 +913,7 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
   p.block_table = block_table;
   p.block_size = block_size;
   p.box_tokens = box;
-  static bool attr = false;
-  if (!attr) {
-    check_rt(cudaFuncSetAttribute(pf::prefill_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  pf::PfL<128>::kSmem), "smem attr");
-    attr = true;
-  }
+  ensure_smem_attr<pf::prefill_kernel<0, true>>(pf::PfL<128>::kSmem);
   const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
   pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
