@@ -629,8 +629,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     // through shared memory and one TMA store: the tile's Q buffer is free once o_final landed
     // (every MMA reading it has retired), and whole 128-byte rows reach L2 instead of the
     // half-sector 16-byte stores of one row per thread.  Varlen tail tiles store directly so
-    // they cannot spill into the next request's rows.
-    const bool via_tma = !VARLEN || q0 + kBM <= p.n_q;
+    // they cannot spill into the next request's rows.  A tile that sees no keys (n == 0) also
+    // stores its zeros directly: it never waited for its Q load, which may still be landing in
+    // that buffer (found under compute-sanitizer's slowed timing).
+    const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
     const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
     __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
     const bool live = qpos < p.n_q;

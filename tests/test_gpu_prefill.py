@@ -52,6 +52,27 @@ def test_prefill_raw_matches_oracle(case, d):
     assert err <= TOL, err
 
 
+def test_prefill_tiles_without_keys_write_exact_zeros():
+    """Bottom-right causal alignment with kv_len < n_q: query rows that see no key output 0
+    (flash-attn convention).  A tile with no keys must not stage its zeros in its Q buffer (the
+    Q load may still be landing there): many heads and repeats to widen the race window."""
+    from paper_2405_04437_b200.attention import prefill_attention_raw
+
+    dev = _cuda()
+    gen = torch.Generator().manual_seed(5)
+    n_q, kv_len, hq, hkv = 129, 1, 64, 8
+    k = torch.randn(1, 128, hkv, 128, generator=gen).to(torch.bfloat16).to(dev)
+    v = torch.randn(1, 128, hkv, 128, generator=gen).to(torch.bfloat16).to(dev)
+    q = torch.randn(n_q, hq, 128, generator=gen).to(torch.bfloat16).to(dev)
+    for _ in range(20):
+        out = prefill_attention_raw(q, k, v, 0, kv_len, causal=True)
+        torch.cuda.synchronize()
+        assert torch.count_nonzero(out[:128]).item() == 0
+        # the last row sees key 0 only: its output is V row 0 of its KV head
+        ref = v[0, 0].repeat_interleave(hq // hkv, dim=0)
+        assert torch.equal(out[128], ref)
+
+
 def test_prefill_full_size_y6_sampled_heads():
     """BASELINE config 3 at full size (16K causal, 32 Q / 4 KV heads): heads checked against
     the oracle on CPU (2 of 32), all heads checked for finiteness."""
