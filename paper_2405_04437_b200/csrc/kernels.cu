@@ -482,18 +482,44 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
   const int row = blockIdx.x * (blockDim.x / (D / 4)) + threadIdx.x / (D / 4);
   const int c4 = threadIdx.x % (D / 4);
   if (row < rows) {
+    // One batch of up to 16 splits per round trip: every lse and partial of the batch is
+    // loaded before any is used, so the L2/DRAM latencies overlap (a plain loop waits ~600
+    // cycles per split).  Batches after the first rescale to a running max; with <= 16 splits
+    // this is exactly the two-pass merge against the global max.
+    constexpr int kB = 16;
     const float* lse = part_lse + (int64_t)row * num_splits;
+    const float* po = part_o + (int64_t)row * num_splits * D + c4 * 4;
     float M = -INFINITY;
-    for (int s = 0; s < num_splits; ++s) M = fmaxf(M, lse[s]);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float wsum = 0.f;
-    if (M != -INFINITY) {
-      for (int s = 0; s < num_splits; ++s) {
-        const float w = exp2f(lse[s] - M);
-        if (w == 0.f) continue;
-        const float4 v = *reinterpret_cast<const float4*>(part_o + ((int64_t)row * num_splits + s) * D + c4 * 4);
-        acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
-        wsum += w;
+    for (int s0 = 0; s0 < num_splits; s0 += kB) {
+      float l[kB];
+      float4 v[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        l[i] = -INFINITY;
+        if (s0 + i < num_splits) {
+          l[i] = lse[s0 + i];
+          v[i] = *reinterpret_cast<const float4*>(po + (int64_t)(s0 + i) * D);
+        }
+      }
+      float mb = M;
+#pragma unroll
+      for (int i = 0; i < kB; ++i) mb = fmaxf(mb, l[i]);
+      if (mb == -INFINITY) continue;
+      if (mb != M && M != -INFINITY) {
+        const float f = exp2f(M - mb);
+        acc.x *= f; acc.y *= f; acc.z *= f; acc.w *= f;
+        wsum *= f;
+      }
+      M = mb;
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const float w = exp2f(l[i] - M);
+        if (w != 0.f) {   // an empty split (lse -inf) may hold stale partials: never read into acc
+          acc.x += w * v[i].x; acc.y += w * v[i].y; acc.z += w * v[i].z; acc.w += w * v[i].w;
+          wsum += w;
+        }
       }
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
