@@ -105,8 +105,11 @@ __global__ void __launch_bounds__(256) kv_append_paged_kernel(PagedAppendParams 
 
 // ------------------------------------------------------------------------------ decode
 constexpr int kTile = 64;        // tokens per pipeline stage
-constexpr int kConsumerWarps = 4;  // each owns 16 tokens of a tile
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + one TMA producer warp
+constexpr int kWarpsPerTile = 4;   // a group of 4 consumer warps owns a tile, 16 tokens each
+// Consumer warps per CTA (template CW): 4 = one group, 2 CTAs per SM (the common case); 8 = two
+// groups taking alternate tiles, for grids of at most one CTA per SM, where a single group per
+// SM leaves each sub-partition one warp to hide the ldmatrix/mma/exp2 latencies with.
+constexpr int decode_threads(int cw) { return (cw + 1) * 32; }   // + one TMA producer warp
 
 struct DecodeParams {
   const __nv_bfloat16* q;     // [batch, hq, D]
@@ -163,23 +166,24 @@ __device__ __forceinline__ void sink_signal(const GatherSink& s, uint32_t total_
   }
 }
 
-template <int D, int STAGES>
+template <int D, int STAGES, int CW = 4>
 struct DecodeSmem {
   static constexpr int kHalfBytes = kTile * 128;             // 64 tokens x 64 dims x bf16
   static constexpr int kTileBytes = (D / 64) * kHalfBytes;   // one of K or V
   static constexpr int kStageBytes = 2 * kTileBytes;
   static constexpr int kQStride = D + 8;                     // bf16 elements, conflict-free ldmatrix
   static constexpr int kQBytes = 16 * kQStride * 2;
-  static constexpr int kRedBytes = kConsumerWarps * 16 * 2 * 4;
+  static constexpr int kRedBytes = CW * 16 * 2 * 4;
+  static_assert(CW * 16 * D * 4 <= STAGES * kStageBytes, "merge scratch reuses the pipeline smem");
   static constexpr int kBarOff = STAGES * kStageBytes + kQBytes + kRedBytes;
   static constexpr int kBytes = kBarOff + 2 * STAGES * 8 + 1024;  // + alignment slack
 };
 
-template <int D, int STAGES, bool PAGED>
-__global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_constant__ CUtensorMap kmap,
+template <int D, int STAGES, bool PAGED, int CW = 4>
+__global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_kernel(const __grid_constant__ CUtensorMap kmap,
                                                           const __grid_constant__ CUtensorMap vmap,
                                                           DecodeParams p) {
-  using L = DecodeSmem<D, STAGES>;
+  using L = DecodeSmem<D, STAGES, CW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * L::kStageBytes);
@@ -221,13 +225,13 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], kConsumerWarps);
+      ptx::mbar_init(&empty[s], kWarpsPerTile);
     }
     ptx::fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == CW) {
     // ===== TMA producer =====
     if (lane == 0 && n_tiles > 0) {
       ptx::prefetch_tmap(&kmap);
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
   // at the new token's position when rotary tables are given
   const bool rotary = fused && p.rot.cos != nullptr;
   const int rhalf_chunks = p.rot.dim / 16;
-  for (int i = threadIdx.x; i < 16 * (D / 8); i += kConsumerWarps * 32) {
+  for (int i = threadIdx.x; i < 16 * (D / 8); i += CW * 32) {
     const int r = i / (D / 8), c = i % (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < p.group) {
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
     }
     *reinterpret_cast<uint4*>(qs + r * L::kQStride + c * 8) = v;
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
   uint32_t qa[D / 16][4];
 #pragma unroll
   for (int kk = 0; kk < D / 16; ++kk) {
@@ -301,12 +305,13 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const int g = lane >> 2, t4 = lane & 3;
 
-  for (int it = 0; it < n_tiles; ++it) {
+  const int wr = warp % kWarpsPerTile;   // 16-token row block of the tile this warp owns
+  for (int it = warp / kWarpsPerTile; it < n_tiles; it += CW / kWarpsPerTile) {
     const int st = it % STAGES;
     ptx::mbar_wait(&full[st], (it / STAGES) & 1);
     const uint32_t ks = ptx::smem_u32(smem + st * L::kStageBytes);
     const uint32_t vs = ks + L::kTileBytes;
-    const int my_tok0 = (tile_begin + it) * kTile + warp * 16;
+    const int my_tok0 = (tile_begin + it) * kTile + wr * 16;
     const int valid = min(16, seqlen - my_tok0);
     if (fused && pos_new >= my_tok0 && pos_new < my_tok0 + 16) {
       // This warp owns the new token's row: patch it into the landed smem tile (the TMA copy
@@ -337,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        const int row = warp * 16 + ((lane >> 4) << 3) + (lane & 7);
+        const int row = wr * 16 + ((lane >> 4) << 3) + (lane & 7);
         const int chunk = ((kk & 3) << 1) + ((lane >> 3) & 1);
         uint32_t b0, b1, b2, b3;
         ptx::ldsm_x4(ptx::swz128(ks + (kk >> 2) * L::kHalfBytes, row, chunk), b0, b1, b2, b3);
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
         // rows past seqlen may hold stale bytes of a reused physical page: 0 * NaN must not
         // reach the accumulator, so zero them (they are the last rows this CTA reads).
         for (int i = lane; i < (16 - valid) * (D / 8); i += 32) {
-          const int r = warp * 16 + valid + i / (D / 8);
+          const int r = wr * 16 + valid + i / (D / 8);
           const int c = i % (D / 8);
           const uint32_t a = ptx::swz128(vs + (c >> 3) * L::kHalfBytes, r, c & 7);
           asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(0u));
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
       pa[3] = ptx::pack_bf16(p_[1][2], p_[1][3]);
 #pragma unroll
       for (int nd = 0; nd < D / 16; ++nd) {
-        const int row = warp * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
+        const int row = wr * 16 + (((lane >> 3) & 1) << 3) + (lane & 7);
         const int chunk = ((nd & 3) << 1) + (lane >> 4);
         uint32_t b0, b1, b2, b3;
         ptx::ldsm_x4_t(ptx::swz128(vs + (nd >> 2) * L::kHalfBytes, row, chunk), b0, b1, b2, b3);
@@ -414,17 +419,17 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   float* red_m = red;
-  float* red_l = red + kConsumerWarps * 16;
+  float* red_l = red + CW * 16;
   if (t4 == 0) {
     red_m[warp * 16 + g] = m0;
     red_m[warp * 16 + g + 8] = m1;
     red_l[warp * 16 + g] = l0;
     red_l[warp * 16 + g + 8] = l1;
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
   float M0 = -INFINITY, M1 = -INFINITY;
 #pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
+  for (int w = 0; w < CW; ++w) {
     M0 = fmaxf(M0, red_m[w * 16 + g]);
     M1 = fmaxf(M1, red_m[w * 16 + g + 8]);
   }
@@ -442,15 +447,15 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
     r1[0] = o[n][2] * sc1;
     r1[1] = o[n][3] * sc1;
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
-  for (int i = threadIdx.x; i < p.group * D; i += kConsumerWarps * 32) {
+  asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
+  for (int i = threadIdx.x; i < p.group * D; i += CW * 32) {
     const int r = i / D, c = i % D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, red_m[w * 16 + r]);
+    for (int w = 0; w < CW; ++w) M = fmaxf(M, red_m[w * 16 + r]);
     float lsum = 0.f, acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
+    for (int w = 0; w < CW; ++w) {
       const float mw = red_m[w * 16 + r];
       const float f = (M == -INFINITY) ? 0.f : ptx::fast_exp2(mw - M);
       lsum += red_l[w * 16 + r] * f;
@@ -468,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
     }
   }
   if (p.sink.n_ranks && p.num_splits == 1)
-    sink_signal(p.sink, gridDim.x * gridDim.y * gridDim.z, kConsumerWarps * 32);
+    sink_signal(p.sink, gridDim.x * gridDim.y * gridDim.z, CW * 32);
 }
 
 // merge split partials with log-sum-exp weights (log2 domain); with a gather sink the merged
@@ -652,14 +657,14 @@ static int auto_splits(int units, int max_len) {
   return std::max(1, std::min(s, kMaxSplits));
 }
 
-template <int D, int STAGES, bool PAGED>
+template <int D, int STAGES, bool PAGED, int CW = 4>
 static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParams p, int batch,
                        int hkv, cudaStream_t st) {
-  using L = DecodeSmem<D, STAGES>;
-  auto kern = decode_kernel<D, STAGES, PAGED>;
-  ensure_smem_attr<decode_kernel<D, STAGES, PAGED>>(L::kBytes);
+  using L = DecodeSmem<D, STAGES, CW>;
+  auto kern = decode_kernel<D, STAGES, PAGED, CW>;
+  ensure_smem_attr<decode_kernel<D, STAGES, PAGED, CW>>(L::kBytes);
   dim3 grid(p.num_splits, hkv, batch);
-  kern<<<grid, kThreads, L::kBytes, st>>>(km, vm, p);
+  kern<<<grid, decode_threads(CW), L::kBytes, st>>>(km, vm, p);
   check_rt(cudaGetLastError(), "decode launch");
   if (p.num_splits > 1) {
     const int rows = batch * p.hq;
@@ -751,11 +756,20 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
     // more CTAs than SMs: 2 CTAs/SM (3 stages) so a grid of up to 2 x 148 runs in one wave
     // (L8 at G = 2: 256 CTAs; measured 6.26 vs 6.12 TB/s with 4 stages in two waves)
     const int stages = forced ? forced : (batch * hkv * p.num_splits > num_sms() ? 3 : 4);
+    // at most one CTA per SM: two consumer groups per CTA (VATTN_DEC_CW=4 forces one)
+    static const int cw_env = [] {
+      const char* e = getenv("VATTN_DEC_CW");
+      return e ? atoi(e) : 0;
+    }();
+    const bool wide = stages == 4 && cw_env != 4 && batch * hkv * p.num_splits <= num_sms();
     if (paged) {   // same rule, so the paged comparison differs from the contiguous path only in layout
       if (stages == 3) run_decode<128, 3, true>(km, vm, p, batch, hkv, st);
+      else if (wide) run_decode<128, 4, true, 8>(km, vm, p, batch, hkv, st);
       else run_decode<128, 4, true>(km, vm, p, batch, hkv, st);
     } else if (stages == 3) {
       run_decode<128, 3, false>(km, vm, p, batch, hkv, st);
+    } else if (wide) {
+      run_decode<128, 4, false, 8>(km, vm, p, batch, hkv, st);
     } else {
       run_decode<128, 4, false>(km, vm, p, batch, hkv, st);
     }
