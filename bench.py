@@ -62,8 +62,42 @@ class ClockSampler:
         self.proc = None
         self.lines: list[str] = []
         self._t = None
+        self._nvml = None          # (pynvml, handle) when NVML is usable
+        self._stop = threading.Event()
+        self._samples: list[tuple[float, float, int]] = []
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        try:   # the CUDA device's NVML handle by UUID (CUDA_VISIBLE_DEVICES may renumber)
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(self.dev).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        except Exception:   # noqa: BLE001
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _nvml_loop(self):
+        nv, h = self._nvml
+        smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self._stop.is_set():
+            try:
+                self._samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), smax,
+                                      int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:   # noqa: BLE001
+                break
+            self._stop.wait(0.005)
 
     def start(self):
+        # NVML in-process every 5 ms (no start-up lag, so short timed regions get many samples);
+        # nvidia-smi -lms 100 when NVML is unavailable
+        try:
+            self._nvml = self._nvml_handle()
+            self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._t.start()
+            return
+        except Exception:   # noqa: BLE001
+            self._nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
@@ -80,6 +114,19 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+            nv = self._nvml[0]
+            bits = {"hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                    "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                    "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                    "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+            sm = [x[0] for x in self._samples]
+            reasons = {n for n, b in bits.items() for x in self._samples if x[2] & b}
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": self._samples[-1][1] if self._samples else None,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -102,7 +149,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 def box_copy_gbs(dev) -> float:
