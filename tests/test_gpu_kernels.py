@@ -91,13 +91,16 @@ def test_decode_ignores_stale_rows_past_seqlen():
 
 @pytest.mark.parametrize("d", [128, 64])
 @pytest.mark.parametrize("block_size", [16, 64, 256])
-def test_decode_paged_matches_oracle(block_size, d):
+@pytest.mark.parametrize("small_grid", [False, True])
+def test_decode_paged_matches_oracle(block_size, d, small_grid):
+    """small_grid: 2 rows x 8 KV heads x auto splits <= 148 CTAs, the two-consumer-group kernel;
+    otherwise 5 rows (> 148 CTAs, 3-stage ring, one group)."""
     from paper_2405_04437_b200.attention import decode_attention_paged
 
     dev = _cuda()
     gen = torch.Generator().manual_seed(2)
-    B, hq, hkv = 5, 32, 8
-    lens = [1, 300, 1024, 17, 2049]
+    B, hq, hkv = (2, 32, 8) if small_grid else (5, 32, 8)
+    lens = [1000, 2049] if small_grid else [1, 300, 1024, 17, 2049]
     maxb = (max(lens) + block_size - 1) // block_size
     nblocks = B * maxb + 3
     kp, vp = _mk_cache(nblocks, block_size, hkv, d, gen)
