@@ -20,8 +20,11 @@ from ._abi import check, lib
 
 
 def _stream(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # the raw handle of the current stream without building a torch.cuda.Stream object
+    # (same value as torch.cuda.current_stream().cuda_stream, graph capture included; ~2 us less)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def _need_cuda(*ts):
