@@ -510,5 +510,5 @@ class KVCacheManager:
 def _stream_ptr(stream) -> int:
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     return getattr(stream, "cuda_stream", stream) or 0
