@@ -25,3 +25,19 @@ def test_reference_arm_prints_one_contract_line():
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_clock_sampler_reports_without_a_gpu():
+    """The clocks object is always present: NVML when it works, else nvidia-smi, else an explicit
+    'unavailable' reason (CPU host)."""
+    import time
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    c = bench.ClockSampler(0)
+    c.start()
+    time.sleep(0.02)
+    d = c.stop()
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d)
+    assert isinstance(d["reasons"], list)
