@@ -40,6 +40,8 @@ DECODE_CASES = [
     (2, 32, 4, 128, [2048, 31], False, 0),                      # Y6 group of 8
     (3, 7, 1, 128, [300, 0, 129], False, 2),                    # Y34/8 shard: 1 KV head, empty row
     (4, 16, 1, 64, [64, 65, 127, 1], True, 0),                  # group of 16
+    (1, 32, 8, 128, [8192], False, 64),                         # 64 splits: 4 combine batches
+    (2, 32, 8, 128, [8000, 1000], False, 40),                   # row 2: splits 16-39 empty
 ]
 
 
