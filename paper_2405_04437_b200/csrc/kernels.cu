@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
 
   const int split = blockIdx.x, kvh = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (p.num_splits > 1) asm volatile("griddepcontrol.launch_dependents;");
   // Longest rows first: CTA z takes the row with the z-th largest length (ties by index), so a
   // batch of mixed contexts does not finish on a tail of long rows started last (uniform(128,
   // 8192) contexts, B 64: 5.87 -> 6.5 TB/s, against 6.7 for equal lengths).
@@ -486,6 +487,9 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
                                                              GatherSink sink) {
   const int row = blockIdx.x * (blockDim.x / (D / 4)) + threadIdx.x / (D / 4);
   const int c4 = threadIdx.x % (D / 4);
+  // launched as a programmatic dependent of the decode grid: wait until its partials are visible
+  // (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (row < rows) {
     // One batch of up to 16 splits per round trip: every lse and partial of the batch is
     // loaded before any is used, so the L2/DRAM latencies overlap (a plain loop waits ~600
@@ -669,8 +673,22 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
   if (p.num_splits > 1) {
     const int rows = batch * p.hq;
     const int per_block = 128 / (D / 4);
-    decode_combine_kernel<D><<<(rows + per_block - 1) / per_block, 128, 0, st>>>(
-        p.part_o, p.part_lse, p.out, rows, p.num_splits, p.hq, p.sink);
+    static const bool pdl = [] {
+      const char* e = getenv("VATTN_DEC_PDL");
+      return !e || atoi(e) != 0;
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((rows + per_block - 1) / per_block);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    check_rt(cudaLaunchKernelEx(&cfg, decode_combine_kernel<D>, (const float*)p.part_o, (const float*)p.part_lse,
+                                p.out, rows, p.num_splits, p.hq, p.sink),
+             "combine launch");
     check_rt(cudaGetLastError(), "combine launch");
   }
 }
