@@ -370,8 +370,11 @@ int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t n_q_heads, int32_t h
  * (north_star: "NCCL over NVLink is used only for the final head all-gather when the caller
  * requests full outputs"; the reference has no multi-GPU code — every worker runs the same
  * allocator, geometry.py:96-98 kv_heads_per_worker).  The decode epilogue stores
- * each row into every rank's full output buffer over peer memory and signals; vattn_gather_wait
- * makes `stream` wait until all ranks' rows have landed. */
+ * each row into every rank's staging area (two, alternating per launch) over peer memory and
+ * signals; vattn_gather_wait makes `stream` wait until all ranks' rows have landed and copies the
+ * full output out.  Every rank issues the same sequence of gathered launches, each followed by a
+ * vattn_gather_wait on the same stream before its next gathered launch; the output then has the
+ * lifetime of any stream-ordered buffer (no peer writes into it). */
 #define VATTN_IPC_HANDLE_BYTES 64
 typedef struct vattn_gather vattn_gather_t;
 /* one per rank (collective setup): allocates this rank's full-output buffer of out_bytes
@@ -384,10 +387,14 @@ vattn_status vattn_gather_open(vattn_gather_t* g, const void* handles);
 /* `world` simulated ranks on one device in this process (out[world]); same kernels/protocol */
 vattn_status vattn_gather_create_local(int32_t device, int32_t world, int64_t out_bytes,
                                        vattn_gather_t** out);
-/* device address of this rank's full output [batch, Hq_total, D] bf16 */
+/* device address of this rank's front area [max_batch, Hq_total, D] bf16 (rank-local; the
+ * destination of vattn_gather_wait when out is NULL) */
 vattn_status vattn_gather_output(vattn_gather_t* g, uint64_t* dptr);
-/* stream-ordered: wait (bounded: 10 s, env VATTN_GATHER_TIMEOUT_MS) until every rank's latest gathered launch has landed */
-vattn_status vattn_gather_wait(vattn_gather_t* g, void* stream);
+/* stream-ordered: wait (bounded: 10 s, env VATTN_GATHER_TIMEOUT_MS) until every rank's latest
+ * gathered launch has landed, then copy the first out_bytes (batch * Hq_total * D * 2; multiple
+ * of 16) of the full output to out (16-byte aligned; NULL = the front area).  out_bytes 0: wait
+ * only. */
+vattn_status vattn_gather_wait(vattn_gather_t* g, void* out, int64_t out_bytes, void* stream);
 /* bit r set = the wait for rank r timed out (a rank skipped a launch) */
 vattn_status vattn_gather_check(vattn_gather_t* g, uint32_t* timed_out_mask);
 vattn_status vattn_gather_destroy(vattn_gather_t* g);

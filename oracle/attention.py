@@ -99,6 +99,20 @@ def max_rel_err(out, ref) -> float:
     return (out.float() - ref).abs().max().item() / max(denom, 1e-30)
 
 
+def elem_rel_err(out, ref, eps: float = 1e-3) -> float:
+    """Elementwise metric SURVEY §8(c) asks to report beside max_rel_err:
+    max over elements of |o - o_ref| / (|o_ref| + eps).  It is dominated by near-zero reference
+    elements (cancellation in the P·V sum), where a bf16-rounded P contributes an absolute error
+    of order 2^-9 · mean|v|; the tests bound it separately from the north-star metric."""
+    ref = ref.float()
+    return ((out.float() - ref).abs() / (ref.abs() + eps)).max().item()
+
+
+def err_report(out, ref) -> dict:
+    """Both metrics plus the element count, for test logs and bench extras."""
+    return {"max_rel_err": max_rel_err(out, ref), "elem_rel_err": elem_rel_err(out, ref), "elements": ref.numel()}
+
+
 def rotary_ref(x, cos, sin, positions, interleaved=False):
     """Rotary embedding of x [B, H, D] at per-row positions [B] (fp32 result).
 

@@ -153,7 +153,7 @@ SIGNATURES = {
     "vattn_gather_open": (c_i32, [c_vp, c_vp]),
     "vattn_gather_create_local": (c_i32, [c_i32, c_i32, c_i64, C.POINTER(c_vp)]),
     "vattn_gather_output": (c_i32, [c_vp, C.POINTER(c_u64)]),
-    "vattn_gather_wait": (c_i32, [c_vp, c_vp]),
+    "vattn_gather_wait": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "vattn_gather_check": (c_i32, [c_vp, C.POINTER(c_u32)]),
     "vattn_gather_destroy": (c_i32, [c_vp]),
     "vattn_decode_gather": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_f32, c_i32, c_vp]),

@@ -19,12 +19,46 @@ from . import _abi
 from ._abi import check, lib
 
 
-def _stream(stream=None) -> int:
+def _stream(stream=None, device: int | None = None) -> int:
     if stream is not None:
         return stream.cuda_stream
     # the raw handle of the current stream without building a torch.cuda.Stream object
     # (same value as torch.cuda.current_stream().cuda_stream, graph capture included; ~2 us less)
-    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice() if device is None else device)
+
+
+# Host-side shape checks of the manager-backed ops (no device->host copy): the kernels take head
+# counts and head_dim from the manager's geometry and the batch from q, so a mismatched tensor
+# would make them read or write past it (ADVICE r1 attention.py:103).
+def _geom(mgr):
+    g = mgr._g
+    return g.q_heads_per_worker, g.kv_heads_per_worker, g.head_dim
+
+
+def _on_mgr_device(mgr, *ts):
+    for t in ts:
+        if t is not None and (t.device.type != "cuda" or t.device.index != mgr.device):
+            raise ValueError(f"tensors must live on the manager's device cuda:{mgr.device}, got {t.device}")
+
+
+def _expect(t, shape, name):
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)} (manager geometry), got {tuple(t.shape)}")
+
+
+def _check_out(out, shape, device):
+    if (out.dtype != torch.bfloat16 or not out.is_contiguous() or tuple(out.shape) != tuple(shape)
+            or out.device != device):
+        raise ValueError(f"out must be a contiguous bf16 tensor of shape {tuple(shape)} on {device}")
+
+
+def _check_rows(batch, seq, idx):
+    if seq is None:
+        raise ValueError("cache_seqlens is required")
+    if seq.dim() != 1 or seq.numel() < batch:
+        raise ValueError(f"cache_seqlens must be a 1-D tensor with at least {batch} entries")
+    if idx is not None and (idx.dim() != 1 or idx.numel() < batch):
+        raise ValueError(f"cache_batch_idx must be a 1-D tensor with at least {batch} entries")
 
 
 def _need_cuda(*ts):
@@ -84,37 +118,60 @@ def kv_append(mgr, layer: int, k_new, v_new, cache_seqlens, cache_batch_idx=None
     mgr.step with the grown lengths first).  With rotary tables, k row i is cached rotated at
     position cache_seqlens[b] + i."""
     _need_cuda(k_new, v_new)
+    _on_mgr_device(mgr, k_new, v_new)
     if k_new.dim() == 3:
         k_new, v_new = k_new.unsqueeze(1), v_new.unsqueeze(1)
+    _, hkv, d = _geom(mgr)
+    if k_new.dim() != 4:
+        raise ValueError("k_new must be [B, T, Hkv, D] or [B, Hkv, D]")
+    _expect(k_new, (k_new.shape[0], k_new.shape[1], hkv, d), "k_new")
+    _expect(v_new, k_new.shape, "v_new")
     k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    _check_rows(k_new.shape[0], seq, idx)
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx, extra_rows=k_new.shape[1])
     rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    st = C.c_void_p(_stream(stream, mgr.device))
     if rot is not None:
         check(lib().vattn_kv_append_rotary(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
-                                           _ptr(seq), _ptr(idx), C.byref(rot), C.c_void_p(_stream(stream))))
+                                           _ptr(seq), _ptr(idx), C.byref(rot), st))
         return
     check(lib().vattn_kv_append(mgr._h, layer, _ptr(k_new), _ptr(v_new), k_new.shape[0], k_new.shape[1],
-                                _ptr(seq), _ptr(idx), C.c_void_p(_stream(stream))))
+                                _ptr(seq), _ptr(idx), st))
 
 
 def decode_attention(mgr, layer: int, q, cache_seqlens, cache_batch_idx=None, softmax_scale=None,
                      out=None, num_splits: int = 0, stream=None):
     """o[b] = softmax(q[b] K[slot, :seqlen]ᵀ·scale) V[slot, :seqlen] for q [B, Hq, D]."""
     _need_cuda(q)
+    _on_mgr_device(mgr, q)
+    hq, _, d = _geom(mgr)
+    _expect(q, (q.shape[0], hq, d), "q")
     q = _bf16(q, "q")
     if out is None:
         out = torch.empty_like(q)
+    else:
+        _check_out(out, q.shape, q.device)
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    _check_rows(q.shape[0], seq, idx)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx)
     check(lib().vattn_decode(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], _ptr(seq), _ptr(idx),
-                             float(scale), int(num_splits), C.c_void_p(_stream(stream))))
+                             float(scale), int(num_splits), C.c_void_p(_stream(stream, mgr.device))))
     return out
+
+
+def _check_decode_new(mgr, q, k_new, v_new):
+    """q [B, Hq_local, D]; k_new / v_new [B, Hkv_local, D] (one new token per row)."""
+    hq, hkv, d = _geom(mgr)
+    _expect(q, (q.shape[0], hq, d), "q")
+    if k_new is not None:
+        _expect(k_new, (q.shape[0], hkv, d), "k_new")
+        _expect(v_new, (q.shape[0], hkv, d), "v_new")
 
 
 def _rotary(rotary_cos, rotary_sin, rotary_interleaved):
@@ -142,50 +199,66 @@ def decode_attention_append(mgr, layer: int, q, k_new, v_new, cache_seqlens, cac
     rotary_cos / rotary_sin [positions, rotary_dim / 2]: q and k_new are rotated at position
     cache_seqlens[b] first and k is cached rotated (flash-attn's rotary semantics)."""
     _need_cuda(q, k_new, v_new)
+    _on_mgr_device(mgr, q, k_new, v_new)
+    _check_decode_new(mgr, q, k_new, v_new)
     q, k_new, v_new = _bf16(q, "q"), _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     if out is None:
         out = torch.empty_like(q)
+    else:
+        _check_out(out, q.shape, q.device)
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    _check_rows(q.shape[0], seq, idx)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx, extra_rows=1)
     rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    st = C.c_void_p(_stream(stream, mgr.device))
     if rot is not None:
         check(lib().vattn_decode_append_rotary(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
                                                q.shape[0], _ptr(seq), _ptr(idx), float(scale), int(num_splits),
-                                               C.byref(rot), C.c_void_p(_stream(stream))))
+                                               C.byref(rot), st))
         return out
     check(lib().vattn_decode_append(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), q.shape[0],
-                                    _ptr(seq), _ptr(idx), float(scale), int(num_splits), C.c_void_p(_stream(stream))))
+                                    _ptr(seq), _ptr(idx), float(scale), int(num_splits), st))
     return out
 
 
 def decode_attention_gather(mgr, layer: int, q, gather, cache_seqlens, cache_batch_idx=None, k_new=None,
-                            v_new=None, softmax_scale=None, num_splits: int = 0, wait: bool = True, stream=None):
+                            v_new=None, softmax_scale=None, num_splits: int = 0, wait: bool = True, stream=None,
+                            out=None):
     """Decode this rank's query heads q [B, Hq/G, D] (k_new/v_new given: fused append, as
     decode_attention_append) and all-gather the heads in the same kernel: every output row is
-    stored over NVLink peer memory into each rank's full output [B, Hq, D] at head offset
-    rank*Hq/G.  With wait=True the stream then waits for all ranks' rows; returns
-    the full-output view (`gather.output(B)`)."""
+    stored over NVLink peer memory into each rank's staging area [B, Hq, D] at head offset
+    rank*Hq/G.  With wait=True the stream then waits for all ranks' rows and the
+    full output is copied to `out` (default: the gather's front buffer, `gather.output(B)`),
+    which is returned; with wait=False call `gather.wait(stream, out)` before the next gathered
+    launch and returns None."""
     _need_cuda(q)
-    q = _bf16(q, "q")
     if (k_new is None) != (v_new is None):
         raise ValueError("k_new and v_new go together")
+    _on_mgr_device(mgr, q, k_new, v_new)
+    _check_decode_new(mgr, q, k_new, v_new)
+    if q.shape[1] * gather.world != gather.hq_total or q.shape[2] != gather.head_dim:
+        raise ValueError("q heads x gather world must equal the gather's Hq_total (and head_dim match)")
+    if q.shape[0] > gather.max_batch:
+        raise ValueError(f"batch {q.shape[0]} exceeds the gather's max_batch {gather.max_batch}")
+    q = _bf16(q, "q")
     if k_new is not None:
         _need_cuda(k_new, v_new)
         k_new, v_new = _bf16(k_new, "k_new"), _bf16(v_new, "v_new")
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
+    _check_rows(q.shape[0], seq, idx)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, seq, idx, extra_rows=0 if k_new is None else 1)
-    st = C.c_void_p(_stream(stream))
+    st = C.c_void_p(_stream(stream, mgr.device))
     check(lib().vattn_decode_gather(mgr._h, layer, _ptr(q), _ptr(k_new), _ptr(v_new), gather.handle, q.shape[0],
                                     _ptr(seq), _ptr(idx), float(scale), int(num_splits), st))
-    if wait:
-        gather.wait(stream)
-    return gather.output(q.shape[0])
+    if not wait:
+        return None
+    return gather.wait(stream, out=out, batch=None if out is not None else q.shape[0])
 
 
 def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None, causal=True,
@@ -195,20 +268,28 @@ def prefill_attention(mgr, layer: int, q, req_id: int, kv_len: int | None = None
     req_id (default kv_len = S, i.e. the prompt just appended).  With rotary tables, query row i
     is rotated at position kv_len - S + i inside the kernel (append k with the same tables)."""
     _need_cuda(q)
+    _on_mgr_device(mgr, q)
+    hq, _, d = _geom(mgr)
+    _expect(q, (q.shape[0], hq, d), "q")
     q = _bf16(q, "q")
     if out is None:
         out = torch.empty_like(q)
+    else:
+        _check_out(out, q.shape, q.device)
     kv_len = q.shape[0] if kv_len is None else kv_len
+    if not 0 <= int(req_id) < mgr._g.max_batch:
+        raise ValueError(f"req_id {req_id} is not a slot (max_batch {mgr._g.max_batch})")
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     if CHECK_BOUNDS:
         check_bounds(mgr, [kv_len], [req_id])
     rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
+    st = C.c_void_p(_stream(stream, mgr.device))
     if rot is not None:
         check(lib().vattn_prefill_rotary(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
-                                         float(scale), int(bool(causal)), C.byref(rot), C.c_void_p(_stream(stream))))
+                                         float(scale), int(bool(causal)), C.byref(rot), st))
         return out
     check(lib().vattn_prefill(mgr._h, layer, _ptr(q), _ptr(out), q.shape[0], int(req_id), int(kv_len),
-                              float(scale), int(bool(causal)), C.c_void_p(_stream(stream))))
+                              float(scale), int(bool(causal)), st))
     return out
 
 
@@ -233,14 +314,22 @@ def prefill_attention_varlen(mgr, layer: int, q, q_lens, req_ids, kv_lens=None, 
     Hq, D] packs each request's query rows in order; request i attends (bottom-right causal)
     over rows [0, kv_lens[i]) of slot req_ids[i] (default kv_lens = q_lens)."""
     _need_cuda(q)
+    _on_mgr_device(mgr, q)
+    hq, _, d = _geom(mgr)
+    _expect(q, (q.shape[0], hq, d), "q")
     q = _bf16(q, "q")
-    out = torch.empty_like(q) if out is None else out
+    if out is None:
+        out = torch.empty_like(q)
+    else:
+        _check_out(out, q.shape, q.device)
     n, st, nq, sl, kl = _varlen_arrays(q, q_lens, req_ids, kv_lens)
+    if any(not 0 <= int(r) < mgr._g.max_batch for r in req_ids):
+        raise ValueError(f"req_ids must be slots in [0, {mgr._g.max_batch})")
     if CHECK_BOUNDS:
         check_bounds(mgr, list(kv_lens if kv_lens is not None else q_lens), list(req_ids))
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(q.shape[-1])
     check(lib().vattn_prefill_varlen(mgr._h, layer, _ptr(q), _ptr(out), n, st, nq, sl, kl, float(scale),
-                                     int(bool(causal)), C.c_void_p(_stream(stream))))
+                                     int(bool(causal)), C.c_void_p(_stream(stream, mgr.device))))
     return out
 
 
@@ -295,13 +384,20 @@ def kv_append_raw(k_cache, v_cache, k_new, v_new, cache_seqlens, cache_batch_idx
 
 
 _ws_cache: dict = {}
+_ws_retired: list = []
 
 
-def _workspace(device, nbytes):
-    ws = _ws_cache.get(device)
+def _workspace(device, nbytes, stream=None):
+    """Split-K workspace of the raw ops, one per (device, launching stream): two streams never
+    share partials.  A grown workspace retires the old one without freeing it, since a CUDA
+    graph may have captured its address."""
+    key = (device, _stream(stream))
+    ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
+        if ws is not None:
+            _ws_retired.append(ws)
         ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-        _ws_cache[device] = ws
+        _ws_cache[key] = ws
     return ws
 
 
@@ -314,7 +410,7 @@ def decode_attention_raw(q, k_cache, v_cache, cache_seqlens, cache_batch_idx=Non
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     b, hq, d = q.shape
     nbytes = lib().vattn_decode_workspace_bytes(b, hq, d, 0)
-    ws = _workspace(q.device, nbytes)
+    ws = _workspace(q.device, nbytes, stream)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
     check(lib().vattn_decode_raw(C.byref(desc), _ptr(q), _ptr(out), b, hq, _ptr(seq), _ptr(idx), float(scale),
                                  int(num_splits), _ptr(ws), ws.numel(), C.c_void_p(_stream(stream))))
@@ -330,7 +426,7 @@ def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     b, hq, d = q.shape
-    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0))
+    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0), stream)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
     rot, _keep = _rotary(rotary_cos, rotary_sin, rotary_interleaved)
     if rot is not None:
@@ -346,7 +442,7 @@ def decode_attention_append_raw(q, k_cache, v_cache, k_new, v_new, cache_seqlens
 
 def decode_attention_gather_raw(q, k_cache, v_cache, gather, cache_seqlens, cache_batch_idx=None, k_new=None,
                                 v_new=None, softmax_scale=None, num_splits: int = 0, wait: bool = True,
-                                stream=None):
+                                stream=None, out=None):
     """decode_attention_gather on caller-owned caches (see cache_desc)."""
     desc = cache_desc(k_cache, v_cache)
     q = _bf16(q, "q")
@@ -355,14 +451,14 @@ def decode_attention_gather_raw(q, k_cache, v_cache, gather, cache_seqlens, cach
     seq = _i32(cache_seqlens, "cache_seqlens")
     idx = _i32(cache_batch_idx, "cache_batch_idx")
     b, hq, d = q.shape
-    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0))
+    ws = _workspace(q.device, lib().vattn_decode_workspace_bytes(b, hq, d, 0), stream)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
     check(lib().vattn_decode_gather_raw(C.byref(desc), _ptr(q), _ptr(k_new), _ptr(v_new), gather.handle, b, hq,
                                         _ptr(seq), _ptr(idx), float(scale), int(num_splits), _ptr(ws), ws.numel(),
                                         C.c_void_p(_stream(stream))))
-    if wait:
-        gather.wait(stream)
-    return gather.output(b)
+    if not wait:
+        return None
+    return gather.wait(stream, out=out, batch=None if out is not None else b)
 
 
 def decode_attention_paged(q, k_pool, v_pool, block_table, seqlens, softmax_scale=None, out=None,
@@ -378,7 +474,7 @@ def decode_attention_paged(q, k_pool, v_pool, block_table, seqlens, softmax_scal
     b, hq, d = q.shape
     nb, bs, hkv, _ = k_pool.shape
     nbytes = lib().vattn_decode_workspace_bytes(b, hq, d, 0)
-    ws = _workspace(q.device, nbytes)
+    ws = _workspace(q.device, nbytes, stream)
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
     check(lib().vattn_decode_paged(_ptr(q), _ptr(k_pool), _ptr(v_pool), nb, bs, hkv, d, _ptr(bt), bt.shape[1],
                                    _ptr(out), b, hq, _ptr(seq), float(scale), int(num_splits), _ptr(ws),

@@ -353,7 +353,10 @@ class Manager {
   CUmemAllocationProp prop_{};
   CUmemAccessDesc access_{};
   std::vector<int64_t> run_begin_, run_end_;  // pending cuMemSetAccess page runs per buffer
-  cudaEvent_t use_event_ = nullptr;
+  // Unmap fence: one "last use" event per stream that launched kernels on this cache (a reclaim
+  // or trim must wait for decode on stream A and prefill on stream B alike).
+  std::mutex use_mu_;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> use_events_;
   std::atomic<bool> use_recorded_{false};
   bool fenced_ = false;
   // measured real-driver statistics
@@ -471,7 +474,6 @@ Manager::Manager(const vattn_config& c) {
       throw Fail(VATTN_UNSUPPORTED, "page-group size is not a multiple of the driver granularity");
     access_.location = prop_.location;
     access_.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    check_rt(cudaEventCreateWithFlags(&use_event_, cudaEventDisableTiming), "cudaEventCreate");
   }
 
   buf_maps_.resize(buffer_count_);
@@ -580,7 +582,7 @@ Manager::~Manager() {
   }
   for (auto h : phys_free_) d.MemRelease(h);
   for (size_t b = 0; b < va_.size(); ++b) d.MemAddressFree(va_[b], (size_t)buffer_size_);
-  if (use_event_) cudaEventDestroy(use_event_);
+  for (auto& se : use_events_) cudaEventDestroy(se.second);
 }
 
 // ---- shadow driver ------------------------------------------------------------------------
@@ -939,7 +941,14 @@ void Manager::fence_unmap() {
   // Never unmap a page that queued kernels may still read (SURVEY §7 hard part 3).
   if (fenced_) return;
   flush_access();
-  if (use_recorded_) check_rt(cudaEventSynchronize(use_event_), "cudaEventSynchronize(unmap fence)");
+  if (use_recorded_) {
+    std::vector<cudaEvent_t> evs;
+    {
+      std::lock_guard<std::mutex> lk(use_mu_);
+      for (auto& se : use_events_) evs.push_back(se.second);
+    }
+    for (cudaEvent_t e : evs) check_rt(cudaEventSynchronize(e), "cudaEventSynchronize(unmap fence)");
+  }
   fenced_ = true;
 }
 
@@ -957,10 +966,22 @@ void Manager::mark_use(cudaStream_t st) {
   // external record becomes a graph node, so every replay re-arms the unmap fence.
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   check_rt(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+  std::lock_guard<std::mutex> lk(use_mu_);
+  cudaEvent_t ev = nullptr;
+  for (auto& se : use_events_)
+    if (se.first == st) ev = se.second;
+  if (!ev) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;   // first use may be inside a capture
+    check_rt(cudaThreadExchangeStreamCaptureMode(&mode), "cudaThreadExchangeStreamCaptureMode");
+    const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    check_rt(e, "cudaEventCreate(use)");
+    use_events_.emplace_back(st, ev);
+  }
   if (cs == cudaStreamCaptureStatusActive)
-    check_rt(cudaEventRecordWithFlags(use_event_, st, cudaEventRecordExternal), "cudaEventRecord(use, graph)");
+    check_rt(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal), "cudaEventRecord(use, graph)");
   else
-    check_rt(cudaEventRecord(use_event_, st), "cudaEventRecord(use)");
+    check_rt(cudaEventRecord(ev, st), "cudaEventRecord(use)");
   use_recorded_ = true;
 }
 
@@ -1421,14 +1442,11 @@ uint64_t Manager::buffer_base(int32_t b) const {
 }
 
 // The decode kernels stream 64-token TMA boxes (kernels.cu kTile); a box that starts below a
-// row's length must end inside its mapped page-groups, which holds for every length only when a
-// page-group spans a whole number of 64-token tiles.
-void Manager::check_decode_tiling() const {
-  if (t_ % (64 * per_buffer_token_bytes_) != 0)
-    throw Fail(VATTN_UNSUPPORTED, "decode kernels need page-groups of a whole number of 64-token tiles (page-group " +
-                                      std::to_string(t_) + " B, token row " + std::to_string(per_buffer_token_bytes_) +
-                                      " B); prefill and append have no such constraint");
-}
+// row's length ends inside its mapped page-groups for every length only when a page-group spans
+// a whole number of 64-token tiles.  Otherwise (layer-sliced layout: 32 tokens per 2 MiB group at
+// Llama-3-8B, 17.07 at Yi-34B) layer_view sets tail_guard and the kernels load each row's last,
+// partial tile with per-row loads bounded by the row's length.
+void Manager::check_decode_tiling() const {}
 
 CacheView Manager::layer_view(int32_t layer) const {
   if (!real()) throw Fail(VATTN_BAD_STATE, "kernels need the CUDA backend");
@@ -1446,6 +1464,7 @@ CacheView Manager::layer_view(int32_t layer) const {
     v.token_stride = row;
   }
   v.slot_stride = slot_stride_;
+  v.tail_guard = (t_ % (64 * per_buffer_token_bytes_) != 0) ? 1 : 0;
   v.slot_tokens = (int32_t)max_context_;
   v.n_slots = (int32_t)slots_.size();
   v.hkv = hkv_local_;
@@ -1475,9 +1494,36 @@ using vattn::Manager;
 
 struct vattn_t {
   Manager* m = nullptr;
-  void* workspace = nullptr;
-  int64_t workspace_bytes = 0;
+  // Split-K decode workspaces, one per launching stream (concurrent decodes on two streams must
+  // not share part_o/part_lse).  Never freed before vattn_destroy: a CUDA graph captured with a
+  // workspace keeps its address, so a grown one only retires the old (ADVICE r1 core.cpp:1783).
+  std::mutex ws_mu;
+  std::unordered_map<cudaStream_t, std::pair<void*, int64_t>> ws;
+  std::vector<void*> ws_all;
 };
+
+// Workspace for a decode of `need` bytes on stream st.  The first one of a stream is sized for the
+// manager's max_batch, so it normally never grows; cudaMalloc runs with the thread's capture mode
+// relaxed, so a first decode inside a graph capture is legal too.
+static void* decode_workspace(vattn_t* h, cudaStream_t st, int64_t need, int64_t max_need, int64_t* bytes) {
+  std::lock_guard<std::mutex> lk(h->ws_mu);
+  auto it = h->ws.find(st);
+  if (it != h->ws.end() && it->second.second >= need) {
+    *bytes = it->second.second;
+    return it->second.first;
+  }
+  const int64_t size = std::max(need, max_need);
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  vattn::check_rt(cudaThreadExchangeStreamCaptureMode(&mode), "cudaThreadExchangeStreamCaptureMode");
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, (size_t)size);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  vattn::check_rt(e, "cudaMalloc(decode workspace)");
+  h->ws_all.push_back(p);
+  h->ws[st] = {p, size};
+  *bytes = size;
+  return p;
+}
 
 template <typename F>
 static vattn_status guard(F&& f) {
@@ -1537,7 +1583,7 @@ vattn_status vattn_destroy(vattn_t* h) {
       if (h->m->ks) vattn::kernel_state_free(h->m->ks);
       delete h->m;
     }
-    if (h->workspace) cudaFree(h->workspace);
+    for (void* p : h->ws_all) cudaFree(p);
     delete h;
   });
 }
@@ -1779,16 +1825,11 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
-    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
-    if (need > h->workspace_bytes) {
-      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
-      h->workspace = nullptr;
-      h->workspace_bytes = 0;
-      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
-      h->workspace_bytes = need;
-    }
+    int64_t ws_bytes = 0;
+    void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
+                                vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, seqlens, batch_idx, scale,
-                         num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream);
+                         num_splits, ws, ws_bytes, (cudaStream_t)stream);
     h->m->mark_use((cudaStream_t)stream);
   });
 }
@@ -1803,16 +1844,11 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
-    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
-    if (need > h->workspace_bytes) {
-      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
-      h->workspace = nullptr;
-      h->workspace_bytes = 0;
-      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
-      h->workspace_bytes = need;
-    }
+    int64_t ws_bytes = 0;
+    void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
+                                vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
-                         num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new);
+                         num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
     h->m->mark_use((cudaStream_t)stream);
   });
 }
@@ -1869,17 +1905,12 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
-    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
-    if (need > h->workspace_bytes) {
-      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
-      h->workspace = nullptr;
-      h->workspace_bytes = 0;
-      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
-      h->workspace_bytes = need;
-    }
+    int64_t ws_bytes = 0;
+    void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
+                                vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale, num_splits,
-                         h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
+                         ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
     h->m->mark_use((cudaStream_t)stream);
   });
 }
@@ -1894,17 +1925,12 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
-    const int64_t need = vattn_decode_workspace_bytes(batch, hq, v.d, 0);
-    if (need > h->workspace_bytes) {
-      if (h->workspace) vattn::check_rt(cudaFree(h->workspace), "cudaFree(workspace)");
-      h->workspace = nullptr;
-      h->workspace_bytes = 0;
-      vattn::check_rt(cudaMalloc(&h->workspace, (size_t)need), "cudaMalloc(workspace)");
-      h->workspace_bytes = need;
-    }
+    int64_t ws_bytes = 0;
+    void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
+                                vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     const vattn::GatherSink s = vattn::gather_sink(g, hq, batch, v.d);
     vattn::launch_decode(h->m->ks, layer, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale,
-                         num_splits, h->workspace, h->workspace_bytes, (cudaStream_t)stream, k_new, v_new, &s);
+                         num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, &s);
     h->m->mark_use((cudaStream_t)stream);
   });
 }

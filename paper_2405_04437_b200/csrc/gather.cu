@@ -1,14 +1,22 @@
 // Fused head all-gather over NVLink peer memory (north_star: "NCCL over NVLink is
 // used only for the final head all-gather when the caller requests full outputs").
 //
-// Each rank (one process per GPU) owns one device buffer: its full decode output
-// [max_batch, Hq_total, D] bf16 followed by a small signal area.  Ranks exchange CUDA IPC
-// handles once (the host side does it over torch.distributed) and map every peer's buffer.
-// The decode kernel (kernels.cu, GatherSink) then writes each output row of its head shard
-// directly into every rank's buffer as it is produced and raises its flag in every peer's
-// signal area when its grid is done; `vattn_gather_wait` launches one tiny kernel that spins
-// (bounded) until all ranks' flags reached this launch's epoch.  There is no separate copy
-// step: the transfer overlaps the attention of the CTAs still running.
+// Each rank (one process per GPU) owns one device buffer: two staging areas of its full decode
+// output [max_batch, Hq_total, D] bf16, a rank-local front area, and a small signal area.  Ranks
+// exchange CUDA IPC handles once (the host side does it over torch.distributed) and map every
+// peer's buffer.  The decode kernel (kernels.cu, GatherSink) writes each output row of its head
+// shard directly into every rank's staging area of the launch's parity as it is produced, and
+// raises its flag in every peer's signal area when its grid is done; `vattn_gather_wait` then
+// spins (bounded) until all ranks' flags reached this launch's epoch and copies the staging area
+// into the caller's output (or the front area) on the caller's stream.
+//
+// Why two staging areas (write-after-read across ranks): rank A's launch e+1 may start as soon as
+// A's wait for e saw every rank's rows of e.  A peer B may still be reading its launch-e output
+// then (a slow consumer), so e+1 must not write where e's rows are: it writes the other parity.
+// A's launch e+2, which does reuse e's area, starts only after A's wait for e+1 saw B's rows of
+// e+1, and B issued its launch e+1 after its wait for e, which had finished copying e's area
+// out (same stream).  The consumer never reads a staging area directly, so its own reads are
+// ordered by its stream alone, exactly as with the NCCL all_gather this replaces.
 //
 // A "local" group places all `world` buffers on one device inside one process; it runs the
 // identical kernels and protocol (peer pointers are simply local) and is how the single-GPU
@@ -30,7 +38,9 @@
 struct vattn_gather {
   int device = 0, rank = 0, world = 1;
   bool local_group = false;
-  int64_t out_bytes = 0;       // bytes of the full output region
+  int64_t out_bytes = 0;       // bytes of one full output region [max_batch, Hq_total, D]
+  int64_t stage_bytes = 0;     // staging area 1 offset (= area stride, 256-aligned)
+  int64_t front_off = 0;       // rank-local front area (default destination of the wait copy)
   int64_t sig_off = 0;         // signal area offset inside every buffer
   void* base = nullptr;        // own buffer (owned)
   void* peer[vattn::kMaxGatherRanks] = {};
@@ -56,31 +66,46 @@ uint32_t* error_of(void* buf, int64_t sig_off) {
   return reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + sig_off + 384);
 }
 
-// One thread per source rank: wait until rank r's flag in our signal area reached our own
-// launch count (advanced by our last gathered launch, earlier on this stream).  Bounded: after
-// timeout_ns it records a timeout instead of hanging the device.
-__global__ void gather_wait_kernel(const uint32_t* flags, int world, const uint32_t* epoch_ptr, uint32_t* err,
-                                   uint64_t timeout_ns) {
+// Every CTA: one thread per source rank waits until rank r's flag in our signal area reached our
+// own launch count (advanced by our last gathered launch, earlier on this stream); then the CTA
+// copies its share of staging area (count & 1) to `out` with 16-byte loads and stores.  Bounded:
+// after timeout_ns a waiter records a timeout instead of hanging the device (the copy then
+// delivers whatever landed; vattn_gather_check reports the ranks).
+__global__ void __launch_bounds__(256) gather_wait_kernel(const char* base, int64_t stage_bytes, const uint32_t* flags,
+                                                          int world, const uint32_t* epoch_ptr, uint32_t* err,
+                                                          uint64_t timeout_ns, uint4* out, int64_t chunks) {
   const int r = threadIdx.x;
-  if (r >= world) return;
   const uint32_t epoch = *epoch_ptr;
-  uint64_t t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (true) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
-    if ((int32_t)(v - epoch) >= 0) break;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > timeout_ns) {
-      atomicOr(err, 1u << r);
-      break;
+  if (r < world) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicOr(err, 1u << r);
+        break;
+      }
+      __nanosleep(200);
     }
-    __nanosleep(200);
+  }
+  __syncthreads();
+  if (!out) return;
+  const uint4* src = reinterpret_cast<const uint4*>(base + ((epoch & 1) ? stage_bytes : 0));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 v;
+    // peers wrote these bytes over NVLink; the acquire above orders them: bypass L1
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i));
+    out[i] = v;
   }
 }
 
 void alloc_buffer(vattn_gather* g) {
-  g->sig_off = (g->out_bytes + 255) / 256 * 256;
+  g->stage_bytes = (g->out_bytes + 255) / 256 * 256;
+  g->front_off = 2 * g->stage_bytes;
+  g->sig_off = 3 * g->stage_bytes;
   check_rt(cudaMalloc(&g->base, (size_t)(g->sig_off + kSigBytes)), "cudaMalloc(gather buffer)");
   check_rt(cudaMemset(g->base, 0, (size_t)(g->sig_off + kSigBytes)), "cudaMemset(gather buffer)");
 }
@@ -111,6 +136,7 @@ GatherSink gather_sink(vattn_gather* g, int hq_local, int batch, int head_dim) {
   }
   s.counter = counter_of(g->base, g->sig_off);
   s.epoch = epoch_of(g->base, g->sig_off);
+  s.stage_bytes = g->stage_bytes;
   s.n_ranks = g->world;
   s.rank = g->rank;
   s.hq_total = hq_local * g->world;
@@ -204,18 +230,26 @@ vattn_status vattn_gather_create_local(int32_t device, int32_t world, int64_t ou
 vattn_status vattn_gather_output(vattn_gather_t* g, uint64_t* dptr) {
   return gguard([&] {
     if (!g || !dptr) throw Fail(VATTN_VALUE_ERROR, "null argument");
-    *dptr = reinterpret_cast<uint64_t>(g->base);
+    *dptr = reinterpret_cast<uint64_t>(static_cast<char*>(g->base) + g->front_off);
   });
 }
 
-vattn_status vattn_gather_wait(vattn_gather_t* g, void* stream) {
+vattn_status vattn_gather_wait(vattn_gather_t* g, void* out, int64_t out_bytes, void* stream) {
   return gguard([&] {
     if (!g) throw Fail(VATTN_VALUE_ERROR, "null gather handle");
+    if (out_bytes < 0 || out_bytes > g->out_bytes || out_bytes % 16)
+      throw Fail(VATTN_VALUE_ERROR, "gather wait: out_bytes must be a multiple of 16 and at most the buffer size");
+    if (out && reinterpret_cast<uintptr_t>(out) % 16) throw Fail(VATTN_VALUE_ERROR, "gather wait: out must be 16-byte aligned");
+    if (!out) out = static_cast<char*>(g->base) + g->front_off;
     uint64_t timeout = vattn::kWaitTimeoutNs;
     if (const char* e = getenv("VATTN_GATHER_TIMEOUT_MS")) timeout = (uint64_t)std::max(1L, atol(e)) * 1000000ull;
-    vattn::gather_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
-        vattn::flags_of(g->base, g->sig_off), g->world, vattn::epoch_of(g->base, g->sig_off),
-        vattn::error_of(g->base, g->sig_off), timeout);
+    const int64_t chunks = out_bytes / 16;
+    // ~8 chunks per thread, at most one wave of 148 x 256 threads (one CTA when nothing to copy)
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, (chunks + 2047) / 2048));
+    vattn::gather_wait_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        static_cast<const char*>(g->base), g->stage_bytes, vattn::flags_of(g->base, g->sig_off), g->world,
+        vattn::epoch_of(g->base, g->sig_off), vattn::error_of(g->base, g->sig_off), timeout,
+        chunks ? static_cast<uint4*>(out) : nullptr, chunks);
     vattn::check_rt(cudaGetLastError(), "gather wait launch");
   });
 }

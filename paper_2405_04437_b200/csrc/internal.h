@@ -62,6 +62,10 @@ struct CacheView {
   int32_t n_slots = 0;
   int32_t hkv = 0;
   int32_t d = 0;
+  // 1 = rows past a slot's length may sit in an unmapped page-group (a page-group is not a whole
+  // number of 64-token decode tiles, e.g. the layer-sliced layout, manager.py:93-96): the decode
+  // kernels then load a row's last, partial tile with bounded per-row loads instead of one TMA box
+  int32_t tail_guard = 0;
 };
 
 CacheView view_from_desc(const vattn_cache_desc* c);
@@ -86,9 +90,10 @@ KernelState* kernel_state_new();
 void kernel_state_free(KernelState*);
 
 // Fused head all-gather (gather.cu): the decode epilogue stores every output row
-// straight into each rank's full [batch, Hq_total, D] buffer over NVLink peer memory (P2P
-// stores) at head offset rank*Hq_local, then the last CTA to finish raises this rank's flag in
-// every peer's signal array.  n_ranks = 0 disables it (plain local output).
+// straight into each rank's [batch, Hq_total, D] staging area of this launch's parity over
+// NVLink peer memory (16-byte P2P stores) at head offset rank*Hq_local, then the last CTA to
+// finish raises this rank's flag in every peer's signal array.  n_ranks = 0 disables it (plain
+// local output).
 // Rotary embedding applied by the fused append+decode kernel to q and the new k at the token's
 // position (flash_attn_with_kvcache rotary_cos / rotary_sin / rotary_interleaved semantics).
 struct Rotary {
@@ -100,11 +105,13 @@ struct Rotary {
 
 constexpr int kMaxGatherRanks = 8;
 struct GatherSink {
-  void* dst[kMaxGatherRanks];          // rank r's full output (peer-mapped; own included)
+  void* dst[kMaxGatherRanks];          // rank r's staging area 0 (peer-mapped; own included)
   uint32_t* flags[kMaxGatherRanks];    // rank r's signal words, indexed by the writing rank
   uint32_t* counter;                   // this rank's CTA-completion counter (reset by the last CTA)
   uint32_t* epoch;                     // this rank's launch count, advanced on the device by the
                                        // last CTA (graph-replay safe: no host-side epoch)
+  int64_t stage_bytes;                 // staging area 1 = dst[r] + stage_bytes; launch e writes
+                                       // area e & 1 (double buffer: see gather.cu)
   int32_t n_ranks, rank, hq_total, head_off;
 };
 

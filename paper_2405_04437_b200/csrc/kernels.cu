@@ -131,19 +131,26 @@ struct DecodeParams {
   int64_t slot_stride, token_stride;
   GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
   int32_t longest_first;        // schedule rows by descending length (B <= 256)
+  int32_t tail_guard;           // contiguous: load a row's partial last tile per row (CacheView)
   Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
 };
 
 
 // ---- fused head all-gather epilogue (gather.cu owns the buffers and the wait) ----
-// Output row (b, local head h) goes to row (b, head_off + h) of every rank's full output: one
-// 2-byte P2P store per rank over NVLink, issued as each element is produced, so the exchange
-// overlaps the other CTAs' attention instead of following it.
-__device__ __forceinline__ void sink_store(const GatherSink& s, int b, int head, int c, int D,
-                                           __nv_bfloat16 v) {
-  const int64_t idx = ((int64_t)b * s.hq_total + s.head_off + head) * D + c;
+// Output row (b, local head h) goes to row (b, head_off + h) of every rank's staging area of
+// this launch's parity: one 16-byte P2P store per rank and 8 elements over NVLink, issued as the
+// chunk is produced, so the exchange overlaps the other CTAs' attention instead of following it.
+// The parity is (own launch count + 1) & 1; the count only moves when the last CTA of this launch
+// signals, after every store of it (sink_signal), so all CTAs read the same value.
+__device__ __forceinline__ int64_t sink_parity_off(const GatherSink& s) {
+  return ((*reinterpret_cast<volatile uint32_t*>(s.epoch) + 1) & 1) ? s.stage_bytes : 0;
+}
+template <typename V>
+__device__ __forceinline__ void sink_store(const GatherSink& s, int64_t par_off, int b, int head, int c, int D,
+                                           V v) {
+  const int64_t off = par_off + (((int64_t)b * s.hq_total + s.head_off + head) * D + c) * 2;
 #pragma unroll 1
-  for (int r = 0; r < s.n_ranks; ++r) reinterpret_cast<__nv_bfloat16*>(s.dst[r])[idx] = v;
+  for (int r = 0; r < s.n_ranks; ++r) *reinterpret_cast<V*>(static_cast<char*>(s.dst[r]) + off) = v;
 }
 
 // Called by all `nthreads` threads of a CTA (named barrier 1) after their last sink_store.
@@ -233,17 +240,45 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
   __syncthreads();
 
   if (warp == CW) {
-    // ===== TMA producer =====
-    if (lane == 0 && n_tiles > 0) {
-      ptx::prefetch_tmap(&kmap);
-      ptx::prefetch_tmap(&vmap);
+    // ===== TMA producer (lane 0; the whole warp for a guarded tail tile) =====
+    if (n_tiles > 0) {
+      if (lane == 0) {
+        ptx::prefetch_tmap(&kmap);
+        ptx::prefetch_tmap(&vmap);
+      }
       for (int it = 0; it < n_tiles; ++it) {
         const int st = it % STAGES;
         if (it >= STAGES) ptx::mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
         uint8_t* ks = smem + st * L::kStageBytes;
         uint8_t* vs = ks + L::kTileBytes;
-        ptx::mbar_arrive_expect_tx(&full[st], L::kStageBytes);
         const int tok0 = (tile_begin + it) * kTile;
+        if (!PAGED && p.tail_guard && tok0 + kTile > seqlen) {
+          // The row's last tile where rows past its length may be unmapped (a page-group holds
+          // a non-multiple of 64 tokens): 16-byte loads of rows [tok0, seqlen) only, stored in
+          // the TMA box's 128B-swizzled layout; the consumers mask the rest.  Generic-proxy
+          // writes; the arrive (release) after __syncwarp publishes them.
+          const int rows = seqlen - tok0;
+          const char* kb = reinterpret_cast<const char*>(p.k_cache) + (int64_t)slot * p.slot_stride +
+                           (int64_t)kvh * D * 2;
+          const char* vb = reinterpret_cast<const char*>(p.v_cache) + (int64_t)slot * p.slot_stride +
+                           (int64_t)kvh * D * 2;
+          const uint32_t ks_a = ptx::smem_u32(ks), vs_a = ptx::smem_u32(vs);
+          for (int i = lane; i < rows * (D / 8); i += 32) {
+            const int r = i / (D / 8), c = i % (D / 8);
+            const int64_t off = (int64_t)(tok0 + r) * p.token_stride + c * 16;
+            const uint4 kv = *reinterpret_cast<const uint4*>(kb + off);
+            const uint4 vv = *reinterpret_cast<const uint4*>(vb + off);
+            const uint32_t ka = ptx::swz128(ks_a + (c >> 3) * L::kHalfBytes, r, c & 7);
+            const uint32_t va = ptx::swz128(vs_a + (c >> 3) * L::kHalfBytes, r, c & 7);
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ka), "r"(kv.x), "r"(kv.y), "r"(kv.z), "r"(kv.w));
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(va), "r"(vv.x), "r"(vv.y), "r"(vv.z), "r"(vv.w));
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&full[st]);
+          continue;
+        }
+        if (lane != 0) continue;
+        ptx::mbar_arrive_expect_tx(&full[st], L::kStageBytes);
         if constexpr (!PAGED) {
 #pragma unroll
           for (int h = 0; h < D / 64; ++h) {
@@ -449,27 +484,39 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
     r1[1] = o[n][3] * sc1;
   }
   asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
-  for (int i = threadIdx.x; i < p.group * D; i += CW * 32) {
-    const int r = i / D, c = i % D;
+  const int64_t par_off = (p.sink.n_ranks && p.num_splits == 1) ? sink_parity_off(p.sink) : 0;
+  // 8 consecutive output elements per thread-iteration: 16-byte stores (local or P2P)
+  for (int i = threadIdx.x; i < p.group * (D / 8); i += CW * 32) {
+    const int r = i / (D / 8), c = (i % (D / 8)) * 8;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < CW; ++w) M = fmaxf(M, red_m[w * 16 + r]);
-    float lsum = 0.f, acc = 0.f;
+    float lsum = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int w = 0; w < CW; ++w) {
       const float mw = red_m[w * 16 + r];
       const float f = (M == -INFINITY) ? 0.f : ptx::fast_exp2(mw - M);
       lsum += red_l[w * 16 + r] * f;
-      acc += scratch[(w * 16 + r) * D + c];
+      const float4* src = reinterpret_cast<const float4*>(scratch + (w * 16 + r) * D + c);
+      const float4 a = src[0], bb = src[1];
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += bb.x; acc[5] += bb.y; acc[6] += bb.z; acc[7] += bb.w;
     }
-    const float val = lsum > 0.f ? acc / lsum : 0.f;
+    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
     const int head = kvh * p.group + r;
     if (p.num_splits == 1) {
-      if (p.sink.n_ranks) sink_store(p.sink, b, head, c, D, __float2bfloat16(val));
-      else p.out[((int64_t)b * p.hq + head) * D + c] = __float2bfloat16(val);
+      uint4 pk;
+      pk.x = ptx::pack_bf16(acc[0] * inv, acc[1] * inv);
+      pk.y = ptx::pack_bf16(acc[2] * inv, acc[3] * inv);
+      pk.z = ptx::pack_bf16(acc[4] * inv, acc[5] * inv);
+      pk.w = ptx::pack_bf16(acc[6] * inv, acc[7] * inv);
+      if (p.sink.n_ranks) sink_store(p.sink, par_off, b, head, c, D, pk);
+      else *reinterpret_cast<uint4*>(p.out + ((int64_t)b * p.hq + head) * D + c) = pk;
     } else {
       const int64_t row = ((int64_t)b * p.hq + head) * p.num_splits + split;
-      p.part_o[row * D + c] = val;
+      float4* dst = reinterpret_cast<float4*>(p.part_o + row * D + c);
+      dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
       if (c == 0) p.part_lse[row] = lsum > 0.f ? M + log2f(lsum) : -INFINITY;
     }
   }
@@ -540,10 +587,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
     if (sink.n_ranks == 0) {
       *reinterpret_cast<uint2*>(out + (int64_t)row * D + c4 * 4) = pk;
     } else {
-      const int64_t idx = ((int64_t)(row / hq) * sink.hq_total + sink.head_off + row % hq) * D + c4 * 4;
-#pragma unroll 1
-      for (int r = 0; r < sink.n_ranks; ++r)
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sink.dst[r]) + idx) = pk;
+      sink_store(sink, sink_parity_off(sink), row / hq, row % hq, c4 * 4, D, pk);
     }
   }
   if (sink.n_ranks) sink_signal(sink, gridDim.x, blockDim.x);
@@ -737,16 +781,17 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   p.longest_first = (lf && batch > 1 && batch <= 256) ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)d);
   p.scale_log2 = scale * 1.4426950408889634f;
-  if (fa) {
-    p.k_new = reinterpret_cast<const __nv_bfloat16*>(fa->k_new);
+  if (fa) {   // contiguous cache: row addresses for the fused append and the guarded tail tile
+    p.k_new = reinterpret_cast<const __nv_bfloat16*>(fa->k_new);   // nullptr: plain decode
     p.v_new = reinterpret_cast<const __nv_bfloat16*>(fa->v_new);
     p.k_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->k_base);
     p.v_cache = reinterpret_cast<__nv_bfloat16*>(fa->view->v_base);
     p.slot_stride = fa->view->slot_stride;
     p.token_stride = fa->view->token_stride;
+    p.tail_guard = fa->view->tail_guard;
   }
   if (rot && rot->cos) {
-    if (!fa) throw Fail(VATTN_VALUE_ERROR, "rotary embedding needs the fused append (k_new / v_new)");
+    if (!fa || !fa->k_new) throw Fail(VATTN_VALUE_ERROR, "rotary embedding needs the fused append (k_new / v_new)");
     if (!rot->sin || rot->dim <= 0 || rot->dim % 16 || rot->dim > d)
       throw Fail(VATTN_VALUE_ERROR, "rotary_dim must be a positive multiple of 16 and <= head_dim");
     p.rot = *rot;
@@ -811,7 +856,7 @@ void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void
   const CUtensorMap vm = cached_map(ks, v.v_base, v.d, v.hkv, v.token_stride, tokens, v.slot_stride, v.n_slots, kTile);
   FusedAppend fa{k_new, v_new, &v};
   decode_common(km, vm, v.d, v.hkv, hq, q, out, batch, seqlens, batch_idx, nullptr, 0, 0, kTile,
-                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, k_new ? &fa : nullptr, sink, rot);
+                scale, num_splits, v.slot_tokens, ws, ws_bytes, false, st, &fa, sink, rot);
 }
 
 }  // namespace vattn

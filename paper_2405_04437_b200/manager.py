@@ -404,8 +404,9 @@ class KVCacheManager:
                                 r.bg_wall_us, r.waited_us)
 
     def mark_use(self, stream=None) -> None:
-        """Fence for unmaps: work queued on `stream` so far may read the cache."""
-        check(lib().vattn_mark_use(self._h, C.c_void_p(_stream_ptr(stream))))
+        """Fence for unmaps: work queued on `stream` (default: the current stream of the
+        manager's device) so far may read the cache."""
+        check(lib().vattn_mark_use(self._h, C.c_void_p(_stream_ptr(stream, self.device))))
 
     # -- parity introspection ---------------------------------------------------------------
     def drain_events(self) -> list[list[int]]:
@@ -479,14 +480,19 @@ class KVCacheManager:
         g = self._g
         if not 0 <= layer < g.n_layers:
             raise ValueError("layer out of range")
+        if g.bytes_per_elem != 2:
+            raise ValueError(f"cache views are bfloat16; this geometry has {g.bytes_per_elem}-byte elements")
         row = g.kv_heads_per_worker * g.head_dim          # elements per token row, one layer
         if self.config.sliced:
+            # layer l starts l rows into each token's N-layer record: the storage starts there too
+            # and ends with the reserved range
             base = self.buffers[kind].device_ptr + layer * row * 2
             token_stride = g.n_layers * row
+            size_bytes = self.buffers[0].size - layer * row * 2
         else:
             base = self.buffers[2 * layer + kind].device_ptr
             token_stride = row
-        size_bytes = self.buffers[0].size
+            size_bytes = self.buffers[0].size
         dev = torch.device("cuda", self.device)
         storage = torch._C._construct_storage_from_data_pointer(base, dev, size_bytes)
         t = torch.empty(0, dtype=torch.bfloat16, device=dev)
@@ -507,8 +513,8 @@ class KVCacheManager:
         return [(self.k_cache(i), self.v_cache(i)) for i in range(self._g.n_layers)]
 
 
-def _stream_ptr(stream) -> int:
+def _stream_ptr(stream, device: int | None = None) -> int:
     if stream is None:
         import torch
-        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice() if device is None else device)
     return getattr(stream, "cuda_stream", stream) or 0

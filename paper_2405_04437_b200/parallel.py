@@ -63,12 +63,16 @@ def exchange_handles(blob: bytes, group=None) -> list[bytes]:
 class HeadGather:
     """Fused output-head all-gather over NVLink peer memory.
 
-    One per rank.  Holds this rank's full output buffer [max_batch, Hq_total, D] bf16 plus the
-    peer mappings of every other rank's buffer; `attention.decode_attention_gather` makes the
-    decode kernel store each output row straight into all of them and `wait()` orders the
-    stream after every rank's rows landed.  Replaces `gather_heads` (NCCL all_gather) for the
-    decode output; `create` is collective (CUDA IPC handles exchanged over torch.distributed),
-    `local_group` simulates `world` ranks on one GPU in one process (tests, single-GPU boxes)."""
+    One per rank.  Holds this rank's two staging areas [max_batch, Hq_total, D] bf16 (launches
+    alternate between them, so a peer's next launch never writes where a slow consumer still
+    reads: csrc/gather.cu) plus the peer mappings of every other rank's buffer;
+    `attention.decode_attention_gather` makes the decode kernel store each output row straight
+    into all of them, and `wait()` orders the stream after every rank's rows landed and copies
+    the full output into the caller's tensor (or the rank-local front buffer, `output()`).
+    Every rank issues the same sequence of gathered launches, each followed by its `wait()` on
+    the same stream.  Replaces `gather_heads` (NCCL all_gather) for the decode output; `create`
+    is collective (CUDA IPC handles exchanged over torch.distributed), `local_group` simulates
+    `world` ranks on one GPU in one process (tests, single-GPU boxes)."""
 
     def __init__(self, handle, rank: int, world: int, max_batch: int, hq_total: int, head_dim: int, device: int):
         self.handle = handle
@@ -134,7 +138,8 @@ class HeadGather:
         return [cls(C.c_void_p(hs[r]), r, world, max_batch, hq_total, head_dim, device) for r in range(world)]
 
     def output(self, batch: int | None = None):
-        """Non-owning [batch, Hq_total, D] bf16 view of this rank's full output buffer."""
+        """Non-owning [batch, Hq_total, D] bf16 view of this rank's front buffer (what the last
+        `wait()` without `out` delivered; rewritten by the next one on its stream)."""
         import ctypes as C
 
         import torch
@@ -152,15 +157,36 @@ class HeadGather:
             self._view = t
         return self._view if batch is None else self._view[:batch]
 
-    def wait(self, stream=None) -> None:
+    def wait(self, stream=None, out=None, batch: int | None = None):
+        """Stream-ordered: wait for every rank's rows of the latest gathered launch, then copy
+        the full [batch, Hq_total, D] output into `out` (default: the front buffer, returned as
+        `output(batch)`).  batch 0 waits without copying and returns None."""
         import ctypes as C
 
         import torch
 
         from ._abi import check, lib
 
-        s = stream if stream is not None else torch.cuda.current_stream()
-        check(lib().vattn_gather_wait(self.handle, C.c_void_p(s.cuda_stream)))
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if out is not None:
+            if (out.dtype != torch.bfloat16 or not out.is_contiguous() or out.device.type != "cuda"
+                    or out.device.index != self.device or out.dim() != 3
+                    or tuple(out.shape[1:]) != (self.hq_total, self.head_dim)):
+                raise ValueError(f"out must be a contiguous bf16 [B, {self.hq_total}, {self.head_dim}] tensor "
+                                 f"on cuda:{self.device}")
+            if batch is not None and batch != out.shape[0]:
+                raise ValueError("batch disagrees with out.shape[0]")
+            batch = out.shape[0]
+        elif batch is None:
+            batch = self.max_batch
+        if not 0 <= batch <= self.max_batch:
+            raise ValueError(f"batch {batch} outside [0, {self.max_batch}]")
+        nbytes = batch * self.hq_total * self.head_dim * 2
+        dst = None if out is None else C.c_void_p(out.data_ptr())
+        check(lib().vattn_gather_wait(self.handle, dst, nbytes, C.c_void_p(s.cuda_stream)))
+        if batch == 0:
+            return None
+        return out if out is not None else self.output(batch)
 
     def timed_out_ranks(self) -> list[int]:
         """Ranks whose rows a wait gave up on (a rank skipped a gathered launch); syncs."""

@@ -291,17 +291,24 @@ def test_sliced_layout_kernels():
         # the view sees the sliced strides
         assert torch.equal(mgr.k_cache(layer)[r, :S].cpu(), kn[0])
     mgr.close()
-    # 3 layers: a 3 KiB token row does not tile a 2 MiB page-group into 64-token boxes, so a decode
-    # box could reach an unmapped page; the decode entry points refuse it instead of faulting
+    # 3 layers: a 3 KiB token row does not tile a 2 MiB page-group into 64-token boxes (682.67
+    # tokens per group), so a decode box could reach an unmapped page: the kernels load each row's
+    # partial last tile with bounded per-row loads (CacheView::tail_guard) and match the oracle
     from paper_2405_04437_b200.attention import decode_attention
-    from paper_2405_04437_b200.errors import UnsupportedError
     g3 = ModelGeometry(3, 4, 128, 2, max_context=2048, max_batch=3, n_q_heads_total=16)
     m3 = KVCacheManager(g3, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, sliced=True))
     r3 = m3.alloc_reqid()
-    assert m3.step([100 if i == r3 else 0 for i in range(3)]).ok
-    with pytest.raises(UnsupportedError):
-        decode_attention(m3, 0, torch.zeros(1, 16, 128, dtype=torch.bfloat16, device=dev),
-                         torch.tensor([100], dtype=torch.int32, device=dev), torch.tensor([r3], dtype=torch.int32, device=dev))
+    n3 = 682                                    # the last whole token of page-group 0
+    assert m3.step([n3 if i == r3 else 0 for i in range(3)]).ok
+    assert m3.slots[r3].mapped_groups == 1
+    k3 = torch.randn(1, n3, 4, 128, generator=gen).to(torch.bfloat16)
+    kv_append(m3, 2, k3.to(dev), k3.to(dev), torch.zeros(1, dtype=torch.int32, device=dev),
+              torch.tensor([r3], dtype=torch.int32, device=dev))
+    q3 = torch.randn(1, 16, 128, generator=gen).to(torch.bfloat16)
+    o3 = decode_attention(m3, 2, q3.to(dev), torch.tensor([n3], dtype=torch.int32, device=dev),
+                          torch.tensor([r3], dtype=torch.int32, device=dev))
+    torch.cuda.synchronize()
+    assert max_rel_err(o3.cpu(), decode_ref(q3, k3, k3, torch.tensor([n3], dtype=torch.int32))) <= 2e-2
     m3.close()
 
 
