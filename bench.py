@@ -173,6 +173,22 @@ def box_copy_gbs(dev) -> float:
     return 2 * (1 << 30) * 2 / (best * 1e-3) / 1e9
 
 
+def traffic_lookup(kernel: str, shape: str, algorithmic_bytes: float):
+    """ncu DRAM traffic (read + write bytes per launch, one `ncu --set full` capture) of `kernel`
+    at the workload shape `shape` from profiles/ncu_traffic.json, scaled to this run's
+    algorithmic bytes when the capture's context differs slightly; (None, why) if not captured."""
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if not tf.exists():
+        return None, "no profiles/ncu_traffic.json"
+    ent = json.loads(tf.read_text()).get(f"{kernel}|{shape}")
+    if not ent:
+        return None, f"no ncu capture of {kernel} at {shape}"
+    t = ent["traffic_bytes"]
+    if ent.get("algorithmic_bytes"):
+        t = t * algorithmic_bytes / ent["algorithmic_bytes"]
+    return t, f"profiles/ncu_traffic.json[{kernel}|{shape}] ({ent.get('capture', 'ncu --set full')})"
+
+
 def dist_setup():
     import torch
     import torch.distributed as dist
@@ -257,7 +273,7 @@ def bench_decode(args, world, rank, local):
 
     from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
     from paper_2405_04437_b200.attention import (decode_attention, decode_attention_append, decode_attention_gather,
-                                                 decode_num_splits, kv_append)
+                                                 decode_kernel_name, decode_num_splits, kv_append)
     from paper_2405_04437_b200.parallel import gather_heads
 
     dev = torch.device("cuda", local)
@@ -401,11 +417,8 @@ def bench_decode(args, world, rank, local):
     pk = peaks()
     achieved = dec_bytes / (dec_us * 1e-6) / 1e9
     box_copy = box_copy_gbs(dev)
-    kernel_name = "decode_kernel<128,3,false>" + ("" if args.unfused else " (fused append)")
-    traffic = None
-    tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists() and args.workload == "l8_decode":
-        traffic = json.loads(tf.read_text()).get(kernel_name, {}).get("traffic_bytes")
+    kernel_name = decode_kernel_name(B, hkv, ctx + 1, splits, d) + ("" if args.unfused else " (fused append)")
+    traffic, traffic_src = traffic_lookup(kernel_name, f"{args.workload}-G{world}", dec_bytes)
 
     # ---- e2e through the public API with host buffers (pinned) ----
     qh = q.cpu().pin_memory()
@@ -479,7 +492,7 @@ def bench_decode(args, world, rank, local):
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "copy_peak_this_box_gbs": box_copy, "frac_of_this_box_copy_peak": achieved / box_copy,
                      "algorithmic_bytes": dec_bytes, "kernel": kernel_name,
-                     "peak_source": pk["source"], "traffic_source": "profiles/ncu_traffic.json (ncu --set full)"},
+                     "peak_source": pk["source"], "traffic_source": traffic_src},
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "clocks": clk,
@@ -620,6 +633,135 @@ def extra_prefill(local):
             "flops": flops, "append_us": app_ms * 1e3, "append_gbs": app_bytes / (app_ms * 1e-3) / 1e9,
             "append_frac_hbm": app_bytes / (app_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
             "map_16k_prompt_ms": map_ms, **paged}
+
+
+def bench_prefill(local, iters=10, cpu=True):
+    """BASELINE config 3 as a measured contract object (top-level `prefill` of the bench line):
+    Yi-6B-shaped 16K-token prompt (32 Q / 4 KV heads, D 128, one layer, causal) appended into a
+    request slot of the virtual cache, then the tcgen05 prefill kernel over it.
+
+    * value / roofline: prefill kernel TFLOP/s (causal flops 2*S^2*D*Hq, the FlashAttention
+      convention) by CUDA events around each launch, against the measured dense bf16 burst peak
+      (the kernel is timed alone); q/out are 128 MiB each, larger than L2.
+    * append: KV append of 4 requests x 16K tokens in one launch (134 MiB read + 134 MiB written,
+      above the 126 MB L2), L2 flushed by a 256 MiB write before each timed launch.
+    * e2e: the public API from pinned host buffers: q/k/v H2D, kv_append, prefill, output D2H.
+    * cpu_baseline: the fp32 oracle restatement (oracle/attention.py prefill_ref) on all host
+      cores over 8 of the 32 query heads (one KV head's GQA group, all 16K rows), scaled x4."""
+    import torch
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import kv_append, prefill_attention
+    from paper_2405_04437_b200.geometry import yi_6b
+
+    dev = torch.device("cuda", local)
+    S, R = 16384, 4
+    hq, hkv, d = 32, 4, 128
+    g = yi_6b(max_context=S, max_batch=R)
+    g = g.__class__(**{**g.to_dict(), "n_layers": 1})
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=(2 * R * 8 + 4) * MB2), device=local)
+    rids = [mgr.alloc_reqid() for _ in range(R)]
+    t0 = time.perf_counter()
+    assert mgr.step([S] * R).ok
+    map_ms = (time.perf_counter() - t0) * 1e3
+    gen = torch.Generator(device=dev).manual_seed(0)
+    kn = torch.randn(R, S, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    vn = torch.randn(R, S, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    q = torch.randn(S, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    zeros = torch.zeros(R, dtype=torch.int32, device=dev)
+    idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+
+    def per_launch(fn, n, flush_l2):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            if flush_l2:
+                flush.fill_(1)
+            e0.record(st)
+            fn()
+            e1.record(st)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    app_ms = per_launch(lambda: kv_append(mgr, 0, kn, vn, zeros, idx), iters, True)
+    app_bytes = 2 * (2 * R * S * hkv * d * 2)                     # K and V: read source + write cache
+    pf_ms = per_launch(lambda: prefill_attention(mgr, 0, q, rids[0], out=out), iters, False)
+    pf_mean = statistics.mean(pf_ms)
+    flops = 2.0 * S * S * d * hq
+    pk = peaks()
+    tf = flops / (pf_mean * 1e-3) / 1e12
+    traffic, traffic_src = traffic_lookup("prefill_kernel<0,false,128,false>", "y6-16k", flops)
+    # e2e through the public API with host buffers
+    qh, kh, vh = q.cpu().pin_memory(), kn[:1].cpu().pin_memory(), vn[:1].cpu().pin_memory()
+    oh = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    q_d, k_d, v_d = torch.empty_like(q), torch.empty_like(kn[:1]), torch.empty_like(vn[:1])
+    one = idx[:1]
+
+    def e2e_once():
+        q_d.copy_(qh, non_blocking=True)
+        k_d.copy_(kh, non_blocking=True)
+        v_d.copy_(vh, non_blocking=True)
+        kv_append(mgr, 0, k_d, v_d, zeros[:1], one)
+        prefill_attention(mgr, 0, q_d, rids[0], out=out)
+        oh.copy_(out, non_blocking=True)
+
+    e2e_ms = statistics.mean(per_launch(e2e_once, max(3, iters // 2), False))
+    res = {
+        "metric": "prefill_attn_tflops", "value": tf, "unit": "TFLOP/s", "dtype": "bf16",
+        "workload": "yi-6b prefill, 16K-token prompt, causal, 1 layer (32 Q / 4 KV heads, D 128), 2 MiB pages",
+        "ms_per_launch": pf_mean, "launches_timed": len(pf_ms), "flops_per_launch": flops,
+        "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": tf / pk["bf16_tflops"], "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": "pf::prefill_kernel<0,false,128,false> (tcgen05.mma cta_group::1, TMEM accumulators)",
+                     "peak_source": pk["source"] + " bf16 burst (kernel timed alone)",
+                     "frac_of_2250_nominal": tf / 2250.0},
+        "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,
+                "d2h_bytes_per_step": oh.numel() * 2, "ms_per_step": e2e_ms,
+                "note": "pinned host q/k/v -> H2D, kv_append, prefill, out -> D2H; one stream"},
+        "append": {"workload": f"{R} requests x {S} tokens in one launch (K+V {app_bytes / 2**20:.0f} MiB moved, > L2)",
+                   "us_per_launch": statistics.mean(app_ms) * 1e3, "bytes_per_launch": app_bytes,
+                   "gbs": app_bytes / (statistics.mean(app_ms) * 1e-3) / 1e9,
+                   "frac_hbm": app_bytes / (statistics.mean(app_ms) * 1e-3) / 1e9 / pk["hbm_gbs"],
+                   "l2": "256 MiB flush write before every timed launch"},
+        "map_16k_prompt_x4_ms": map_ms,
+        "gpu_launches": len(pf_ms),
+    }
+    if cpu:
+        res["cpu_baseline"] = cpu_prefill_baseline(S, hq, hkv, d)
+    del kn, vn, flush
+    mgr.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+def cpu_prefill_baseline(S, hq, hkv, d, head_groups=1):
+    """fp32 CPU causal prefill (oracle/attention.py prefill_ref) on all host cores: `head_groups`
+    of the hkv GQA groups (all S query rows of those hq/hkv heads), scaled to every head."""
+    import torch
+
+    from oracle.attention import prefill_ref
+
+    torch.set_num_threads(host_cores())
+    gen = torch.Generator().manual_seed(0)
+    grp = hq // hkv
+    q = torch.randn(S, grp * head_groups, d, generator=gen).to(torch.bfloat16)
+    k = torch.randn(S, head_groups, d, generator=gen).to(torch.bfloat16)
+    v = torch.randn(S, head_groups, d, generator=gen).to(torch.bfloat16)
+    t0 = time.perf_counter()
+    prefill_ref(q, k, v, causal=True)
+    dt = (time.perf_counter() - t0) * (hkv / head_groups)
+    flops = 2.0 * S * S * d * hq
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": host_cores(), "kind": "port",
+            "sample": (f"{head_groups} of {hkv} KV-head groups ({grp * head_groups} of {hq} query heads, all {S} rows, "
+                       f"causal) of one layer, fp32 torch restatement oracle/attention.py prefill_ref on "
+                       f"{host_cores()} threads, scaled x{hkv / head_groups:g}; cpu: {cpu_model()}"),
+            "ms_per_layer": dt * 1e3}
 
 
 def extra_long_prefill(local, lengths=(4096, 16384, 65536, 131072)):
@@ -1038,28 +1180,30 @@ def extra_serving(local, requests=48):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-class CpuDecodeSample:
-    """Oracle port (fp32 torch on all host cores + the oracle allocator) on a bounded sample of
-    the decode step: `layers` of the geometry's layers are computed and scaled to the full step."""
+class CpuDecodeStep:
+    """Oracle port on the host: the fp32 torch restatement of decode attention
+    (oracle/attention.py decode_ref_equal: every batch row over its whole context, all query
+    heads, on all host cores) for `layers` layers per step + the oracle allocator's `step` for
+    the same iteration (1 thread).  Every layer is computed in full; with layers == n_layers the
+    step is the whole decode iteration and nothing is extrapolated.  The layers share one K/V
+    array (identical shapes; 1 GiB per layer, far above the host LLC, so every layer streams
+    from DRAM as distinct layers would)."""
 
-    def __init__(self, workload: str, world: int, layers: int = 1, batch_frac: int = 4):
+    def __init__(self, workload: str, world: int, layers: int | None = None):
         import torch
 
         from oracle.allocator import Geometry, OracleManager
 
         g, ctx, _ = decode_geometry(workload, world)
-        self.g, self.ctx, self.layers = g, ctx, layers
+        self.g, self.ctx = g, ctx
+        self.layers = g.n_layers if layers is None else layers
         self.cores = host_cores()
         torch.set_num_threads(self.cores)
-        hkv, hq, d = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim
-        self.rows = max(1, g.max_batch // batch_frac)     # batch rows computed per sampled layer
-        B = self.rows
+        hkv, hq, d, B = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim, g.max_batch
         gen = torch.Generator().manual_seed(0)
         self.k = torch.randn(B, ctx + 1, hkv, d, generator=gen, dtype=torch.bfloat16)
         self.v = torch.randn(B, ctx + 1, hkv, d, generator=gen, dtype=torch.bfloat16)
-        self.q = torch.randn(B, hq, d, generator=gen, dtype=torch.bfloat16)
-        self.seq = torch.full((B,), ctx + 1, dtype=torch.int32)
-        B = g.max_batch
+        self.q = torch.randn(self.layers, B, hq, d, generator=gen, dtype=torch.bfloat16)
         og = Geometry(g.n_layers, g.kv_heads_total, g.head_dim, g.bytes_per_elem, g.max_context, B,
                       g.tp_degree)
         pool = (g.max_context * g.per_token_layer_bytes // MB2 + 2) * 2 * g.n_layers * B * MB2
@@ -1071,8 +1215,8 @@ class CpuDecodeSample:
         self.om.step(self.sl)
 
     def step(self) -> float:
-        """Seconds for one full decode iteration (sampled layers scaled to all layers)."""
-        from oracle.attention import decode_ref
+        """Seconds for one decode iteration (scaled by n_layers / layers when layers < n_layers)."""
+        from oracle.attention import decode_ref_equal
 
         t0 = time.perf_counter()
         for r in self.rids:
@@ -1080,36 +1224,46 @@ class CpuDecodeSample:
         self.om.step(self.sl)
         t_alloc = time.perf_counter() - t0
         t0 = time.perf_counter()
-        for _ in range(self.layers):
-            decode_ref(self.q, self.k, self.v, self.seq)
-        t_layer = (time.perf_counter() - t0) / self.layers * (self.g.max_batch / self.rows)
-        return t_alloc + t_layer * self.g.n_layers
+        for layer in range(self.layers):
+            decode_ref_equal(self.q[layer], self.k, self.v, self.ctx + 1)
+        t_layers = time.perf_counter() - t0
+        return t_alloc + t_layers * (self.g.n_layers / self.layers)
 
     def describe(self) -> str:
         g = self.g
-        return (f"{self.layers} of {g.n_layers} layers x {self.rows} of {g.max_batch} batch rows per step "
-                f"(ctx={self.ctx + 1}, "
-                f"Hq={g.q_heads_per_worker}, Hkv={g.kv_heads_per_worker}, D={g.head_dim}; fp32 torch "
-                f"restatement oracle/attention.py on {self.cores} threads) scaled to the full step"
-                f" + oracle allocator step (1 thread); cpu: {cpu_model()}")
+        scope = ("every layer, no extrapolation" if self.layers == g.n_layers else
+                 f"{self.layers} of {g.n_layers} identical layers computed in full, scaled x{g.n_layers / self.layers:g}")
+        return (f"full decode step: {g.max_batch} rows x ctx {self.ctx + 1} x Hq {g.q_heads_per_worker} / "
+                f"Hkv {g.kv_heads_per_worker} x D {g.head_dim}, {scope}; fp32 torch restatement "
+                f"oracle/attention.py decode_ref_equal on {self.cores} threads + oracle allocator step "
+                f"(1 thread); cpu: {cpu_model()}")
+
+
+def _cpu_layers(workload: str) -> int | None:
+    # Llama-3-8B: the whole 32-layer step (~1-3 s on 16 cores); Yi-34B's 8 layers at B 128 x 8K
+    # read 4 GiB each: one full layer per step, scaled to the 8 timed layers
+    return None if workload == "l8_decode" else 1
 
 
 def cpu_baseline(workload: str, world: int, steps: int = 2):
-    s = CpuDecodeSample(workload, world)
+    """Main-arm cpu_baseline (rank 0, N = 1): 1 warm-up + `steps` timed full steps (~10 s)."""
+    s = CpuDecodeStep(workload, world, _cpu_layers(workload))
     s.step()
     t = statistics.mean(s.step() for _ in range(steps))
     return {"value": s.g.max_batch / t, "unit": "tokens/s", "cores": s.cores, "kind": "port",
-            "sample": s.describe(), "ms_per_step": t * 1e3}
+            "sample": s.describe() + f"; mean of {steps} steps after 1 warm-up", "ms_per_step": t * 1e3}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference path's CPU implementation (the oracle port, since the
-    reference itself is a hardware-free Python simulator with no attention code) on host cores."""
+    """--impl reference: the reference path's CPU implementation on the host cores.  The reference
+    (kvsim) is a hardware-free Python simulator with no attention code, so this arm is the oracle
+    port (CpuDecodeStep), whose allocator half is pinned bit-exact to the reference itself
+    (tests/test_core_parity.py) and whose attention half follows the paper's equation 2."""
     if rank != 0:
         return None
     # the whole job's work (every KV head) on the one host, whatever N is: the host cores do not
     # multiply with the GPU count
-    s = CpuDecodeSample(args.workload, 1, batch_frac=8)   # 8 of 64 rows per step keeps the arm to ~1 min
+    s = CpuDecodeStep(args.workload, 1, _cpu_layers(args.workload))
     for _ in range(args.warmup):
         s.step()
     times = [s.step() for _ in range(args.steps)]
@@ -1137,7 +1291,8 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["l8_decode", "y34_decode"], default="l8_decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip prefill / paged / serving sub-benches")
+    ap.add_argument("--no-extras", action="store_true", help="skip the paged / shard / serving sub-benches")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the config-3 prefill contract object")
     ap.add_argument("--unfused", action="store_true", help="separate kv_append + decode launches per layer")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (no CUDA graph)")
     ap.add_argument("--gather", choices=["none", "fused", "nccl"], default="none",
@@ -1168,9 +1323,14 @@ def main(argv=None):
             "e2e": res.pop("e2e"), "clocks": res.pop("clocks"), "gpu_launches": res.pop("gpu_launches"),
             **res,
         }
+        if world == 1 and not args.no_prefill:
+            try:
+                line["prefill"] = bench_prefill(local, cpu=not args.no_cpu_baseline)
+            except Exception as e:   # must not void the headline line
+                line["prefill"] = {"error": repr(e)[:300]}
         if not args.no_extras and world == 1:
             extras = {}
-            for name, fn in (("decode_growth", extra_decode_growth), ("prefill", extra_prefill),
+            for name, fn in (("decode_growth", extra_decode_growth), ("prefill_paged", extra_prefill),
                              ("long_prefill", extra_long_prefill), ("varlen_prefill", extra_varlen_prefill),
                              ("paged_vs_contiguous", extra_paged), ("long_decode", extra_long_decode),
                              ("y34_shards", extra_y34_shards), ("l8_shards", extra_l8_shards),

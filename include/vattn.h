@@ -364,6 +364,11 @@ vattn_status vattn_prefill_paged(const void* q, const void* k_pool, const void* 
                                  void* stream);
 int64_t vattn_decode_workspace_bytes(int32_t batch, int32_t n_q_heads, int32_t head_dim,
                                      int32_t num_splits);
+/* Name of the decode kernel variant (template arguments) a contiguous launch of this shape runs,
+ * written to buf (NUL-terminated, at most cap bytes); returns the split count (num_splits 0 =
+ * automatic) or -1.  For labelling measurements (bench.py roofline.kernel). */
+int32_t vattn_decode_kernel_name(int32_t batch, int32_t hkv, int32_t max_seqlen, int32_t num_splits,
+                                 int32_t head_dim, char* buf, int32_t cap);
 
 /* ---- fused head all-gather over NVLink peer memory ----------------------------
  * Replaces the NCCL all-gather of the per-rank decode outputs [B, Hq/G, D] into [B, Hq, D]

@@ -65,6 +65,31 @@ def decode_ref(q, k_cache, v_cache, cache_seqlens, cache_batch_idx=None, scale=N
     return out
 
 
+def decode_ref_equal(q, k_cache, v_cache, n: int, scale=None, rows_per_chunk: int = 1):
+    """decode_ref for a batch whose rows all attend over their first n cached tokens of slot b
+    (no cache_batch_idx), as batched fp32 matmuls over chunks of rows (the CPU baseline's form of
+    the same equation; equal to decode_ref up to fp32 summation order).  One row per chunk is
+    the fastest on the host: a row's fp32 K/V transients (16 MiB at 4K x 8 x 128) are recycled by
+    the allocator, while multi-row chunks page-fault fresh mappings every call (measured 0.15 vs
+    0.9 s per Llama-3-8B layer on 8 cores).  q: [B, Hq, D]; k_cache/v_cache: [B, >= n, Hkv, D]."""
+    batch, hq, d = q.shape
+    hkv = k_cache.shape[2]
+    group = hq // hkv
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    out = torch.zeros(batch, hq, d, dtype=torch.float32)
+    if n == 0:
+        return out
+    for b0 in range(0, batch, rows_per_chunk):
+        b1 = min(batch, b0 + rows_per_chunk)
+        k = k_cache[b0:b1, :n].float().permute(0, 2, 1, 3)            # [b, Hkv, n, D]
+        v = v_cache[b0:b1, :n].float().permute(0, 2, 1, 3)
+        qb = q[b0:b1].float().view(b1 - b0, hkv, group, d)            # head h -> kv head h // group
+        s = torch.matmul(qb, k.transpose(-1, -2)) * scale             # [b, Hkv, group, n]
+        p = torch.softmax(s, dim=-1)
+        out[b0:b1] = torch.matmul(p, v).reshape(b1 - b0, hq, d)
+    return out
+
+
 def prefill_ref(q, k, v, causal=True, scale=None):
     """Self-attention of one request's Sq query rows over its Sk cached keys.
 

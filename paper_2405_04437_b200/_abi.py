@@ -149,6 +149,7 @@ SIGNATURES = {
     "vattn_compute_proxy": (c_i32, [c_u64, c_vp]),
     "vattn_decode_num_splits": (c_i32, [c_i32, c_i32, c_i32]),
     "vattn_decode_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
+    "vattn_decode_kernel_name": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_i32, C.c_char_p, c_i32]),
     "vattn_gather_create": (c_i32, [c_i32, c_i32, c_i32, c_i64, C.POINTER(c_vp), c_vp]),
     "vattn_gather_open": (c_i32, [c_vp, c_vp]),
     "vattn_gather_create_local": (c_i32, [c_i32, c_i32, c_i64, C.POINTER(c_vp)]),

@@ -486,6 +486,15 @@ def decode_num_splits(batch: int, n_kv_heads: int, max_seqlen: int) -> int:
     return lib().vattn_decode_num_splits(batch, n_kv_heads, max_seqlen)
 
 
+def decode_kernel_name(batch: int, n_kv_heads: int, max_seqlen: int, num_splits: int = 0,
+                       head_dim: int = 128) -> str:
+    """Kernel variant a contiguous decode launch of this shape runs (measurement labels)."""
+    buf = C.create_string_buffer(128)
+    if lib().vattn_decode_kernel_name(batch, n_kv_heads, max_seqlen, num_splits, head_dim, buf, 128) < 0:
+        raise RuntimeError("vattn_decode_kernel_name failed")
+    return buf.value.decode()
+
+
 def prefill_attention_raw(q, k_cache, v_cache, req_slot: int, kv_len: int, causal=True,
                           softmax_scale=None, out=None, stream=None, rotary_cos=None, rotary_sin=None,
                           rotary_interleaved: bool = False):

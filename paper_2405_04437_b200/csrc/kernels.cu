@@ -16,6 +16,8 @@
 #include <mutex>
 #include <climits>
 #include <cstdlib>
+#include <cstdio>
+#include <cstring>
 #include <tuple>
 
 #include "internal.h"
@@ -620,9 +622,12 @@ void set_decode_order_hint(int h) { g_order_hint = h; }
 static int g_num_sms = 0;
 static int num_sms() {
   if (g_num_sms == 0) {
-    int dev = 0;
-    check_rt(cudaGetDevice(&dev), "cudaGetDevice");
-    check_rt(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return 148;       // no device (CPU host: only the labelling query gets here): B200's count
+    }
+    g_num_sms = n;
   }
   return g_num_sms;
 }
@@ -737,6 +742,30 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
   }
 }
 
+// Kernel variant for a D = 128 launch.  Measured (tools/decode_stage_sweep.py): with >= 2 CTAs per
+// SM worth of work a 3-stage ring (97 KB smem, 2 CTAs/SM) beats the 4-stage one (L8 layer 6.9 vs
+// 6.2 TB/s), so a grid of up to 2 x 148 runs in one wave (L8 at G = 2: 256 CTAs; 6.26 vs 6.12
+// TB/s with 4 stages in two waves); with at most one CTA per SM the deeper pipeline wins
+// (B 128 x 1 KV head: 6.6 vs 6.3 TB/s) and two consumer groups per CTA keep every sub-partition
+// busy.  VATTN_DEC_STAGES / VATTN_DEC_CW=4 override.
+struct DecodeChoice {
+  int stages, cw;
+};
+static DecodeChoice choose_decode(int batch, int hkv, int num_splits) {
+  static const int forced = [] {
+    const char* e = getenv("VATTN_DEC_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  static const int cw_env = [] {
+    const char* e = getenv("VATTN_DEC_CW");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t ctas = (int64_t)batch * hkv * num_splits;
+  const int stages = forced ? forced : (ctas > num_sms() ? 3 : 4);
+  const bool wide = stages == 4 && cw_env != 4 && ctas <= num_sms();
+  return {stages, wide ? 8 : 4};
+}
+
 struct FusedAppend {
   const void* k_new;
   const void* v_new;
@@ -809,22 +838,9 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
                                           (int64_t)batch * hq * num_splits * d * 4);
   }
   if (d == 128) {
-    // Measured (tools/decode_stage_sweep.py): with >= 2 CTAs per SM worth of work a 3-stage ring
-    // (97 KB smem, 2 CTAs/SM) beats the 4-stage one (L8 layer 6.9 vs 6.2 TB/s); with fewer CTAs
-    // the deeper per-CTA pipeline wins (B 128 x 1 KV head: 6.6 vs 6.3 TB/s).
-    static const int forced = [] {
-      const char* e = getenv("VATTN_DEC_STAGES");
-      return e ? atoi(e) : 0;
-    }();
-    // more CTAs than SMs: 2 CTAs/SM (3 stages) so a grid of up to 2 x 148 runs in one wave
-    // (L8 at G = 2: 256 CTAs; measured 6.26 vs 6.12 TB/s with 4 stages in two waves)
-    const int stages = forced ? forced : (batch * hkv * p.num_splits > num_sms() ? 3 : 4);
-    // at most one CTA per SM: two consumer groups per CTA (VATTN_DEC_CW=4 forces one)
-    static const int cw_env = [] {
-      const char* e = getenv("VATTN_DEC_CW");
-      return e ? atoi(e) : 0;
-    }();
-    const bool wide = stages == 4 && cw_env != 4 && batch * hkv * p.num_splits <= num_sms();
+    const DecodeChoice ch = choose_decode(batch, hkv, p.num_splits);
+    const int stages = ch.stages;
+    const bool wide = ch.cw == 8;
     if (paged) {   // same rule, so the paged comparison differs from the contiguous path only in layout
       if (stages == 3) run_decode<128, 3, true>(km, vm, p, batch, hkv, st);
       else if (wide) run_decode<128, 4, true, 8>(km, vm, p, batch, hkv, st);
@@ -892,6 +908,29 @@ int32_t vattn_decode_num_splits(int32_t batch, int32_t hkv, int32_t max_seqlen) 
     return vattn::auto_splits(batch * hkv, max_seqlen);
   } catch (...) {
     return 1;
+  }
+}
+
+int32_t vattn_decode_kernel_name(int32_t batch, int32_t hkv, int32_t max_seqlen, int32_t num_splits,
+                                 int32_t head_dim, char* buf, int32_t cap) {
+  try {
+    if (num_splits <= 0) num_splits = vattn::auto_splits(batch * hkv, max_seqlen);
+    num_splits = std::min(num_splits, vattn::kMaxSplits);
+    char tmp[96];
+    if (head_dim == 128) {
+      const vattn::DecodeChoice ch = vattn::choose_decode(batch, hkv, num_splits);
+      snprintf(tmp, sizeof tmp, "decode_kernel<128,%d,false,%d>%s", ch.stages, ch.cw,
+               num_splits > 1 ? " + decode_combine_kernel<128>" : "");
+    } else {
+      snprintf(tmp, sizeof tmp, "decode_kernel<64,6,false,4>%s", num_splits > 1 ? " + decode_combine_kernel<64>" : "");
+    }
+    if (buf && cap > 0) {
+      strncpy(buf, tmp, (size_t)cap - 1);
+      buf[cap - 1] = 0;
+    }
+    return num_splits;
+  } catch (...) {
+    return -1;
   }
 }
 
