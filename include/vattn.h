@@ -187,8 +187,14 @@ vattn_status vattn_reclaim_until(vattn_t* h, int64_t target_available_bytes, int
 vattn_status vattn_bg_submit(vattn_t* h, const int64_t* triples, int64_t n_entries,
                              uint32_t flags, int64_t eager_k);
 vattn_status vattn_bg_wait(vattn_t* h, vattn_bg_result* out);
-/* unmap fence: record "the KV cache may be read by work queued on `stream` so far" */
+/* unmap fence: record "the KV cache may be read by work queued on `stream` so far" (one event
+ * per stream; unmaps wait for every stream's) */
 vattn_status vattn_mark_use(vattn_t* h, void* stream);
+/* Read guard: the decode / append kernels clamp every row to the rows its slot backs (and skip
+ * slots outside [0, max_batch)) instead of faulting the context, and record the violation in
+ * host-mapped words.  The next allocator call or kernel launch on the handle — or this call —
+ * returns VATTN_VALUE_ERROR for it (after the kernel ran; synchronize first to be sure). */
+vattn_status vattn_check_errors(vattn_t* h);
 
 /* ---- introspection ------------------------------------------------------------------ */
 vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out);

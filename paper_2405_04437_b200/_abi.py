@@ -99,6 +99,7 @@ SIGNATURES = {
     "vattn_bg_submit": (c_i32, [c_vp, P_i64, c_i64, c_u32, c_i64]),
     "vattn_bg_wait": (c_i32, [c_vp, C.POINTER(BgResult)]),
     "vattn_mark_use": (c_i32, [c_vp, c_vp]),
+    "vattn_check_errors": (c_i32, [c_vp]),
     "vattn_counters_get": (c_i32, [c_vp, C.POINTER(Counters)]),
     "vattn_counters_peek": (c_i32, [c_vp, C.POINTER(Counters)]),
     "vattn_slot_state": (c_i32, [c_vp, P_i64, c_i64]),

@@ -205,6 +205,25 @@ class Manager {
   void reset_credits() { std::fill(plan_credit_.begin(), plan_credit_.end(), 0); }
 
   void mark_use(cudaStream_t st);
+  // Device-side read guard: rows each slot may be read at (backed page-groups), published to the
+  // device for the decode / append kernels, which clamp to it and record a violation in a
+  // host-mapped word instead of faulting the context; check_device_errors() raises it.
+  void publish_rows();                          // grow to the slots' backed rows
+  void shrink_rows(int64_t off);                // before unmapping the page at buffer offset off
+  void check_device_errors();
+  int32_t rows_of(int64_t groups) const {
+    return (int32_t)std::min<int64_t>(max_context_, groups * t_ / per_buffer_token_bytes_);
+  }
+  int64_t mapped_rows(int32_t slot) const { return rows_of(slots_.at(slot).mapped_groups); }
+  // prefill takes kv_len on the host: check it against the slot's backed rows before launching
+  void check_prefill_rows(int32_t slot, int64_t kv_len) const {
+    if (slot < 0 || slot >= (int32_t)slots_.size())
+      throw Fail(VATTN_VALUE_ERROR, "slot " + std::to_string(slot) + " out of range");
+    if (real() && kv_len > mapped_rows(slot))
+      throw Fail(VATTN_VALUE_ERROR, "prefill over " + std::to_string(kv_len) + " rows of slot " +
+                                        std::to_string(slot) + ", which backs " + std::to_string(mapped_rows(slot)) +
+                                        " (call step() with the prompt length first)");
+  }
   void begin_call() { fenced_ = false; }
   void end_call() { flush_access(); }
 
@@ -359,6 +378,17 @@ class Manager {
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> use_events_;
   std::atomic<bool> use_recorded_{false};
   bool fenced_ = false;
+  // read guard (publish_rows): device copy of every slot's readable rows, its pinned staging
+  // buffer and host shadow, a private stream for the copy, and the host-mapped violation words
+  // [flag, slot, requested rows, readable rows]
+  std::mutex pub_mu_;
+  std::mutex slot_mu_;   // free_reqid's writes vs the prefetch job's slot snapshot
+  int32_t* d_rows_ = nullptr;
+  int32_t* h_rows_ = nullptr;
+  std::vector<int32_t> pub_rows_;
+  cudaStream_t pub_stream_ = nullptr;
+  uint32_t* h_err_ = nullptr;
+  uint32_t* d_err_ = nullptr;
   // measured real-driver statistics
   int64_t real_maps_ = 0, real_unmaps_ = 0, real_access_ = 0, real_creates_ = 0,
           real_releases_ = 0;
@@ -495,6 +525,19 @@ Manager::Manager(const vattn_config& c) {
   init_us_ += dev_precreate(pre);
   slots_.resize(c.max_batch);
   plan_credit_.assign(c.max_batch, 0);
+  // counters_peek walks ledger_order_ while a background job may append to it: never reallocate
+  ledger_order_.reserve(A_COUNT);
+  if (real()) {
+    const size_t n = (size_t)c.max_batch;
+    check_rt(cudaMalloc(reinterpret_cast<void**>(&d_rows_), n * 4), "cudaMalloc(read guard)");
+    check_rt(cudaMemset(d_rows_, 0, n * 4), "cudaMemset(read guard)");
+    check_rt(cudaHostAlloc(reinterpret_cast<void**>(&h_rows_), n * 4, cudaHostAllocDefault), "cudaHostAlloc(read guard)");
+    check_rt(cudaStreamCreateWithFlags(&pub_stream_, cudaStreamNonBlocking), "cudaStreamCreate(read guard)");
+    check_rt(cudaHostAlloc(reinterpret_cast<void**>(&h_err_), 64, cudaHostAllocMapped), "cudaHostAlloc(error words)");
+    std::memset(h_err_, 0, 64);
+    check_rt(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_err_), h_err_, 0), "cudaHostGetDevicePointer");
+    pub_rows_.assign(n, 0);
+  }
   init_wall_us_ = now_us() - t0;
 
   bg_thread_ = std::thread([this] { bg_loop(); });
@@ -583,6 +626,10 @@ Manager::~Manager() {
   for (auto h : phys_free_) d.MemRelease(h);
   for (size_t b = 0; b < va_.size(); ++b) d.MemAddressFree(va_[b], (size_t)buffer_size_);
   for (auto& se : use_events_) cudaEventDestroy(se.second);
+  if (d_rows_) cudaFree(d_rows_);
+  if (h_rows_) cudaFreeHost(h_rows_);
+  if (h_err_) cudaFreeHost(h_err_);
+  if (pub_stream_) cudaStreamDestroy(pub_stream_);
 }
 
 // ---- shadow driver ------------------------------------------------------------------------
@@ -809,7 +856,17 @@ bool Manager::slot_ready(int32_t slot, int64_t tokens) const {
 }
 
 void Manager::prefetch() {
+  Nvtx nv("vattn.prefetch");
   if (!real()) return;
+  // free_reqid may run concurrently (it does not join prefetch jobs): work on a snapshot of the
+  // slot table taken under slot_mu_ (ADVICE r1 core.cpp:1554)
+  std::vector<Slot> slots;
+  int32_t eager_slot;
+  {
+    std::lock_guard<std::mutex> lk(slot_mu_);
+    slots = slots_;
+    eager_slot = eager_slot_;
+  }
   // Runs inside a bg window (state owned): choose the pages, hand them to the worker, return.
   // (urgency, key): pages are mapped soonest-needed first — decode growth by the tokens left
   // before the row reaches the page, then the speculative-eager slots in alloc_reqid order
@@ -825,8 +882,8 @@ void Manager::prefetch() {
   };
   // 1. decode growth of active slots within prefetch_tokens_ more tokens
   if (prefetch_tokens_ > 0)
-    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
-      const Slot& s = slots_[r];
+    for (int32_t r = 0; r < (int32_t)slots.size(); ++r) {
+      const Slot& s = slots[r];
       if (!s.active) continue;
       spec_range(r, s.mapped_groups, std::min(groups_required(s.context_len + prefetch_tokens_), groups_per_slot_),
                  0, s.context_len);
@@ -835,16 +892,16 @@ void Manager::prefetch() {
   //    (mapped_groups, -req_id), manager.py:166-174) up to prefetch_slot_tokens_ of prompt
   if (prefetch_slots_ > 0 && prefetch_slot_tokens_ > 0) {
     std::vector<int32_t> cand;
-    for (int32_t r = 0; r < (int32_t)slots_.size(); ++r)
-      if (!slots_[r].active) cand.push_back(r);
+    for (int32_t r = 0; r < (int32_t)slots.size(); ++r)
+      if (!slots[r].active) cand.push_back(r);
     std::stable_sort(cand.begin(), cand.end(), [&](int32_t a, int32_t b) {
-      const bool ea = a == eager_slot_, eb = b == eager_slot_;
+      const bool ea = a == eager_slot, eb = b == eager_slot;
       if (ea != eb) return ea;
-      return slots_[a].mapped_groups > slots_[b].mapped_groups;
+      return slots[a].mapped_groups > slots[b].mapped_groups;
     });
     const int64_t target = std::min(groups_required(prefetch_slot_tokens_), groups_per_slot_);
     for (size_t i = 0; i < cand.size() && (int64_t)i < prefetch_slots_; ++i)
-      spec_range(cand[i], slots_[cand[i]].mapped_groups, target, (int64_t)(1 + i) << 40, -1);
+      spec_range(cand[i], slots[cand[i]].mapped_groups, target, (int64_t)(1 + i) << 40, -1);
   }
   // 3. prompts queued for admission, at the slots they are predicted to get (after growth)
   std::vector<std::pair<int32_t, int64_t>> hints;
@@ -854,7 +911,7 @@ void Manager::prefetch() {
   }
   for (size_t i = 0; i < hints.size(); ++i) {
     const auto& hs = hints[i];
-    if (slots_[hs.first].active) continue;
+    if (slots[hs.first].active) continue;
     spec_range(hs.first, 0, std::min(groups_required(hs.second), groups_per_slot_), ((int64_t)1 << 38) + ((int64_t)i << 20), -1);
   }
   std::stable_sort(targets.begin(), targets.end(),
@@ -938,6 +995,7 @@ void Manager::flush_access() {
 }
 
 void Manager::fence_unmap() {
+  Nvtx nv("vattn.unmap_fence");
   // Never unmap a page that queued kernels may still read (SURVEY §7 hard part 3).
   if (fenced_) return;
   flush_access();
@@ -954,6 +1012,7 @@ void Manager::fence_unmap() {
 
 void Manager::real_unmap(int32_t b, int64_t off) {
   fence_unmap();
+  shrink_rows(off);
   const double t0 = now_us();
   check_cu(driver().MemUnmap(va_[b] + off, (size_t)t_), "cuMemUnmap");
   real_unmap_us_ += now_us() - t0;
@@ -1028,6 +1087,7 @@ void Manager::free_reqid(int32_t rid) {  // manager.py:180-190 — no driver cal
   if (rid < 0 || rid >= (int32_t)slots_.size()) throw Fail(VATTN_VALUE_ERROR, "req_id out of range");
   Slot& s = slots_[rid];
   if (!s.active) throw Fail(VATTN_DOUBLE_FREE, "slot " + std::to_string(rid) + " is not active");
+  std::lock_guard<std::mutex> lk(slot_mu_);   // a prefetch job may be snapshotting the table
   s.active = false;
   s.context_len = 0;
   s.phase = INACTIVE;
@@ -1105,6 +1165,7 @@ std::pair<int64_t, double> Manager::reclaim_until(int64_t target) {  // manager.
 }
 
 bool Manager::step(const int64_t* seq, int32_t n, double* sync_out) {  // manager.py:255-296
+  Nvtx nv("vattn.step");
   if (n != (int32_t)slots_.size())
     throw Fail(VATTN_VALUE_ERROR, "expected " + std::to_string(slots_.size()) + " sequence lengths, got " +
                                       std::to_string(n));
@@ -1128,7 +1189,11 @@ bool Manager::step(const int64_t* seq, int32_t n, double* sync_out) {  // manage
         if (f.code != VATTN_POOL_EXHAUSTED) throw;
         auto fr = reclaim_until(buffer_count_ * t_);
         sync_us += fr.second;
-        if (fr.first == 0) { *sync_out = sync_us; return false; }
+        if (fr.first == 0) {
+          *sync_out = sync_us;
+          publish_rows();   // earlier slots of this step did grow
+          return false;
+        }
         continue;
       }
       s.mapped_groups += 1;
@@ -1137,7 +1202,56 @@ bool Manager::step(const int64_t* seq, int32_t n, double* sync_out) {  // manage
     s.phase = DECODE;
   }
   *sync_out = sync_us;
+  publish_rows();
   return true;
+}
+
+// The published rows track what is PHYSICALLY readable without a fault: they grow with the
+// logical state (end of step / of a background job) and shrink only in real_unmap, after the
+// unmap fence, for the page about to go.  A lazily kept page (lazy_unmap) stays readable until
+// it is really unmapped.  Copies go through a private non-blocking stream, so a publish never
+// waits for the caller's in-flight kernels.
+static void push_rows(int32_t* d, int32_t* h, const std::vector<int32_t>& v, cudaStream_t st) {
+  std::memcpy(h, v.data(), v.size() * 4);
+  check_rt(cudaMemcpyAsync(d, h, v.size() * 4, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync(read guard)");
+  check_rt(cudaStreamSynchronize(st), "cudaStreamSynchronize(read guard)");
+}
+
+void Manager::publish_rows() {
+  if (!real()) return;
+  std::lock_guard<std::mutex> lk(pub_mu_);
+  bool changed = false;
+  for (int32_t r = 0; r < (int32_t)slots_.size(); ++r) {
+    const int32_t v = rows_of(slots_[r].mapped_groups);
+    if (v > pub_rows_[r]) {
+      pub_rows_[r] = v;
+      changed = true;
+    }
+  }
+  if (changed) push_rows(d_rows_, h_rows_, pub_rows_, pub_stream_);
+}
+
+void Manager::shrink_rows(int64_t off) {
+  if (!d_rows_) return;
+  const int64_t r = off / slot_stride_, g = (off % slot_stride_) / t_;
+  if (r < 0 || r >= (int64_t)pub_rows_.size()) return;
+  std::lock_guard<std::mutex> lk(pub_mu_);
+  const int32_t v = rows_of(g);
+  if (v >= pub_rows_[r]) return;
+  pub_rows_[r] = v;
+  push_rows(d_rows_, h_rows_, pub_rows_, pub_stream_);
+}
+
+void Manager::check_device_errors() {
+  if (!h_err_) return;
+  volatile uint32_t* e = h_err_;
+  if (e[0] == 0) return;
+  const uint32_t slot = e[1], want = e[2], have = e[3];
+  e[0] = 0;
+  throw Fail(VATTN_VALUE_ERROR, "a kernel was asked to read " + std::to_string(want) + " rows of slot " +
+                                    std::to_string(slot) + ", which has " + std::to_string(have) +
+                                    " backed rows (or the slot index is out of range); its reads were clamped"
+                                    " (call step() with the grown lengths first)");
 }
 
 int64_t Manager::plan_overlap(const int64_t* next, int32_t n) {  // manager.py:298-311
@@ -1159,6 +1273,7 @@ int64_t Manager::plan_overlap(const int64_t* next, int32_t n) {  // manager.py:2
 }
 
 double Manager::execute_plan(const int64_t* trip, int64_t n) {  // manager.py:313-333
+  Nvtx nv("vattn.execute_plan");
   double us = 0.0;
   std::unordered_set<int64_t> done;
   for (int64_t i = 0; i < n; ++i) {
@@ -1187,6 +1302,7 @@ double Manager::execute_plan(const int64_t* trip, int64_t n) {  // manager.py:31
 }
 
 double Manager::eager_prepare(int64_t k) {  // manager.py:335-361
+  Nvtx nv("vattn.eager_prepare");
   if (k < 0) k = eager_groups_;
   if (k <= 0) return 0.0;
   k = std::min(k, groups_per_slot_);
@@ -1231,6 +1347,7 @@ void Manager::bg_loop() {
       job = std::move(bg_queue_.front());
       bg_queue_.pop_front();
     }
+    Nvtx nv("vattn.bg_job");
     vattn_bg_result res{};
     vattn_status st = VATTN_OK;
     std::string err;
@@ -1253,6 +1370,7 @@ void Manager::bg_loop() {
         res.reclaim_us = r.second;
       }
       flush_access();
+      publish_rows();
       if (job.flags & VATTN_BG_PREFETCH) prefetch();
     } catch (const Fail& f) {
       st = f.code;
@@ -1282,6 +1400,7 @@ void Manager::bg_loop() {
 double Manager::join_bg() {
   std::unique_lock<std::mutex> lk(bg_mu_);
   if (bg_completed_ == bg_submitted_) return 0.0;
+  Nvtx nv("vattn.bg_join_wait");
   prefetch_cancel_.store(true, std::memory_order_relaxed);
   const double t0 = now_us();
   bg_cv_.wait(lk, [&] { return bg_completed_ == bg_submitted_; });
@@ -1465,6 +1584,8 @@ CacheView Manager::layer_view(int32_t layer) const {
   }
   v.slot_stride = slot_stride_;
   v.tail_guard = (t_ % (64 * per_buffer_token_bytes_) != 0) ? 1 : 0;
+  v.slot_rows = d_rows_;
+  v.err = d_err_;
   v.slot_tokens = (int32_t)max_context_;
   v.n_slots = (int32_t)slots_.size();
   v.hkv = hkv_local_;
@@ -1550,6 +1671,7 @@ static vattn_status api_call(vattn_t* h, F&& f) {
   }
   return guard([&] {
     h->m->join_bg();
+    h->m->check_device_errors();
     h->m->begin_call();
     try {
       f(*h->m);
@@ -1723,6 +1845,11 @@ vattn_status vattn_bg_wait(vattn_t* h, vattn_bg_result* out) {
   return guard([&] { h->m->bg_wait(out); });
 }
 
+vattn_status vattn_check_errors(vattn_t* h) {
+  if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
+  return guard([&] { h->m->check_device_errors(); });
+}
+
 vattn_status vattn_mark_use(vattn_t* h, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] { h->m->mark_use((cudaStream_t)stream); });
@@ -1809,6 +1936,8 @@ vattn_status vattn_kv_append(vattn_t* h, int32_t layer, const void* k_new, const
                              const int32_t* batch_idx, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
+    vattn::Nvtx nv("vattn.kv_append");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
                             (cudaStream_t)stream);
@@ -1823,6 +1952,8 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
   return guard([&] {
     h->m->check_decode_tiling();
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
+    vattn::Nvtx nv("vattn.decode");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     int64_t ws_bytes = 0;
@@ -1842,6 +1973,8 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
   return guard([&] {
     h->m->check_decode_tiling();
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
+    vattn::Nvtx nv("vattn.decode_append");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     int64_t ws_bytes = 0;
@@ -1859,6 +1992,8 @@ vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    vattn::Nvtx nv("vattn.kv_append");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
     vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
@@ -1873,7 +2008,10 @@ vattn_status vattn_prefill_varlen(vattn_t* h, int32_t layer, const void* q, void
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     if (n_req > 0 && (!q_start || !n_q || !slots || !kv_len)) throw Fail(VATTN_VALUE_ERROR, "null argument");
+    vattn::Nvtx nv("vattn.prefill_varlen");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
+    for (int32_t i = 0; i < n_req; ++i) h->m->check_prefill_rows(slots[i], kv_len[i]);
     vattn::launch_prefill_varlen(v, q, out, h->m->hq_local(), n_req, q_start, n_q, slots, kv_len, scale,
                                  causal != 0, (cudaStream_t)stream);
     h->m->mark_use((cudaStream_t)stream);
@@ -1886,8 +2024,11 @@ vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
     if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
+    vattn::Nvtx nv("vattn.prefill");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    h->m->check_prefill_rows(slot, kv_len);
     vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
                           causal != 0, (cudaStream_t)stream, &rot);
     h->m->mark_use((cudaStream_t)stream);
@@ -1903,6 +2044,8 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
     if (!rotary) throw Fail(VATTN_VALUE_ERROR, "null rotary descriptor");
     h->m->check_decode_tiling();
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
+    vattn::Nvtx nv("vattn.decode_append");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     int64_t ws_bytes = 0;
@@ -1923,6 +2066,8 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
   return guard([&] {
     h->m->check_decode_tiling();
     vattn::set_decode_order_hint(h->m->mixed_lengths() ? 1 : 0);
+    vattn::Nvtx nv("vattn.decode_gather");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
     const int hq = h->m->hq_local();
     int64_t ws_bytes = 0;
@@ -1940,7 +2085,10 @@ vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, 
                            void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
   return guard([&] {
+    vattn::Nvtx nv("vattn.prefill");
+    h->m->check_device_errors();
     const vattn::CacheView v = h->m->layer_view(layer);
+    h->m->check_prefill_rows(slot, kv_len);
     vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
                           causal != 0, (cudaStream_t)stream);
     h->m->mark_use((cudaStream_t)stream);

@@ -10,8 +10,18 @@
 #include <string>
 
 #include "vattn.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace vattn {
+
+// NVTX range for the allocator and launch paths (SURVEY §5 tracing): visible in Nsight Systems /
+// ncu --nvtx; a no-op costing a few ns when no tool is attached.  Header-only NVTX v3.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // Internal failure carrying a vattn_status; converted to a return code at the C ABI edge.
 struct Fail : std::runtime_error {
@@ -66,6 +76,10 @@ struct CacheView {
   // number of 64-token decode tiles, e.g. the layer-sliced layout, manager.py:93-96): the decode
   // kernels then load a row's last, partial tile with bounded per-row loads instead of one TMA box
   int32_t tail_guard = 0;
+  // read guard (manager caches): rows slot i may be read at, and the host-mapped words
+  // [flag, slot, requested, readable] a kernel fills when asked for more (its reads are clamped)
+  const int32_t* slot_rows = nullptr;
+  uint32_t* err = nullptr;
 };
 
 CacheView view_from_desc(const vattn_cache_desc* c);

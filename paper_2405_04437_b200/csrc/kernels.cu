@@ -31,6 +31,9 @@ namespace vattn {
 // One 16-byte chunk per thread-iteration; rows are contiguous in both source and destination
 // so warps issue fully coalesced 128-bit loads and stores.
 struct AppendParams {
+  const int32_t* slot_rows;   // read/write guard (CacheView): rows a slot backs; nullptr = slot_cap
+  uint32_t* err;
+  int32_t n_slots, slot_cap;
   const uint4* k_src;
   const uint4* v_src;
   char* k_dst;
@@ -53,6 +56,18 @@ __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
     const int32_t i = (int32_t)(row - (int64_t)b * p.n_new);
     const int32_t slot = p.batch_idx ? __ldg(p.batch_idx + b) : b;
     const int64_t pos = (int64_t)__ldg(p.seqlens + b) + i;
+    const bool bad_slot = slot < 0 || slot >= p.n_slots;
+    const int lim = bad_slot ? 0 : (p.slot_rows ? min(p.slot_cap, __ldg(p.slot_rows + slot)) : p.slot_cap);
+    if (pos < 0 || pos >= lim) {   // not backed: skip the row, report once per row
+      if (p.err && within == 0) {
+        p.err[1] = (uint32_t)slot;
+        p.err[2] = (uint32_t)(pos + 1);
+        p.err[3] = (uint32_t)lim;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(p.err) = 1u;
+      }
+      continue;
+    }
     const int64_t dst = (int64_t)slot * p.slot_stride + pos * p.token_stride + (int64_t)within * 16;
     uint4 kv, vv;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -134,6 +149,11 @@ struct DecodeParams {
   GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
   int32_t longest_first;        // schedule rows by descending length (B <= 256)
   int32_t tail_guard;           // contiguous: load a row's partial last tile per row (CacheView)
+  // contiguous read guard (CacheView::slot_rows / err): rows are clamped to the slot's readable
+  // rows (and to slot_cap); slots outside [0, n_slots) read nothing
+  const int32_t* slot_rows;
+  uint32_t* err;
+  int32_t n_slots, slot_cap;
   Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
 };
 
@@ -223,14 +243,32 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
     __syncthreads();
     b = s_row;
   }
-  const bool fused = p.k_new != nullptr;
-  const int pos_new = fused ? __ldg(p.seqlens + b) : -1;      // row receiving the new token
-  const int seqlen = fused ? pos_new + 1 : __ldg(p.seqlens + b);
+  const int slot = (!PAGED && p.batch_idx) ? __ldg(p.batch_idx + b) : b;
+  bool fused = p.k_new != nullptr;
+  int pos_new = fused ? __ldg(p.seqlens + b) : -1;            // row receiving the new token
+  int seqlen = fused ? pos_new + 1 : __ldg(p.seqlens + b);
+  if constexpr (!PAGED) {
+    // Read guard: never touch rows a slot does not back (a bad cache_seqlens / cache_batch_idx
+    // would otherwise fault the context).  Clamp, and report through the host-mapped words.
+    const bool bad_slot = slot < 0 || slot >= p.n_slots;
+    const int lim = bad_slot ? 0 : (p.slot_rows ? min(p.slot_cap, __ldg(p.slot_rows + slot)) : p.slot_cap);
+    if (bad_slot || seqlen > lim || seqlen < 0) {
+      if (p.err && threadIdx.x == 0 && split == 0 && kvh == 0) {
+        p.err[1] = (uint32_t)slot;
+        p.err[2] = (uint32_t)seqlen;
+        p.err[3] = (uint32_t)lim;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(p.err) = 1u;
+      }
+      if (fused && (pos_new >= lim || pos_new < 0)) fused = false;   // no room for the new row
+      seqlen = max(0, min(seqlen, lim));
+      if (!fused) pos_new = -1;
+    }
+  }
   const int n_tiles_all = (seqlen + kTile - 1) / kTile;
   const int tps = (n_tiles_all + p.num_splits - 1) / p.num_splits;
   const int tile_begin = split * tps;
   const int n_tiles = max(0, min(n_tiles_all, tile_begin + tps) - tile_begin);
-  const int slot = (!PAGED && p.batch_idx) ? __ldg(p.batch_idx + b) : b;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -675,6 +713,10 @@ void launch_kv_append(KernelState*, int, const CacheView& v, const void* k_new, 
   const int64_t row_bytes = (int64_t)v.hkv * v.d * 2;
   AppendParams p{};
   p.d = v.d;
+  p.slot_rows = v.slot_rows;
+  p.err = v.err;
+  p.n_slots = v.n_slots;
+  p.slot_cap = v.slot_tokens;
   if (rot && rot->cos) {
     if (!rot->sin || rot->dim <= 0 || rot->dim % 16 || rot->dim > v.d)
       throw Fail(VATTN_VALUE_ERROR, "rotary_dim must be a positive multiple of 16 and <= head_dim");
@@ -818,6 +860,10 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
     p.slot_stride = fa->view->slot_stride;
     p.token_stride = fa->view->token_stride;
     p.tail_guard = fa->view->tail_guard;
+    p.slot_rows = fa->view->slot_rows;
+    p.err = fa->view->err;
+    p.n_slots = fa->view->n_slots;
+    p.slot_cap = fa->view->slot_tokens;
   }
   if (rot && rot->cos) {
     if (!fa || !fa->k_new) throw Fail(VATTN_VALUE_ERROR, "rotary embedding needs the fused append (k_new / v_new)");

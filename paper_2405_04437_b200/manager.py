@@ -408,6 +408,12 @@ class KVCacheManager:
         manager's device) so far may read the cache."""
         check(lib().vattn_mark_use(self._h, C.c_void_p(_stream_ptr(stream, self.device))))
 
+    def check_errors(self) -> None:
+        """Raise ValueError if a kernel on this cache was asked for rows its slot does not back
+        (it clamped them instead of faulting; see vattn_check_errors).  Synchronizes nothing:
+        call torch.cuda.synchronize() first to cover every launched kernel."""
+        check(lib().vattn_check_errors(self._h))
+
     # -- parity introspection ---------------------------------------------------------------
     def drain_events(self) -> list[list[int]]:
         n = C.c_int64()

@@ -365,3 +365,68 @@ def test_foreground_window_holds_the_prefetch_worker():
         time.sleep(0.01)
     assert mgr.driver_stats()["spec_maps"] == 3 * 4     # 3 groups x 4 buffers
     mgr.close()
+
+
+def test_device_read_guard_clamps_and_raises_without_faulting():
+    """Default-on device guard: lengths past a slot's backed rows, a slot
+    index out of range, and appends past the backed rows are clamped / skipped by the kernels,
+    which report through host-mapped words; the next call on the manager raises ValueError and
+    the CUDA context stays usable.  Prefill (host kv_len) is refused before launch."""
+    _cuda()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, attention
+    from paper_2405_04437_b200.geometry import ModelGeometry
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(1, 8, 128, 2, max_context=8192, max_batch=2, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=16 * MB2))
+    try:
+        r = mgr.alloc_reqid()
+        lens = [0, 0]
+        lens[r] = 1000
+        assert mgr.step(lens).ok                     # one 2 MiB group = 1024 rows backed
+        gen = torch.Generator(device=dev).manual_seed(9)
+        q = torch.randn(1, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        idx = torch.tensor([r], dtype=torch.int32, device=dev)
+        kv = torch.randn(1, 1024, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        attention.kv_append(mgr, 0, kv, kv, torch.zeros(1, dtype=torch.int32, device=dev), idx)
+        good = attention.decode_attention(mgr, 0, q, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        mgr.check_errors()
+        # 1) a length past the backed rows: clamped to 1024 (same result), reported
+        bad = attention.decode_attention(mgr, 0, q, torch.tensor([7000], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        assert torch.equal(bad, good)
+        with pytest.raises(ValueError, match="backed rows"):
+            mgr.check_errors()
+        mgr.check_errors()                           # reported once
+        # 2) a slot index out of range: no reads, zeros, reported at the next allocator call
+        z = attention.decode_attention(mgr, 0, q, torch.tensor([10], dtype=torch.int32, device=dev),
+                                       torch.tensor([5], dtype=torch.int32, device=dev))
+        torch.cuda.synchronize()
+        assert z.abs().max().item() == 0
+        with pytest.raises(ValueError, match="backed rows"):
+            mgr.step(lens)
+        assert mgr.step(lens).ok
+        # 3) fused append at a row that is not backed: the row is not written, reported
+        k1 = torch.randn(1, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        attention.decode_attention_append(mgr, 0, q, k1, k1, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError):
+            mgr.check_errors()
+        # 4) plain append past the backed rows: skipped, reported
+        attention.kv_append(mgr, 0, kv[:, :8], kv[:, :8], torch.tensor([1020], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError):
+            mgr.check_errors()
+        # rows 1020..1023 are backed and were written; 1024..1027 were skipped
+        assert torch.equal(mgr.k_cache(0)[r, 1020:1024].cpu(), kv[0, :4].cpu())
+        # 5) prefill with kv_len past the backed rows is refused on the host
+        with pytest.raises(ValueError, match="backs"):
+            attention.prefill_attention(mgr, 0, torch.zeros(2000, 32, 128, device=dev, dtype=torch.bfloat16), r)
+        # the context is healthy: a normal decode still matches
+        again = attention.decode_attention(mgr, 0, q, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
+        torch.cuda.synchronize()
+        assert torch.equal(again, good)
+        mgr.check_errors()
+    finally:
+        mgr.close()
