@@ -692,7 +692,10 @@ def bench_prefill(local, iters=10, cpu=True):
 
     app_ms = per_launch(lambda: kv_append(mgr, 0, kn, vn, zeros, idx), iters, True)
     app_bytes = 2 * (2 * R * S * hkv * d * 2)                     # K and V: read source + write cache
+    clocks = ClockSampler(local)          # the prefill is tensor-bound: its SM clock is the context
+    clocks.start()
     pf_ms = per_launch(lambda: prefill_attention(mgr, 0, q, rids[0], out=out), iters, False)
+    clk = clocks.stop()
     pf_mean = statistics.mean(pf_ms)
     flops = 2.0 * S * S * d * hq
     pk = peaks()
@@ -733,6 +736,7 @@ def bench_prefill(local, iters=10, cpu=True):
                    "l2": "256 MiB read (L2 flush, no dirty lines) before every timed launch"},
         "map_16k_prompt_x4_ms": map_ms,
         "gpu_launches": len(pf_ms),
+        "clocks": clk,
     }
     if cpu:
         res["cpu_baseline"] = cpu_prefill_baseline(S, hq, hkv, d)

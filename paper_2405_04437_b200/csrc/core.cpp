@@ -1615,6 +1615,11 @@ using vattn::Manager;
 
 struct vattn_t {
   Manager* m = nullptr;
+  // per launching stream, the layer the last decode through this handle appended a row to (-1
+  // none): the next decode of a DIFFERENT layer may stream its K/V under PDL before that kernel
+  // completes (kernels.cu DecodeParams::kv_early)
+  std::mutex early_mu;
+  std::unordered_map<cudaStream_t, int32_t> last_append_layer;
   // Split-K decode workspaces, one per launching stream (concurrent decodes on two streams must
   // not share part_o/part_lse).  Never freed before vattn_destroy: a CUDA graph captured with a
   // workspace keeps its address, so a grown one only retires the old (ADVICE r1 core.cpp:1783).
@@ -1622,6 +1627,19 @@ struct vattn_t {
   std::unordered_map<cudaStream_t, std::pair<void*, int64_t>> ws;
   std::vector<void*> ws_all;
 };
+
+// Decide kv_early for a decode of `layer` on `st` and record whether it appends (fused).
+static void decode_pdl_hint(vattn_t* h, cudaStream_t st, int32_t layer, bool appends) {
+  static const bool on = [] {
+    const char* e = getenv("VATTN_DEC_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  std::lock_guard<std::mutex> lk(h->early_mu);
+  auto it = h->last_append_layer.find(st);
+  const int32_t prev = it == h->last_append_layer.end() ? -2 : it->second;
+  vattn::set_decode_kv_early(on && prev != -2 && prev != layer ? 1 : 0);
+  h->last_append_layer[st] = appends ? layer : -1;
+}
 
 // Workspace for a decode of `need` bytes on stream st.  The first one of a stream is sized for the
 // manager's max_batch, so it normally never grows; cudaMalloc runs with the thread's capture mode
@@ -1729,6 +1747,7 @@ vattn_status vattn_step(vattn_t* h, const int64_t* seq, int32_t n, vattn_step_re
   return guard([&] {
     const double t0 = vattn::now_us();
     const double waited = h->m->join_bg();
+    h->m->check_device_errors();
     h->m->begin_call();
     double us = 0.0;
     bool ok;
@@ -1757,6 +1776,7 @@ vattn_status vattn_iteration_step(vattn_t* h, const int64_t* seq, int32_t n, uin
     const double t0 = vattn::now_us();
     vattn_iteration_result r{};
     r.bg_wait_us = m.join_bg();
+    m.check_device_errors();
     m.begin_call();
     try {
       const bool want = (flags & (VATTN_BG_EAGER | VATTN_BG_RECLAIM)) != 0;
@@ -1959,6 +1979,7 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
     int64_t ws_bytes = 0;
     void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
                                 vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
+    decode_pdl_hint(h, (cudaStream_t)stream, layer, false);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream);
     h->m->mark_use((cudaStream_t)stream);
@@ -1980,6 +2001,7 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
     int64_t ws_bytes = 0;
     void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
                                 vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
+    decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
     h->m->mark_use((cudaStream_t)stream);
@@ -2052,6 +2074,7 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
     void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
                                 vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
+    decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale, num_splits,
                          ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
     h->m->mark_use((cudaStream_t)stream);
@@ -2074,6 +2097,7 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
     void* ws = decode_workspace(h, (cudaStream_t)stream, vattn_decode_workspace_bytes(batch, hq, v.d, 0),
                                 vattn_decode_workspace_bytes(h->m->max_batch(), hq, v.d, 0), &ws_bytes);
     const vattn::GatherSink s = vattn::gather_sink(g, hq, batch, v.d);
+    decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, &s);
     h->m->mark_use((cudaStream_t)stream);

@@ -135,6 +135,9 @@ GatherSink gather_sink(vattn_gather_t* g, int hq_local, int batch, int head_dim)
 
 // Decode row-order hint for the next launches on this thread (-1 none, 0 keep, 1 longest first).
 void set_decode_order_hint(int h);
+// PDL hint for the next decode launch on this thread: 1 = its K/V may be streamed before the
+// previous kernel on the stream completes (the host knows that kernel wrote no row of the layer).
+void set_decode_kv_early(int e);
 
 // Entry points from kernels.cu used by the handle-based C ABI wrappers in core.cpp.
 void launch_kv_append(KernelState* ks, int cache_key, const CacheView& v, const void* k_new,

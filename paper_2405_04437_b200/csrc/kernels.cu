@@ -149,6 +149,8 @@ struct DecodeParams {
   GatherSink sink;              // fused head all-gather (n_ranks = 0: write `out` only)
   int32_t longest_first;        // schedule rows by descending length (B <= 256)
   int32_t tail_guard;           // contiguous: load a row's partial last tile per row (CacheView)
+  int32_t kv_early;             // PDL: the producer may stream K/V before the previous kernel on
+                                // the stream completed (it wrote no row of this layer's cache)
   // contiguous read guard (CacheView::slot_rows / err): rows are clamped to the slot's readable
   // rows (and to slot_cap); slots outside [0, n_slots) read nothing
   const int32_t* slot_rows;
@@ -222,7 +224,12 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
 
   const int split = blockIdx.x, kvh = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (p.num_splits > 1) asm volatile("griddepcontrol.launch_dependents;");
+  // Programmatic dependent launch: the next kernel on the stream (this layer's
+  // split combine, or the next layer's decode) may launch once every CTA of this grid started, so
+  // its K/V streaming fills the SMs this grid's tail leaves idle.  Everything a dependent reads
+  // that this grid writes (out / partials / the appended row) is read after its
+  // griddepcontrol.wait, which waits for this whole grid.
+  asm volatile("griddepcontrol.launch_dependents;");
   // Longest rows first: CTA z takes the row with the z-th largest length (ties by index), so a
   // batch of mixed contexts does not finish on a tail of long rows started last (uniform(128,
   // 8192) contexts, B 64: 5.87 -> 6.5 TB/s, against 6.7 for equal lengths).
@@ -286,6 +293,9 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
         ptx::prefetch_tmap(&kmap);
         ptx::prefetch_tmap(&vmap);
       }
+      // K/V rows may have been written by the previous kernel (a fused append of this same
+      // layer): stream them early only when the host knows they were not (kv_early)
+      if (!p.kv_early) asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = 0; it < n_tiles; ++it) {
         const int st = it % STAGES;
         if (it >= STAGES) ptx::mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
@@ -347,6 +357,10 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
   }
 
   // ===== consumers: 4 warps x 16 tokens of every tile =====
+  // As a programmatic dependent of the previous kernel on the stream, q / k_new / v_new and the
+  // output (or split partials / gather staging) belong to it until it completes: wait here.  The
+  // producer warp above streams this layer's K/V meanwhile (a no-op for a normal launch).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // Q rows of this GQA group -> smem (rows >= group are zero padding of the m16 tile), rotated
   // at the new token's position when rotary tables are given
   const bool rotary = fused && p.rot.cos != nullptr;
@@ -575,7 +589,8 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __rest
   const int row = blockIdx.x * (blockDim.x / (D / 4)) + threadIdx.x / (D / 4);
   const int c4 = threadIdx.x % (D / 4);
   // launched as a programmatic dependent of the decode grid: wait until its partials are visible
-  // (a no-op for a normal launch)
+  // (a no-op for a normal launch); the next layer's decode may launch behind this grid
+  asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (row < rows) {
     // One batch of up to 16 splits per round trip: every lse and partial of the batch is
@@ -656,6 +671,8 @@ void kernel_state_free(KernelState* s) { delete s; }
 
 thread_local int g_order_hint = -1;
 void set_decode_order_hint(int h) { g_order_hint = h; }
+thread_local int g_kv_early = 0;
+void set_decode_kv_early(int e) { g_kv_early = e; }
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -758,16 +775,27 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
   using L = DecodeSmem<D, STAGES, CW>;
   auto kern = decode_kernel<D, STAGES, PAGED, CW>;
   ensure_smem_attr<decode_kernel<D, STAGES, PAGED, CW>>(L::kBytes);
-  dim3 grid(p.num_splits, hkv, batch);
-  kern<<<grid, decode_threads(CW), L::kBytes, st>>>(km, vm, p);
+  static const bool pdl = [] {
+    const char* e = getenv("VATTN_DEC_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.num_splits, hkv, batch);
+    cfg.blockDim = dim3(decode_threads(CW));
+    cfg.dynamicSmemBytes = L::kBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    check_rt(cudaLaunchKernelEx(&cfg, kern, km, vm, p), "decode launch");
+  }
   check_rt(cudaGetLastError(), "decode launch");
   if (p.num_splits > 1) {
     const int rows = batch * p.hq;
     const int per_block = 128 / (D / 4);
-    static const bool pdl = [] {
-      const char* e = getenv("VATTN_DEC_PDL");
-      return !e || atoi(e) != 0;
-    }();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((rows + per_block - 1) / per_block);
     cfg.blockDim = dim3(128);
@@ -850,6 +878,8 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   g_order_hint = -1;                 // a hint applies to the one launch it was set for
   const int lf = lf_env >= 0 ? lf_env : (hint > 0 ? 1 : 0);
   p.longest_first = (lf && batch > 1 && batch <= 256) ? 1 : 0;
+  p.kv_early = g_kv_early;
+  g_kv_early = 0;                   // like the order hint: applies to the one launch
   if (scale <= 0.f) scale = 1.f / sqrtf((float)d);
   p.scale_log2 = scale * 1.4426950408889634f;
   if (fa) {   // contiguous cache: row addresses for the fused append and the guarded tail tile

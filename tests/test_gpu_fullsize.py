@@ -83,3 +83,45 @@ def test_l8_full_layer_paged_equals_contiguous_and_splits_agree():
     for s in (2, 5):                              # split-K + LSE combine stays within tolerance
         out = decode_attention_raw(q, k, v, seq, num_splits=s)
         assert max_rel_err(out.float().cpu(), base.float().cpu()) <= 1e-2
+
+
+def test_pdl_layer_chain_equals_serial_launches():
+    """Decode launches are programmatic dependents of the previous kernel on the stream: a layer's
+    K/V stream starts under the previous layer's tail (kv_early), but never when the previous
+    launch appended to the SAME layer.  Back-to-back fused launches over 4 layers, then a plain
+    decode of the last layer that must see the row its predecessor appended, all bit-equal to the
+    raw-path kernels (which always wait) on plain-memory copies."""
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig
+    from paper_2405_04437_b200.attention import (decode_attention, decode_attention_append, decode_attention_append_raw,
+                                                 decode_attention_raw, kv_append)
+    from paper_2405_04437_b200.geometry import ModelGeometry
+
+    dev = _cuda()
+    N, B, ctx = 4, 16, 2000
+    g = ModelGeometry(N, 8, 128, 2, max_context=4096, max_batch=B, n_q_heads_total=32)
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=2 * N * B * 2 * MB2))
+    rids = [mgr.alloc_reqid() for _ in range(B)]
+    assert mgr.step([ctx + 2] * B).ok
+    gen = torch.Generator(device=dev).manual_seed(17)
+    idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+    zero = torch.zeros(B, dtype=torch.int32, device=dev)
+    for layer in range(N):
+        kv = torch.randn(B, ctx, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        kv_append(mgr, layer, kv, kv * 0.5, zero, idx)
+    q = torch.randn(N, B, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+    k1 = torch.randn(N, B, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+    pos = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    plain = [(mgr.k_cache(l)[rids, :ctx + 2].clone(), mgr.v_cache(l)[rids, :ctx + 2].clone()) for l in range(N)]
+    outs = [decode_attention_append(mgr, l, q[l], k1[l], k1[l] * 2, pos, idx, num_splits=s)
+            for l, s in zip(range(N), (1, 3, 0, 2))]
+    again = decode_attention(mgr, N - 1, q[0], pos + 1, idx)          # same layer as its predecessor
+    torch.cuda.synchronize()
+    for l, s in zip(range(N), (1, 3, 0, 2)):
+        kp, vp = plain[l]
+        want = decode_attention_append_raw(q[l], kp, vp, k1[l], k1[l] * 2, pos, num_splits=s)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[l], want), l
+    kp, vp = plain[N - 1]
+    assert torch.equal(again, decode_attention_raw(q[0], kp, vp, pos + 1))
+    mgr.close()
