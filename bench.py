@@ -1134,16 +1134,26 @@ def extra_decode_growth(local, steps=96, warm=8):
     return res
 
 
-def extra_serving(local, requests=48):
+def extra_serving(local, requests=48, out_dir=ROOT / "gpurun_out" / "serving_bench"):
     """BASELINE config 5: Algorithm-1 loop on the config-5 trace (Llama-3-8B shape), real kernels
-    + dense-layer compute proxy (reference IterationModel), sync vs overlapped+deferred+eager."""
+    + the dense layers as real bf16 GEMMs sized to the reference IterationModel (serving.GemmDense),
+    sync vs overlapped+deferred+eager (+ the B200 prefetch / staged variants) vs the paged layout.
+    Per-iteration CSVs and summaries go to gpurun_out/serving_bench/ (Fig. 11/13 analogs); the
+    whole 512-request trace runs in tools/serving_trace.py (profiles/r02_serving512/)."""
     from paper_2405_04437_b200.geometry import llama3_8b
-    from paper_2405_04437_b200.serving import IterationModel, load_trace_csv, median_prompt_groups, run, run_paged
+    from paper_2405_04437_b200.serving import GemmDense, load_trace_csv, median_prompt_groups, run, run_paged
 
     rows = load_trace_csv(ROOT / "tests" / "golden" / "trace_config5.csv")[:requests]
     g = llama3_8b(max_context=4096, max_batch=64)
     eager = median_prompt_groups(rows, g, MB2)
-    out = {"trace": f"tests/golden/trace_config5.csv first {requests} requests", "eager_groups": eager}
+    dense = GemmDense(device=local)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    out = {"trace": f"tests/golden/trace_config5.csv first {requests} requests", "eager_groups": eager,
+           "dense": f"bf16 GEMM units of {dense.unit_ms:.3f} ms sized to IterationModel (10 ms + 0.5 us/token)",
+           "csv_dir": str(out_dir.relative_to(ROOT))}
+    keys = ("iterations", "tokens_per_s", "exposed_map_ms_per_iter", "exposed_map_ms_p99", "exposed_map_ms_max",
+            "sync_alloc_ms_total", "stall_ms_total", "preemptions", "ttft_ms_p50", "ttft_ms_p99", "queue_ms_p50",
+            "queue_ms_p99", "mean_waste_bytes")
     variants = {
         "sync": dict(mode="sync"),
         "overlapped": dict(mode="overlapped"),
@@ -1160,13 +1170,13 @@ def extra_serving(local, requests=48):
     for mode, kw in variants.items():
         m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
                 eager_groups=eager if kw["mode"] == "overlapped" else 0, reclaim_threshold=0.10,
-                preemption_cap=100_000, dense_proxy=IterationModel(), **kw)
+                preemption_cap=100_000, dense_proxy=dense, **kw)
         s = m.summary()
+        m.write_iterations_csv(out_dir / f"{mode}.csv")
+        m.write_summary_json(out_dir / f"{mode}.json")
         its = m.iterations
         dec = [r.exposed_ms for r in its if r.prefills == 0]
-        out[mode] = {k: s[k] for k in ("iterations", "tokens_per_s", "exposed_map_ms_per_iter",
-                                       "exposed_map_ms_p99", "exposed_map_ms_max", "sync_alloc_ms_total",
-                                       "stall_ms_total", "preemptions")}
+        out[mode] = {k: s[k] for k in keys}
         out[mode]["exposed_map_ms_per_decode_iter"] = sum(dec) / max(1, len(dec))
         out[mode]["exposed_map_ms_median"] = statistics.median([r.exposed_ms for r in its]) if its else 0.0
         out[mode]["exposed_breakdown_ms"] = {k: sum(getattr(r, k) for r in its) for k in
@@ -1174,13 +1184,34 @@ def extra_serving(local, requests=48):
         out[mode]["driver_set_access_ms_total"] = sum(r.drv_set_access_ms for r in its)
         out[mode]["driver_maps_total"] = sum(r.drv_maps for r in its)
         out[mode]["kernel_ms_total"] = s["kernel_ms_total"]
+    # Layer-sliced layout (manager.py:93-96): one page-group spans all 32 layers of 32 tokens, so
+    # a request's tail wastes 1/N of what the per-layer layout wastes.  Memory
+    # is a property of the allocator state alone: all 512 requests on the model clock (shadow
+    # backend, the reference's IterationModel), and the staged wall-clock loop in the sliced layout.
+    full = load_trace_csv(ROOT / "tests" / "golden" / "trace_config5.csv")
+    waste = {}
+    for name, sl in (("layered", False), ("sliced", True)):
+        mm = run(full, g, clock="model", backend="shadow", mode="overlapped", page_group_size=MB2,
+                 pool_bytes=24 * GIB, eager_groups=median_prompt_groups(full, g, MB2, sliced=sl), sliced=sl,
+                 reclaim_threshold=0.10, preemption_cap=100_000).summary()
+        waste[name] = {"mean_waste_mib": mm["mean_waste_bytes"] / 2 ** 20,
+                       "peak_committed_gib": mm["peak_committed_bytes"] / GIB, "iterations": mm["iterations"]}
+    waste["waste_ratio_layered_over_sliced"] = waste["layered"]["mean_waste_mib"] / max(1e-9, waste["sliced"]["mean_waste_mib"])
+    out["sliced_vs_layered_512_model_clock"] = waste
+    m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB, sliced=True,
+            eager_groups=median_prompt_groups(rows, g, MB2, sliced=True), reclaim_threshold=0.10,
+            preemption_cap=100_000, dense_proxy=dense, **variants["overlapped_staged"])
+    s = m.summary()
+    m.write_iterations_csv(out_dir / "overlapped_staged_sliced.csv")
+    out["overlapped_staged_sliced"] = {k: s[k] for k in keys}
     # PagedAttention layout with the in-repo paged kernels (block 16), same trace and proxy
     import torch
     torch.cuda.empty_cache()
-    m = run_paged(rows, g, block_size=16, pool_bytes=24 * GIB, dense_proxy=IterationModel(), device=local)
+    m = run_paged(rows, g, block_size=16, pool_bytes=24 * GIB, dense_proxy=dense, device=local)
     s = m.summary()
-    out["paged_bs16"] = {k: s[k] for k in ("iterations", "tokens_per_s", "exposed_map_ms_per_iter",
-                                           "kernel_ms_total", "preemptions")}
+    m.write_iterations_csv(out_dir / "paged_bs16.csv")
+    m.write_summary_json(out_dir / "paged_bs16.json")
+    out["paged_bs16"] = {k: s[k] for k in keys + ("kernel_ms_total",) if k in s}
     out["paged_bs16"]["note"] = "exposed = host block allocation + block-table preparation + upload"
     return out
 

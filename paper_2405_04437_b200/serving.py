@@ -47,6 +47,59 @@ class IterationModel:
         return self.c0_ms + self.c1_ms_per_token * tokens
 
 
+class GemmDense:
+    """Dense layers of an iteration (QKV/O projections, MLP) as real bf16 GEMMs on the GPU, sized
+    to the reference IterationModel's duration (simulator.py:45-62): each unit multiplies a
+    [1024, 8192] activation by one of 8 distinct [8192, 8192] weight matrices (137 GFLOP and 128 MiB
+    of weights per unit, 1 GiB per cycle through the 8), so the attention kernels and the
+    allocator's driver calls see real tensor-core and HBM contention instead of an idle sleep.  Calibrated once at
+    construction (median unit time on this GPU).  cuBLAS, not a product kernel."""
+
+    def __init__(self, model: "IterationModel | None" = None, device: int = 0, n_weights: int = 8,
+                 dim: int = 8192, rows: int = 1024):
+        import torch
+
+        self.model = model or IterationModel()
+        dev = torch.device("cuda", device)
+        gen = torch.Generator(device=dev).manual_seed(1)
+        self.w = [torch.randn(dim, dim, device=dev, generator=gen, dtype=torch.bfloat16) * 0.01
+                  for _ in range(n_weights)]
+        self.x = torch.randn(rows, dim, device=dev, generator=gen, dtype=torch.bfloat16)
+        self.y = torch.empty(rows, dim, device=dev, dtype=torch.bfloat16)
+        self.i = 0
+        for _ in range(3):
+            self._unit()
+        torch.cuda.synchronize(dev)
+        times = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(16):
+                self._unit()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            times.append(e0.elapsed_time(e1) / 16)
+        self.unit_ms = sorted(times)[len(times) // 2]
+        self.launches = 0
+
+    def _unit(self):
+        import torch
+
+        torch.matmul(self.x, self.w[self.i % len(self.w)], out=self.y)
+        self.i += 1
+
+    def compute_ms(self, tokens: int) -> float:
+        return self.model.compute_ms(tokens)
+
+    def launch(self, tokens: int) -> int:
+        """Enqueue GEMM units totalling ~compute_ms(tokens) on the current stream."""
+        n = max(1, round(self.compute_ms(tokens) / self.unit_ms))
+        for _ in range(n):
+            self._unit()
+        self.launches += n
+        return n
+
+
 @dataclass
 class IterationRecord:
     iteration: int
@@ -96,6 +149,24 @@ class ServingMetrics:
     preemptions: int = 0
     init_alloc_ms: float = 0.0
     init_wall_ms: float = 0.0
+    # per request (trace index): arrival, first admission and first-token times (clock ms); the
+    # first token of a request is produced by the iteration that runs its prefill
+    req_arrival_ms: dict = field(default_factory=dict)
+    req_admit_ms: dict = field(default_factory=dict)
+    req_first_token_ms: dict = field(default_factory=dict)
+
+    def request_summary(self) -> dict:
+        """Time to first token and queueing delay (admission - arrival), ms: what staged admission
+        or a stalled iteration costs a request (not in the reference's summary)."""
+        ttft = [self.req_first_token_ms[i] - self.req_arrival_ms[i] for i in self.req_first_token_ms]
+        queue = [self.req_admit_ms[i] - self.req_arrival_ms[i] for i in self.req_admit_ms]
+        out = {"requests_with_first_token": len(ttft)}
+        for name, v in (("ttft_ms", ttft), ("queue_ms", queue)):
+            out[f"{name}_mean"] = sum(v) / len(v) if v else 0.0
+            out[f"{name}_p50"] = self._pct(v, 0.50)
+            out[f"{name}_p99"] = self._pct(v, 0.99)
+            out[f"{name}_max"] = max(v, default=0.0)
+        return out
 
     @staticmethod
     def _pct(values, q):
@@ -137,6 +208,7 @@ class ServingMetrics:
             "kernel_ms_total": sum(r.kernel_ms for r in its),
             "init_wall_ms": self.init_wall_ms,
         })
+        out.update(self.request_summary())
         return out
 
     def write_iterations_csv(self, path) -> None:
@@ -198,6 +270,7 @@ class SyntheticModel:
         from .attention import decode_attention_append, kv_append, prefill_attention, prefill_attention_varlen
 
         t = self.t
+        dense_tokens = sum(n for _, n in prefills) + len(decodes)
         if len(prefills) > 1:   # all new prompts' attention in one varlen launch per layer
             lens = [n for _, n in prefills]
             total = sum(lens)
@@ -224,13 +297,17 @@ class SyntheticModel:
                 decode_attention_append(self.mgr, layer, self.q_dec[:B], self.k_dec[:B], self.v_dec[:B],
                                         before, idx, out=self.out_dec[:B])
         if self.dense_model is not None:
-            # the dense layers (QKV/O projections, MLP) of the iteration, as device time
-            import ctypes as C
+            # the dense layers (QKV/O projections, MLP) of the iteration, as device time: real
+            # GEMMs (GemmDense) or the calibrated sleep kernel (IterationModel)
+            tokens = dense_tokens
+            if hasattr(self.dense_model, "launch"):
+                self.dense_model.launch(tokens)
+            else:
+                import ctypes as C
 
-            from ._abi import check, lib
-            tokens = sum(n for _, n in prefills) + len(decodes)
-            ns = int(self.dense_model.compute_ms(tokens) * 1e6)
-            check(lib().vattn_compute_proxy(ns, C.c_void_p(t.cuda.current_stream().cuda_stream)))
+                from ._abi import check, lib
+                ns = int(self.dense_model.compute_ms(tokens) * 1e6)
+                check(lib().vattn_compute_proxy(ns, C.c_void_p(t.cuda.current_stream().cuda_stream)))
 
 
 def median_prompt_groups(records, geometry, page_group_size: int, sliced: bool = False) -> int:
@@ -259,7 +336,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
         prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0,
         lazy_unmap: bool = False, stage_admission: bool = False, stage_max_iters: int = 8,
-        hold_worker: bool = False) -> ServingMetrics:
+        hold_worker: bool = False, record: list | None = None) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31).
 
     B200 additions (wall clock, CUDA backend; the allocator's logical state stays the
@@ -267,7 +344,13 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     their handle is needed; `stage_admission` holds an arrived request at the head of the queue
     (FIFO kept) until the slot alloc_reqid will give it has its prompt pages mapped by the
     prefetch worker, for at most `stage_max_iters` iterations and never while the batch is
-    empty, so prompt mapping overlaps the running batch's compute instead of stalling it."""
+    empty, so prompt mapping overlaps the running batch's compute instead of stalling it.
+
+    `record` (a list): append one entry per iteration with the logical allocator calls in the
+    reference's order (admits, the plan executed for this iteration, eager/reclaim, the step
+    arguments, preemptions, frees) and the allocator state after the step
+    (`parity_state()`, joining the background thread), for replay through the oracle
+    (tests/test_gpu_serving_replay.py)."""
     if mode not in ("sync", "overlapped"):
         raise ValueError(f"mode must be 'sync' or 'overlapped', got {mode!r}")
     if clock not in ("model", "wall"):
@@ -308,9 +391,12 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     overlapped = mode == "overlapped"
     drv_prev = mgr.driver_stats(peek=True) if wall else None
 
+    prev_plan = None
     while pending or running:
         if max_iterations is not None and iteration >= max_iterations:
             break
+        rec_it = {"it": iteration, "admits": [], "plan": prev_plan, "bg": overlapped, "steps": [],
+                  "preempted": [], "frees": []} if record is not None else None
         t_it = time.perf_counter()
         if wall:
             clock_us = max(clock_us, int((t_it - t_start) * 1e6))
@@ -339,6 +425,10 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             running[rid] = _Running(index, rec[1], rec[2], ctx=rec[1], admit_order=admit_counter)
             admit_counter += 1
             seq_lens[rid] = rec[1]
+            metrics.req_arrival_ms.setdefault(index, float(rec[0]))
+            metrics.req_admit_ms.setdefault(index, clock_us / 1000.0)
+            if record is not None:
+                rec_it["admits"].append(rid)
         if not running and pending:
             raise SimulationAborted("no request can be admitted into an empty batch")
         t_adm = time.perf_counter()
@@ -358,6 +448,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         else:
             r = mgr.step(seq_lens)
             ok, us = r.ok, r.sync_us
+        if record is not None:
+            rec_it["steps"].append(list(seq_lens))
         overflow_us = max(0.0, bg_us - prev_compute_budget_us)
         sync_us = us
         t_stp = time.perf_counter()
@@ -377,8 +469,14 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             r = mgr.step(seq_lens)
             ok = r.ok
             sync_us += r.sync_us
+            if record is not None:
+                rec_it["preempted"].append(victim)
+                rec_it["steps"].append(list(seq_lens))
         if observer is not None:
             observer(mgr, list(seq_lens), iteration)
+        if record is not None:
+            rec_it["state"] = mgr.parity_state()
+            record.append(rec_it)
 
         batch = len(running)
         tokens = sum(seq_lens[rid] for rid in running)
@@ -408,6 +506,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             for rid in running:
                 next_seq[rid] = min(seq_lens[rid] + 1, geometry.max_context)
             plan = mgr.plan_overlap(next_seq)
+            if record is not None:
+                prev_plan = [list(t_) for t_ in plan]
             if stage:
                 # prompts that have arrived -> the slots alloc_reqid would give them now; the
                 # prefetch worker backs them during these kernels (state is owned here: no join)
@@ -447,11 +547,15 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         t_ret = time.perf_counter()
         for rid in list(running):
             st = running[rid]
+            if st.produced == 0:
+                metrics.req_first_token_ms.setdefault(st.record_index, clock_us / 1000.0)
             st.produced += 1
             if st.produced >= st.decode_tokens:
                 metrics.completed_requests += 1
                 metrics.generated_tokens += st.decode_tokens
                 mgr.free_reqid(rid)
+                if record is not None:
+                    rec_it["frees"].append(rid)
                 seq_lens[rid] = 0
                 del running[rid]
             else:
@@ -560,6 +664,8 @@ def run_paged(records, geometry, *, block_size: int = 16, pool_bytes: int = 24 *
             rid = free_slots.popleft()
             running[rid] = _Running(idx, rec[1], rec[2], ctx=rec[1], admit_order=admit_counter)
             admit_counter += 1
+            metrics.req_arrival_ms.setdefault(idx, float(rec[0]))
+            metrics.req_admit_ms.setdefault(idx, clock_ms)
         preempted = 0
         for rid in sorted(running, key=lambda r: running[r].admit_order):
             while rid in running and not pool.grow(rid, running[rid].ctx):
@@ -606,8 +712,11 @@ def run_paged(records, geometry, *, block_size: int = 16, pool_bytes: int = 24 *
                     decode_attention_paged(q_dec[:Bd], k_pools[layer], v_pools[layer], tb, after, out=out_dec[:Bd])
             if dense_proxy is not None:
                 tokens_now = sum(running[r].ctx for r in pf) + len(dec)
-                check(lib().vattn_compute_proxy(int(dense_proxy.compute_ms(tokens_now) * 1e6),
-                                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                if hasattr(dense_proxy, "launch"):
+                    dense_proxy.launch(tokens_now)
+                else:
+                    check(lib().vattn_compute_proxy(int(dense_proxy.compute_ms(tokens_now) * 1e6),
+                                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)))
             torch.cuda.synchronize()
         kernel_ms = (time.perf_counter() - t_k) * 1e3
         tokens = sum(r.ctx for r in running.values())
@@ -617,8 +726,11 @@ def run_paged(records, geometry, *, block_size: int = 16, pool_bytes: int = 24 *
             committed_bytes=sum(len(b) for b in pool.owned.values()) * block_size * token_bytes,
             used_bytes=tokens * token_bytes, alloc_bytes=0, preemptions=preempted, exposed_ms=exposed_ms,
             kernel_ms=kernel_ms))
+        end_ms = metrics.iterations[-1].end_ms
         for rid in list(running):
             st = running[rid]
+            if st.produced == 0:
+                metrics.req_first_token_ms.setdefault(st.record_index, end_ms)
             st.produced += 1
             if st.produced >= st.decode_tokens:
                 metrics.completed_requests += 1

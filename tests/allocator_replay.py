@@ -175,3 +175,39 @@ class CoreAdapter:
 
     def close(self):
         self.m.close()
+
+
+def replay_serving_log(record, geo, page_group_size, pool, eager, threshold):
+    """Re-issue a serving.run(record=...) log to oracle/allocator.py in the reference order and
+    assert the allocator state after every iteration (see tests/test_gpu_serving_replay.py)."""
+    from oracle.allocator import Geometry, OracleManager
+
+    om = OracleManager(Geometry(geo.n_layers, geo.kv_heads_total, geo.head_dim, geo.bytes_per_elem,
+                                geo.max_context, geo.max_batch, geo.tp_degree), page_group_size, pool_bytes=pool,
+                       reclaim_threshold=threshold, eager_groups=eager)
+    stats = {"iterations": 0, "plans": 0, "preemptions": 0, "reclaims": 0}
+    for it in record:
+        for rid in it["admits"]:
+            assert om.alloc_reqid() == rid, (it["it"], "admit")
+        if it["bg"]:
+            if it["plan"]:
+                om.execute_plan([tuple(x) for x in it["plan"]])
+                stats["plans"] += 1
+            om.eager_prepare()
+            freed, _ = om.reclaim()
+            stats["reclaims"] += int(freed > 0)
+        ok, _ = om.step(it["steps"][0])
+        for victim, seq in zip(it["preempted"], it["steps"][1:]):
+            assert not ok
+            om.free_reqid(victim)
+            ok, _ = om.step(seq)
+            stats["preemptions"] += 1
+        assert ok, (it["it"], "step")
+        want = it["state"]
+        got = om.state()
+        for key in ("slots", "eager_slot", "created", "mapped", "precreated", "calls", "total_mapped_bytes"):
+            assert got[key] == want[key], (it["it"], key, got[key], want[key])
+        for rid in it["frees"]:
+            om.free_reqid(rid)
+        stats["iterations"] += 1
+    return stats

@@ -89,3 +89,29 @@ def test_config5_trace_prefix(ref_kvsim, mode):
     eager = median_prompt_groups(rows, ModelGeometry(**geo), MB2)
     _compare(ref_kvsim, geo, rows, page_group_size=MB2, pool_bytes=6 * GIB, mode=mode,
              eager_groups=eager, reclaim_threshold=0.10, preemption_cap=100_000)
+
+
+@pytest.mark.parametrize("mode", ["sync", "overlapped"])
+def test_serving_call_log_replays_through_oracle(mode):
+    """The serving loop's call recorder (serving.run(record=...)) replayed through the oracle on
+    the shadow backend: the harness tests/test_gpu_serving_replay.py applies to the GPU run."""
+    import random
+
+    from allocator_replay import replay_serving_log
+    from paper_2405_04437_b200.geometry import ModelGeometry
+    from paper_2405_04437_b200.serving import run
+
+    rnd = random.Random(3)
+    t, rows = 0, []
+    for _ in range(60):
+        t += rnd.randint(0, 20)
+        rows.append((t, rnd.randint(64, 3000), rnd.randint(2, 40)))
+    geo = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=8, n_q_heads_total=32)
+    record = []
+    m = run(rows, geo, clock="model", backend="shadow", mode=mode, page_group_size=MB2, pool_bytes=80 * MB2,
+            eager_groups=2 if mode == "overlapped" else 0, reclaim_threshold=0.10, preemption_cap=100_000,
+            record=record)
+    stats = replay_serving_log(record, geo, MB2, 80 * MB2, 2 if mode == "overlapped" else 0, 0.10)
+    assert stats["iterations"] == len(m.iterations) > 0
+    s = m.summary()
+    assert s["requests_with_first_token"] == 60
