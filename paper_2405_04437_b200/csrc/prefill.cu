@@ -35,19 +35,23 @@ namespace pf {
 constexpr int kBM = 128;           // query rows per tile
 constexpr int kBN = 128;           // keys per KV tile
 constexpr int kD = 128;            // head dim (Yi-6B / Llama / Yi-34B)
-constexpr int kStages = 2;         // K/V ring depth
+constexpr int kStages = 2;         // V ring depth
+constexpr int kKStages = 3;        // K ring depth: K runs one tile ahead of V, each stage released
+                                   // after its own last MMA (K: both S; V: both PV).  Measured +1.5 %
+                                   // (16K) over a shared 2-deep K/V ring (tools/pf_var_ab.py)
 constexpr int kThreads = 320;
 constexpr int kHalf = kBN * 128;               // one 64-column half of a 128-row tile (16 KB)
 constexpr float kRescaleThreshold = 8.0f;      // log2 domain: rescale O when max grows > 2^8
 
 // Shared-memory layout for head dim D (64 or 128): every 128-row tile is D/64 swizzled 64-column
 // halves of 16 KB.
-template <int D>
+template <int D, int KS = kKStages>
 struct PfL {
   static constexpr int kTile = (D / 64) * kHalf;
+  static constexpr int kKS = KS;                                // K ring depth
   static constexpr int kQOff = 0;                               // Q_A, Q_B
   static constexpr int kKOff = 2 * kTile;                       // K stages
-  static constexpr int kVOff = kKOff + kStages * kTile;
+  static constexpr int kVOff = kKOff + KS * kTile;
   static constexpr int kBarOff = kVOff + kStages * kTile;
   static constexpr int kSmem = kBarOff + 256 + 1024;
 };
@@ -271,19 +275,23 @@ template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
-  using L = PfL<D>;
+  // the paged comparison variant keeps one shared 2-deep K/V ring (K_j and V_j loaded together)
+  constexpr int KS = PAGED ? kStages : kKStages;     // K ring depth
+  constexpr bool SPLIT = !PAGED;                     // K / V stages released separately
+  using L = PfL<D, KS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;            // [kStages]
-  uint64_t* v_full = bars + 3;            // [kStages]
-  uint64_t* kv_empty = bars + 5;          // [kStages]
-  uint64_t* s_full = bars + 7;            // [2] tiles A, B
-  uint64_t* p_full = bars + 9;            // [2]
-  uint64_t* o_final = bars + 11;          // [2]
-  uint64_t* q_ready = bars + 13;          // rotary: both Q tiles rotated in shared memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* k_full = bars + 1;            // [KS]
+  uint64_t* v_full = bars + 5;            // [kStages]
+  uint64_t* k_empty = bars + 7;           // [KS]; releases K and V together unless SPLIT
+  uint64_t* v_empty = bars + 11;          // [kStages] (SPLIT only)
+  uint64_t* s_full = bars + 13;           // [2] tiles A, B
+  uint64_t* p_full = bars + 15;           // [2]
+  uint64_t* o_final = bars + 17;          // [2]
+  uint64_t* q_ready = bars + 19;          // rotary: both Q tiles rotated in shared memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int witem = p.head_fast ? blockIdx.y : blockIdx.x;
@@ -311,10 +319,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < KS; ++s) {
       ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&v_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&s_full[x], 1);
@@ -346,21 +357,35 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0A);
         ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0B);
       }
-      for (int j = 0; j < n_kv; ++j) {
+      if constexpr (!PAGED) {
+        // K runs KS - kStages tiles ahead of V (K_j then V_{j-ahead}); each stage waits for its
+        // own release (K and V share one release when !SPLIT)
+        constexpr int ahead = KS - kStages;
+        for (int j = 0; j < n_kv + ahead; ++j) {
+          if (j < n_kv) {
+            const int s = j % KS;
+            if (j >= KS) ptx::mbar_wait(&k_empty[s], ((j / KS) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&k_full[s], L::kTile);
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh, j * kBN);
+          }
+          const int jv = j - ahead;
+          if (jv >= 0) {
+            const int s = jv % kStages;
+            if (SPLIT && jv >= kStages) ptx::mbar_wait(&v_empty[s], ((jv / kStages) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh, jv * kBN);
+          }
+        }
+      }
+      for (int j = 0; PAGED && j < n_kv; ++j) {
         const int s = j % kStages;
-        if (j >= kStages) ptx::mbar_wait(&kv_empty[s], ((j / kStages) - 1) & 1);
+        if (j >= kStages) ptx::mbar_wait(&k_empty[s], ((j / kStages) - 1) & 1);
         ptx::mbar_arrive_expect_tx(&k_full[s], L::kTile);
-        if constexpr (!PAGED) {
-#pragma unroll
-          for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh,
-                             j * kBN);
-          ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
-#pragma unroll
-          for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh,
-                             j * kBN);
-        } else {
+        {
           // PagedAttention layout: one TMA box per KV block (4-D map over [D, Hkv, block, n_blocks])
           const int last_blk = (p.kv_len - 1) / p.block_size;
           for (int sub = 0; sub < kBN / p.box_tokens; ++sub) {
@@ -394,7 +419,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
       const int nX[2] = {nA, nB};
       auto issue_s = [&](int x, int j) {   // S_x(j) = Q_x K_j^T
-        const int s = j % kStages;
+        const int s = j % KS;
         const uint32_t qa = sbase + L::kQOff + x * L::kTile;
         const uint32_t kb = sbase + L::kKOff + s * L::kTile;
 #pragma unroll
@@ -415,11 +440,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       if (p.rot_cos) ptx::mbar_wait(q_ready, 0);
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % kStages;
-        ptx::mbar_wait(&k_full[s], (j / kStages) & 1);
-        fence_after();
         if (j == 0) {
+          ptx::mbar_wait(&k_full[0], 0);
+          fence_after();
           for (int x = 0; x < 2; ++x)
             if (nX[x] > 0) issue_s(x, 0);
+          if (SPLIT) mma_commit(&k_empty[0]);
         }
         ptx::mbar_wait(&v_full[s], (j / kStages) & 1);
         fence_after();
@@ -431,17 +457,24 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
           PF_TRACE(2 + x, j, 1);
           fence_after();
           issue_pv(x, j);
+          PF_TRACE(2 + x, j, 2);
           if (j + 1 == nX[x]) {
             mma_commit(&o_final[x]);
           } else {
             // S_x(j+1) needs K_{j+1}
-            const int s1 = (j + 1) % kStages;
-            ptx::mbar_wait(&k_full[s1], ((j + 1) / kStages) & 1);
+            const int s1 = (j + 1) % KS;
+            ptx::mbar_wait(&k_full[s1], ((j + 1) / KS) & 1);
             fence_after();
             issue_s(x, j + 1);
+            PF_TRACE(2 + x, j, 3);
           }
         }
-        mma_commit(&kv_empty[s]);   // K_j / V_j fully consumed once these MMAs retire
+        if (SPLIT) {
+          mma_commit(&v_empty[s]);                               // V_j: its last PV was issued
+          if (j + 1 < n_kv) mma_commit(&k_empty[(j + 1) % KS]);  // K_{j+1}: both its S issued
+        } else {
+          mma_commit(&k_empty[s]);   // K_j / V_j fully consumed once these MMAs retire
+        }
       }
     }
   } else {
@@ -915,9 +948,9 @@ void launch_prefill_paged(const void* q, const void* k_pool, const void* v_pool,
   p.block_table = block_table;
   p.block_size = block_size;
   p.box_tokens = box;
-  ensure_smem_attr<pf::prefill_kernel<0, true>>(pf::PfL<128>::kSmem);
+  ensure_smem_attr<pf::prefill_kernel<0, true>>(pf::PfL<128, pf::kStages>::kSmem);
   const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
-  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+  pf::prefill_kernel<0, true><<<grid, pf::kThreads, pf::PfL<128, pf::kStages>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
   check_rt(cudaGetLastError(), "prefill (paged) launch");
 }
 
