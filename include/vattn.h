@@ -101,6 +101,12 @@ typedef struct vattn_config {
    * its handle is needed elsewhere, or never when the slot grows back over it.  Needs
    * release_physical = 0. */
   int32_t lazy_unmap;
+  /* B200 addition: back `phys_chunk_groups` consecutive page-groups of a buffer with ONE physical
+   * handle (cuMemCreate of phys_chunk_groups x page_group_size), mapped by one cuMemMap + one
+   * cuMemSetAccess when the first of them is mapped (logically or speculatively) and unmapped when
+   * the last one goes.  The page-group bookkeeping (shadow state, counters, events) is unchanged;
+   * only the driver traffic and the physical footprint change.  0 or 1 = one handle per group. */
+  int32_t phys_chunk_groups;
 } vattn_config;
 
 typedef struct vattn_t vattn_t;
@@ -126,6 +132,8 @@ typedef struct vattn_counters {
   double init_wall_us;
   int64_t spec_maps, spec_hits, spec_steals, spec_pages;   /* physical prefetch */
   int64_t lazy_unmaps;         /* logical unmaps that kept the page mapped (lazy_unmap) */
+  /* physical chunks (phys_chunk_groups > 1): groups per chunk, chunks mapped now, their bytes */
+  int64_t phys_chunk_groups, phys_chunks_mapped, phys_mapped_bytes;
 } vattn_counters;
 
 typedef struct vattn_bg_result {

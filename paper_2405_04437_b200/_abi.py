@@ -38,6 +38,7 @@ class Config(C.Structure):
         ("log_events", c_i32), ("batch_set_access", c_i32),
         ("latency", C.POINTER(LatencyEntry)), ("n_latency", c_i32), ("prefetch_tokens", c_i32),
         ("prefetch_slots", c_i32), ("prefetch_slot_tokens", c_i32), ("lazy_unmap", c_i32),
+        ("phys_chunk_groups", c_i32),
     ]
 
 
@@ -54,7 +55,8 @@ class Counters(C.Structure):
             "real_maps", "real_unmaps", "real_set_access_calls", "real_creates", "real_releases")] + [
         (n, c_f64) for n in ("real_map_wall_us", "real_unmap_wall_us", "real_create_wall_us",
                              "real_set_access_wall_us", "init_wall_us")] + [
-        (n, c_i64) for n in ("spec_maps", "spec_hits", "spec_steals", "spec_pages", "lazy_unmaps")]
+        (n, c_i64) for n in ("spec_maps", "spec_hits", "spec_steals", "spec_pages", "lazy_unmaps",
+                             "phys_chunk_groups", "phys_chunks_mapped", "phys_mapped_bytes")]
 
 
 class BgResult(C.Structure):

@@ -338,6 +338,28 @@ class Manager {
   int64_t prefetch_tokens_ = 0;
   int64_t prefetch_slots_ = 0, prefetch_slot_tokens_ = 0;   // speculative eager for likely-next slots
   bool lazy_unmap_ = false;
+  // Physical chunks (phys_chunk_groups): chunk_ consecutive page-groups of a buffer share one
+  // physical handle, mapped (cuMemMap + cuMemSetAccess over chunk_ * t_ bytes) when its first group
+  // is referenced and unmapped when its last reference goes.  The per-group handles the logical
+  // layer passes around (phys_free_, spec_, Handle::real) are then plain tokens.
+  int64_t chunk_ = 1;
+  struct Chunk {
+    int32_t refs = 0;
+    bool busy = false;                 // a driver call on it is in flight (ch_mu_ released)
+    CUmemGenericAllocationHandle h = 0;
+  };
+  std::unordered_map<int64_t, Chunk> chunks_;                                        // ch_mu_
+  std::unordered_map<int64_t, std::vector<CUmemGenericAllocationHandle>> ch_free_;  // by bytes
+  std::mutex ch_mu_;
+  std::condition_variable ch_cv_;
+  std::atomic<uint64_t> next_token_{0};
+  int64_t ch_mapped_ = 0, ch_mapped_bytes_ = 0;
+  bool chunked() const { return chunk_ > 1; }
+  CUmemGenericAllocationHandle make_token() { return (1ull << 62) | ++next_token_; }
+  int64_t chunk_bytes(int64_t c) const { return std::min(chunk_ * t_, buffer_size_ - c * chunk_ * t_); }
+  void chunk_ref(int32_t b, int64_t off);
+  void chunk_unref(int32_t b, int64_t off);
+  void prop_size_create(CUmemGenericAllocationHandle* h, int64_t bytes);
   int64_t lazy_unmaps_ = 0;
   std::vector<std::pair<int32_t, int64_t>> pf_hints_;       // (slot, tokens) of queued prompts (pf_mu_)
   std::atomic<bool> prefetch_cancel_{false};   // legacy; the detached worker never blocks a join
@@ -448,6 +470,7 @@ Manager::Manager(const vattn_config& c) {
   prefetch_slots_ = std::max<int64_t>(0, c.prefetch_slots);
   prefetch_slot_tokens_ = std::max<int64_t>(0, c.prefetch_slot_tokens);
   lazy_unmap_ = c.lazy_unmap != 0 && c.release_physical == 0;
+  chunk_ = std::max<int64_t>(1, c.phys_chunk_groups);
 
   lat_ = LatencyTable::table2();
   if (c.latency && c.n_latency > 0) {
@@ -576,13 +599,25 @@ void Manager::pf_loop() {
     lk.unlock();
     const int64_t b = key / buffer_size_, off = key % buffer_size_;
     const double t0 = now_us();
-    bool ok = d.MemMap(va_[b] + off, (size_t)t_, 0, h, 0) == CUDA_SUCCESS;
-    const double t1 = now_us();
-    if (ok && d.MemSetAccess(va_[b] + off, (size_t)t_, &access_, 1) != CUDA_SUCCESS) {
-      d.MemUnmap(va_[b] + off, (size_t)t_);
-      ok = false;
+    bool ok;
+    double t1, t2;
+    if (chunked()) {           // one reference on the page's chunk: a driver call only if unmapped
+      try {
+        chunk_ref((int32_t)b, off);
+        ok = true;
+      } catch (...) {
+        ok = false;
+      }
+      t1 = t2 = now_us();
+    } else {
+      ok = d.MemMap(va_[b] + off, (size_t)t_, 0, h, 0) == CUDA_SUCCESS;
+      t1 = now_us();
+      if (ok && d.MemSetAccess(va_[b] + off, (size_t)t_, &access_, 1) != CUDA_SUCCESS) {
+        d.MemUnmap(va_[b] + off, (size_t)t_);
+        ok = false;
+      }
+      t2 = now_us();
     }
-    const double t2 = now_us();
     lk.lock();
     pf_inflight_ = -1;
     pf_map_us_ += t1 - t0;
@@ -614,6 +649,24 @@ Manager::~Manager() {
   const Driver& d = driver();
   d.CtxSetCurrent(ctx_);
   cudaDeviceSynchronize();
+  if (chunked()) {
+    const int64_t per_buf = buffer_size_ / t_ + 1;
+    for (auto& kv : chunks_)
+      if (kv.second.h) {
+        const int64_t b = kv.first / per_buf, c = kv.first % per_buf;
+        d.MemUnmap(va_[b] + (CUdeviceptr)(c * chunk_ * t_), (size_t)chunk_bytes(c));
+        d.MemRelease(kv.second.h);
+      }
+    for (auto& fl : ch_free_)
+      for (auto h : fl.second) d.MemRelease(h);
+    for (size_t b = 0; b < va_.size(); ++b) d.MemAddressFree(va_[b], (size_t)buffer_size_);
+    for (auto& se : use_events_) cudaEventDestroy(se.second);
+    if (d_rows_) cudaFree(d_rows_);
+    if (h_rows_) cudaFreeHost(h_rows_);
+    if (h_err_) cudaFreeHost(h_err_);
+    if (pub_stream_) cudaStreamDestroy(pub_stream_);
+    return;
+  }
   for (int32_t b = 0; b < (int32_t)buf_maps_.size(); ++b)
     for (auto& kv : buf_maps_[b]) d.MemUnmap(va_[b] + kv.first, (size_t)t_);
   for (auto& kv : handles_)
@@ -677,7 +730,21 @@ int64_t Manager::dev_create() {
 double Manager::dev_precreate(int64_t count) {
   if (count < 0) throw Fail(VATTN_VALUE_ERROR, "count must be >= 0");
   if (free_bytes() < count * t_) throw Fail(VATTN_POOL_EXHAUSTED, "cannot pre-create page-groups");
-  if (real()) {
+  if (real() && chunked()) {
+    // tokens for the logical layer; full-size chunk handles for the physical one
+    std::lock_guard<std::mutex> lk(pf_mu_);
+    for (int64_t i = 0; i < count; ++i) phys_free_.push_back(make_token());
+    const int64_t n = (count + chunk_ - 1) / chunk_;
+    std::lock_guard<std::mutex> lc(ch_mu_);
+    for (int64_t i = 0; i < n; ++i) {
+      CUmemGenericAllocationHandle h = 0;
+      const double t0 = now_us();
+      prop_size_create(&h, chunk_ * t_);
+      real_create_us_ += now_us() - t0;
+      real_creates_ += 1;
+      ch_free_[chunk_ * t_].push_back(h);
+    }
+  } else if (real()) {
     phys_free_.reserve(phys_free_.size() + (size_t)count);
     for (int64_t i = 0; i < count; ++i) {
       CUmemGenericAllocationHandle h = 0;
@@ -936,6 +1003,7 @@ CUmemGenericAllocationHandle Manager::real_create() {
     none_unattached = phys_free_.empty() && spec_.empty() && pf_inflight_ < 0;
   }
   if (!none_unattached) return take_unattached();
+  if (chunked()) return make_token();
   CUmemGenericAllocationHandle h = 0;
   const double t0 = now_us();
   check_cu(driver().MemCreate(&h, (size_t)t_, &prop_, 0), "cuMemCreate");
@@ -945,6 +1013,13 @@ CUmemGenericAllocationHandle Manager::real_create() {
 }
 
 void Manager::real_release(CUmemGenericAllocationHandle h) {
+  if (chunked()) {                 // a token: the physical chunk is released in chunk_unref
+    if (!release_physical_) {
+      std::lock_guard<std::mutex> lk(pf_mu_);
+      phys_free_.push_back(h);
+    }
+    return;
+  }
   if (!release_physical_) {
     std::lock_guard<std::mutex> lk(pf_mu_);
     phys_free_.push_back(h);
@@ -955,6 +1030,10 @@ void Manager::real_release(CUmemGenericAllocationHandle h) {
 }
 
 void Manager::real_map(int32_t b, int64_t off, CUmemGenericAllocationHandle h) {
+  if (chunked()) {
+    chunk_ref(b, off);
+    return;
+  }
   const Driver& d = driver();
   const double t0 = now_us();
   check_cu(d.MemMap(va_[b] + off, (size_t)t_, 0, h, 0), "cuMemMap");
@@ -1011,12 +1090,130 @@ void Manager::fence_unmap() {
 }
 
 void Manager::real_unmap(int32_t b, int64_t off) {
+  if (chunked()) {
+    shrink_rows(off);
+    chunk_unref(b, off);        // fences and unmaps only when the chunk's last group goes
+    return;
+  }
   fence_unmap();
   shrink_rows(off);
   const double t0 = now_us();
   check_cu(driver().MemUnmap(va_[b] + off, (size_t)t_), "cuMemUnmap");
   real_unmap_us_ += now_us() - t0;
   real_unmaps_ += 1;
+}
+
+void Manager::prop_size_create(CUmemGenericAllocationHandle* h, int64_t bytes) {
+  check_cu(driver().MemCreate(h, (size_t)bytes, &prop_, 0), "cuMemCreate(chunk)");
+}
+
+// Reference one page-group of chunk (b, off / (chunk_ * t_)); the first reference maps the chunk.
+// Driver calls run with ch_mu_ released (the chunk is marked busy), so a concurrent reference to
+// another chunk never waits behind them.
+void Manager::chunk_ref(int32_t b, int64_t off) {
+  const int64_t c = off / (chunk_ * t_);
+  const int64_t key = (int64_t)b * (buffer_size_ / t_ + 1) + c;
+  std::unique_lock<std::mutex> lk(ch_mu_);
+  Chunk& ch = chunks_[key];                  // node-based map: the reference stays valid
+  ch_cv_.wait(lk, [&] { return !ch.busy; });
+  ch.refs += 1;
+  if (ch.refs > 1) return;
+  const int64_t bytes = chunk_bytes(c);
+  CUmemGenericAllocationHandle h = 0;
+  auto& fl = ch_free_[bytes];
+  if (!fl.empty()) {
+    h = fl.back();
+    fl.pop_back();
+  }
+  ch.busy = true;
+  lk.unlock();
+  const Driver& d = driver();
+  CUresult e = CUDA_SUCCESS;
+  double t_create = 0, t_map = 0, t_acc = 0;
+  const double t0 = now_us();
+  if (!h) e = d.MemCreate(&h, (size_t)bytes, &prop_, 0);
+  const double t1 = now_us();
+  const CUdeviceptr va = va_[b] + (CUdeviceptr)(c * chunk_ * t_);
+  bool mapped = false;
+  if (e == CUDA_SUCCESS) {
+    e = d.MemMap(va, (size_t)bytes, 0, h, 0);
+    mapped = e == CUDA_SUCCESS;
+  }
+  const double t2 = now_us();
+  if (e == CUDA_SUCCESS) e = d.MemSetAccess(va, (size_t)bytes, &access_, 1);
+  const double t3 = now_us();
+  if (e != CUDA_SUCCESS && mapped) d.MemUnmap(va, (size_t)bytes);
+  t_create = t1 - t0;
+  t_map = t2 - t1;
+  t_acc = t3 - t2;
+  lk.lock();
+  ch.busy = false;
+  if (e != CUDA_SUCCESS) {
+    ch.refs -= 1;
+    if (h) ch_free_[bytes].push_back(h);
+    ch_cv_.notify_all();
+    lk.unlock();
+    check_cu(e, "cuMemCreate/cuMemMap/cuMemSetAccess(chunk)");
+  }
+  ch.h = h;
+  if (t_create > 1e-3) {      // a fresh handle (free list was empty)
+    real_create_us_ += t_create;
+    real_creates_ += 1;
+  }
+  real_map_us_ += t_map;
+  real_maps_ += 1;
+  real_access_us_ += t_acc;
+  real_access_ += 1;
+  ch_mapped_ += 1;
+  ch_mapped_bytes_ += bytes;
+  ch_cv_.notify_all();
+}
+
+void Manager::chunk_unref(int32_t b, int64_t off) {
+  const int64_t c = off / (chunk_ * t_);
+  const int64_t key = (int64_t)b * (buffer_size_ / t_ + 1) + c;
+  std::unique_lock<std::mutex> lk(ch_mu_);
+  auto it = chunks_.find(key);
+  if (it == chunks_.end() || it->second.refs < 1) throw Fail(VATTN_BAD_STATE, "chunk reference count underflow");
+  Chunk& ch = it->second;
+  ch_cv_.wait(lk, [&] { return !ch.busy; });
+  ch.refs -= 1;
+  if (ch.refs > 0) return;
+  ch.busy = true;
+  const CUmemGenericAllocationHandle h = ch.h;
+  const int64_t bytes = chunk_bytes(c);
+  lk.unlock();
+  CUresult e = CUDA_SUCCESS;
+  double t_unmap = 0;
+  try {
+    fence_unmap();            // queued kernels may still read the chunk
+    const double t0 = now_us();
+    e = driver().MemUnmap(va_[b] + (CUdeviceptr)(c * chunk_ * t_), (size_t)bytes);
+    t_unmap = now_us() - t0;
+  } catch (...) {
+    lk.lock();
+    ch.refs += 1;
+    ch.busy = false;
+    ch_cv_.notify_all();
+    throw;
+  }
+  if (e == CUDA_SUCCESS && release_physical_) e = driver().MemRelease(h);
+  lk.lock();
+  ch.busy = false;
+  if (e != CUDA_SUCCESS) {
+    ch.refs += 1;             // still mapped: keep the reference so state stays consistent
+    ch_cv_.notify_all();
+    lk.unlock();
+    check_cu(e, "cuMemUnmap(chunk)");
+  }
+  ch.h = 0;
+  if (!release_physical_) ch_free_[bytes].push_back(h);
+  else real_releases_ += 1;
+  real_unmap_us_ += t_unmap;
+  real_unmaps_ += 1;
+  ch_mapped_ -= 1;
+  ch_mapped_bytes_ -= bytes;
+  ch_cv_.notify_all();
 }
 
 void Manager::mark_use(cudaStream_t st) {
@@ -1497,21 +1694,27 @@ void Manager::counters(vattn_counters* o) const {
   o->init_us = init_us_;
   o->charged_us = charged_total();
   std::lock_guard<std::mutex> lk(pf_mu_);
-  o->real_maps = real_maps_ + pf_maps_;
+  // chunk mode: every driver call (control thread and prefetch worker) goes through chunk_ref /
+  // chunk_unref, which count them in real_*; pf_* then count the worker's logical pages only
+  const bool ck = chunked();
+  o->real_maps = real_maps_ + (ck ? 0 : pf_maps_);
   o->real_unmaps = real_unmaps_;
-  o->real_set_access_calls = real_access_ + pf_access_;
+  o->real_set_access_calls = real_access_ + (ck ? 0 : pf_access_);
   o->real_creates = real_creates_;
   o->real_releases = real_releases_;
-  o->real_map_wall_us = real_map_us_ + pf_map_us_;
+  o->real_map_wall_us = real_map_us_ + (ck ? 0 : pf_map_us_);
   o->real_unmap_wall_us = real_unmap_us_;
   o->real_create_wall_us = real_create_us_;
-  o->real_set_access_wall_us = real_access_us_ + pf_access_us_;
+  o->real_set_access_wall_us = real_access_us_ + (ck ? 0 : pf_access_us_);
   o->init_wall_us = init_wall_us_;
   o->spec_maps = spec_maps_;
   o->spec_hits = spec_hits_;
   o->spec_steals = spec_steals_;
   o->spec_pages = (int64_t)spec_.size();
   o->lazy_unmaps = lazy_unmaps_;
+  o->phys_chunk_groups = chunk_;
+  o->phys_chunks_mapped = ch_mapped_;
+  o->phys_mapped_bytes = chunked() ? ch_mapped_bytes_ : (real() ? total_mapped_bytes_ + (int64_t)spec_.size() * t_ : 0);
 }
 
 void Manager::slot_state(int64_t* out) const {

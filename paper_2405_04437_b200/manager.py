@@ -195,7 +195,7 @@ class KVCacheManager:
     def __init__(self, geometry, config, *, backend: str | None = None, device: int | None = None,
                  log_events: bool | None = None, release_physical: bool = False,
                  batch_set_access: bool = True, prefetch_tokens: int = 0, prefetch_slots: int = 0,
-                 prefetch_slot_tokens: int = 0, lazy_unmap: bool = False):
+                 prefetch_slot_tokens: int = 0, lazy_unmap: bool = False, phys_chunk_groups: int = 1):
         g = as_geometry(geometry)
         if g.max_batch < 1:
             raise ValueError("geometry.max_batch must be >= 1 to serve requests")
@@ -230,6 +230,9 @@ class KVCacheManager:
         cfg.prefetch_slots = int(prefetch_slots)
         cfg.prefetch_slot_tokens = int(prefetch_slot_tokens)
         cfg.lazy_unmap = int(bool(lazy_unmap))
+        if int(phys_chunk_groups) < 1:
+            raise ValueError("phys_chunk_groups must be >= 1")
+        cfg.phys_chunk_groups = int(phys_chunk_groups)
         lat, n_lat = _latency_entries(getattr(config, "latency_model", None))
         if lat is not None:
             cfg.latency, cfg.n_latency = C.cast(lat[0], C.POINTER(_abi.LatencyEntry)), n_lat

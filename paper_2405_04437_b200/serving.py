@@ -130,12 +130,15 @@ class IterationRecord:
     t_bgwait_ms: float = 0.0
     t_step_ms: float = 0.0
     t_retire_ms: float = 0.0
+    # physically mapped bytes (logical + speculative/lazily kept pages, or whole chunks with
+    # phys_chunk_groups > 1); equals committed_bytes on the model clock
+    phys_bytes: int = 0
 
     REF_FIELDS = ("iteration", "end_ms", "batch", "prefills", "tokens", "compute_ms", "sync_alloc_ms",
                   "stall_ms", "cpu_ms", "committed_bytes", "used_bytes", "alloc_bytes", "preemptions")
     CSV_FIELDS = REF_FIELDS + ("exposed_ms", "kernel_ms", "bg_wall_ms", "deferred", "drv_maps", "drv_unmaps",
                                "drv_set_access_ms", "drv_unmap_ms", "drv_create_ms", "t_admit_ms",
-                               "t_bgwait_ms", "t_step_ms", "t_retire_ms")
+                               "t_bgwait_ms", "t_step_ms", "t_retire_ms", "phys_bytes")
 
     def row(self, fields=CSV_FIELDS) -> list:
         return [getattr(self, f) for f in fields]
@@ -198,6 +201,8 @@ class ServingMetrics:
             "peak_committed_bytes": max((r.committed_bytes for r in its), default=0),
             "peak_used_bytes": max((r.used_bytes for r in its), default=0),
             "mean_waste_bytes": sum(r.committed_bytes - r.used_bytes for r in its) / n if n else 0.0,
+            "mean_phys_waste_bytes": sum(max(r.phys_bytes, r.committed_bytes) - r.used_bytes for r in its) / n if n else 0.0,
+            "peak_phys_bytes": max((max(r.phys_bytes, r.committed_bytes) for r in its), default=0),
             "init_alloc_ms": self.init_alloc_ms,
         }
         ex = [r.exposed_ms for r in its]
@@ -336,7 +341,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         manager: KVCacheManager | None = None, dense_proxy: IterationModel | None = None,
         prefetch_tokens: int = 0, prefetch_slots: int = 0, prefetch_slot_tokens: int = 0,
         lazy_unmap: bool = False, stage_admission: bool = False, stage_max_iters: int = 8,
-        hold_worker: bool = False, record: list | None = None) -> ServingMetrics:
+        hold_worker: bool = False, record: list | None = None, phys_chunk_groups: int = 1) -> ServingMetrics:
     """Replay `records` = [(arrival_ms, prompt_tokens, decode_tokens)] (trace.py:26-31).
 
     B200 additions (wall clock, CUDA backend; the allocator's logical state stays the
@@ -345,6 +350,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
     (FIFO kept) until the slot alloc_reqid will give it has its prompt pages mapped by the
     prefetch worker, for at most `stage_max_iters` iterations and never while the batch is
     empty, so prompt mapping overlaps the running batch's compute instead of stalling it.
+    `phys_chunk_groups` backs that many consecutive page-groups of a buffer with one physical
+    handle (one cuMemMap + cuMemSetAccess per chunk; bookkeeping still per 2 MiB group).
 
     `record` (a list): append one entry per iteration with the logical allocator calls in the
     reference's order (admits, the plan executed for this iteration, eager/reclaim, the step
@@ -368,7 +375,8 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
                                 reclaim_threshold=reclaim_threshold, eager_groups=eager_groups,
                                 sliced=sliced, pre_create_fraction=pre_create_fraction),
         backend=backend or ("cuda" if wall else "shadow"), prefetch_tokens=prefetch_tokens,
-        prefetch_slots=prefetch_slots, prefetch_slot_tokens=prefetch_slot_tokens, lazy_unmap=lazy_unmap)
+        prefetch_slots=prefetch_slots, prefetch_slot_tokens=prefetch_slot_tokens, lazy_unmap=lazy_unmap,
+        phys_chunk_groups=phys_chunk_groups)
     stage = bool(stage_admission) and wall and mode == "overlapped"
     staged_iters: dict[int, int] = {}     # record index -> iterations held at the queue head
     if wall and model is None:
@@ -486,9 +494,11 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
         if wall:
             cnt = mgr.peek_counters()
             alloc_cum, committed = cnt.total_mapped_bytes, cnt.mapped * cnt.page_group_size
+            phys = cnt.phys_mapped_bytes
         else:
             alloc_cum = mgr.vmm.total_mapped_bytes
             committed = mgr.committed_bytes()
+            phys = committed
         exposed_ms = (time.perf_counter() - t_exp) * 1e3
         # -- compute (line 14) + overlapped planning of the next iteration's maps --
         kernel_ms = 0.0
@@ -531,7 +541,7 @@ def run(records, geometry, *, mode: str = "overlapped", clock: str = "model",
             compute_ms=compute_ms, sync_alloc_ms=sync_us / 1000.0, stall_ms=stall_us / 1000.0, cpu_ms=0.0,
             committed_bytes=committed, used_bytes=tokens * token_bytes, alloc_bytes=alloc_cum - prev_alloc_cum,
             preemptions=preempted_here, exposed_ms=exposed_ms if wall else 0.0, kernel_ms=kernel_ms,
-            bg_wall_ms=bg_wall_ms, deferred=deferred))
+            bg_wall_ms=bg_wall_ms, deferred=deferred, phys_bytes=phys))
         if wall:
             drv = mgr.driver_stats(peek=True)
             rec = metrics.iterations[-1]

@@ -129,14 +129,14 @@ class CoreAdapter:
     backend="shadow" runs the same core without a device (CPU tests); backend="cuda" issues
     every map/unmap to the real driver at 2 MiB (GPU tests)."""
 
-    def __init__(self, fixture, backend="shadow"):
+    def __init__(self, fixture, backend="shadow", **mgr_kw):
         from paper_2405_04437_b200 import errors
         from paper_2405_04437_b200.geometry import ModelGeometry
         from paper_2405_04437_b200.manager import KVCacheManager, ManagerConfig
 
         self._errs = (errors.BatchFullError, errors.DoubleFreeError, ValueError, errors.VmmError)
         g = ModelGeometry(**fixture["geometry"])
-        self.m = KVCacheManager(g, ManagerConfig(**fixture["config"]), backend=backend, log_events=True)
+        self.m = KVCacheManager(g, ManagerConfig(**fixture["config"]), backend=backend, log_events=True, **mgr_kw)
 
     def init_info(self):
         m = self.m

@@ -34,6 +34,72 @@ def test_cuda_backend_bookkeeping_matches_reference(fixture):
         a.close()
 
 
+@pytest.mark.parametrize("fixture", GPU_FIXTURES[::3], ids=[f["name"] for f in GPU_FIXTURES[::3]])
+def test_cuda_backend_chunked_bookkeeping_matches_reference(fixture):
+    """phys_chunk_groups=4: four consecutive 2 MiB groups of a buffer share one 8 MiB physical
+    handle.  The logical state after every reference call is unchanged (bit-exact replay); the
+    driver sees at most as many cuMemMap calls as the 2 MiB mode, and the mapped chunks cover
+    every logically mapped group."""
+    _cuda()
+    a = CoreAdapter(fixture, backend="cuda", phys_chunk_groups=4)
+    try:
+        replay(fixture, a)
+        st = a.m.driver_stats()
+        c = a.m._counters()
+        assert c.phys_chunk_groups == 4
+        assert st["real_maps"] <= a.m.vmm.calls.get("cuMemMap", 0)
+        assert c.phys_mapped_bytes >= c.mapped * c.page_group_size
+        assert c.phys_chunks_mapped * 4 * MB2 >= c.phys_mapped_bytes
+    finally:
+        a.close()
+
+
+def test_chunked_cache_data_survives_neighbour_unmaps():
+    """Chunk mode on a real cache: rows written while their group shares a chunk with groups that
+    are later trimmed/reclaimed keep their values; decode over them equals the 2 MiB-mode result
+    bit for bit, with fewer driver maps."""
+    _cuda()
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+    from paper_2405_04437_b200.attention import decode_attention, kv_append
+
+    dev = torch.device("cuda")
+    g = ModelGeometry(2, 8, 128, 2, max_context=16384, max_batch=4, n_q_heads_total=32)
+    outs, maps = [], []
+    for chunk in (1, 4):
+        mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=256 * MB2, reclaim_threshold=0.0),
+                             phys_chunk_groups=chunk)
+        gen = torch.Generator(device=dev).manual_seed(5)
+        rids = [mgr.alloc_reqid() for _ in range(3)]
+        lens = [0] * 4
+        for r, n in zip(rids, (5000, 3000, 9000)):
+            lens[r] = n
+        assert mgr.step(lens).ok
+        idx = torch.tensor(rids, dtype=torch.int32, device=dev)
+        for layer in range(2):
+            for r in rids:
+                n = lens[r]
+                kv = torch.randn(1, n, 8, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+                kv_append(mgr, layer, kv, kv, torch.zeros(1, dtype=torch.int32, device=dev),
+                          torch.tensor([r], dtype=torch.int32, device=dev))
+        # free the middle request and shrink the first: their groups (and maybe chunks) go
+        mgr.free_reqid(rids[1])
+        lens[rids[1]] = 0
+        lens[rids[0]] = 2100
+        assert mgr.step(lens).ok
+        mgr.reclaim()
+        q = torch.randn(2, 32, 128, device=dev, generator=gen, dtype=torch.bfloat16)
+        sel = torch.tensor([rids[0], rids[2]], dtype=torch.int32, device=dev)
+        seq = torch.tensor([lens[rids[0]], lens[rids[2]]], dtype=torch.int32, device=dev)
+        o = [decode_attention(mgr, layer, q, seq, sel) for layer in range(2)]
+        torch.cuda.synchronize()
+        mgr.check_errors()
+        outs.append(torch.stack(o).cpu())
+        maps.append(mgr.driver_stats()["real_maps"])
+        mgr.close()
+    assert torch.equal(outs[0], outs[1])
+    assert maps[1] < maps[0]
+
+
 def test_tiny_config_end_to_end():
     """BASELINE config 1: 1 layer, 8 Q / 2 KV heads, D 64, batch 2, contexts 128-512, 2 MiB."""
     _cuda()
@@ -423,7 +489,9 @@ def test_device_read_guard_clamps_and_raises_without_faulting():
         # 5) prefill with kv_len past the backed rows is refused on the host
         with pytest.raises(ValueError, match="backs"):
             attention.prefill_attention(mgr, 0, torch.zeros(2000, 32, 128, device=dev, dtype=torch.bfloat16), r)
-        # the context is healthy: a normal decode still matches
+        # the context is healthy: restore rows 1020..1023 (step 4 overwrote them) and a normal
+        # decode matches the first one bit for bit
+        attention.kv_append(mgr, 0, kv[:, 1020:], kv[:, 1020:], torch.tensor([1020], dtype=torch.int32, device=dev), idx)
         again = attention.decode_attention(mgr, 0, q, torch.tensor([1024], dtype=torch.int32, device=dev), idx)
         torch.cuda.synchronize()
         assert torch.equal(again, good)

@@ -31,6 +31,7 @@ ap.add_argument("--dense-proxy", action="store_true", help="add IterationModel d
 ap.add_argument("--dense", choices=["sleep", "gemm"], default="gemm",
                 help="dense-layer proxy with --dense-proxy: bf16 GEMMs (default) or the sleep kernel")
 ap.add_argument("--sliced", action="store_true", help="layer-sliced cache layout (manager.py:93-96)")
+ap.add_argument("--chunk", type=int, default=1, help="page-groups per physical handle (phys_chunk_groups)")
 a = ap.parse_args()
 rows = load_trace_csv(Path("tests/golden/trace_config5.csv"))[: a.requests]
 g = llama3_8b(max_context=4096, max_batch=64)
@@ -45,10 +46,12 @@ else:
             preemption_cap=100_000, defer=not a.no_defer,
             dense_proxy=dense, prefetch_tokens=a.prefetch, sliced=a.sliced,
             prefetch_slots=a.spec_slots, prefetch_slot_tokens=a.spec_tokens, lazy_unmap=a.lazy_unmap,
-            stage_admission=a.stage > 0, stage_max_iters=a.stage, hold_worker=a.hold)
+            stage_admission=a.stage > 0, stage_max_iters=a.stage, hold_worker=a.hold,
+            phys_chunk_groups=a.chunk)
 s = m.summary()
 s.update({"mode": a.mode, "requests": a.requests, "eager_groups": eager, "defer": not a.no_defer,
-          "dense_proxy": (a.dense if a.dense_proxy else None), "sliced": a.sliced, "prefetch": a.prefetch, "lazy_unmap": a.lazy_unmap, "stage": a.stage})
+          "dense_proxy": (a.dense if a.dense_proxy else None), "sliced": a.sliced, "prefetch": a.prefetch, "lazy_unmap": a.lazy_unmap, "stage": a.stage,
+          "phys_chunk_groups": a.chunk})
 if a.mode != "paged":
     its = m.iterations
     s["exposed_map_ms_median"] = sorted(r.exposed_ms for r in its)[len(its) // 2] if its else 0.0
@@ -61,7 +64,7 @@ if a.out:
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     tag = (a.mode + (f"_{a.dense}" if a.dense_proxy else "") + ("_sliced" if a.sliced else "") + (f"_pf{a.prefetch}" if a.prefetch else "")
            + (f"_ss{a.spec_slots}x{a.spec_tokens}" if a.spec_slots else "") + ("_lazy" if a.lazy_unmap else "")
-           + (f"_stage{a.stage}" if a.stage else "") + ("_hold" if a.hold else ""))
+           + (f"_stage{a.stage}" if a.stage else "") + ("_hold" if a.hold else "") + (f"_chunk{a.chunk}" if a.chunk > 1 else ""))
     m.write_iterations_csv(a.out + f"_{tag}.csv")
     with open(a.out + f"_{tag}.json", "w") as fh:
         json.dump(s, fh, indent=1)
