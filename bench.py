@@ -1153,7 +1153,7 @@ def extra_serving(local, requests=48, out_dir=ROOT / "gpurun_out" / "serving_ben
            "csv_dir": str(out_dir.relative_to(ROOT))}
     keys = ("iterations", "tokens_per_s", "exposed_map_ms_per_iter", "exposed_map_ms_p99", "exposed_map_ms_max",
             "sync_alloc_ms_total", "stall_ms_total", "preemptions", "ttft_ms_p50", "ttft_ms_p99", "queue_ms_p50",
-            "queue_ms_p99", "mean_waste_bytes")
+            "queue_ms_p99", "mean_waste_bytes", "mean_phys_waste_bytes", "peak_phys_bytes")
     variants = {
         "sync": dict(mode="sync"),
         "overlapped": dict(mode="overlapped"),
@@ -1166,6 +1166,13 @@ def extra_serving(local, requests=48, out_dir=ROOT / "gpurun_out" / "serving_ben
         "overlapped_staged": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
                                   prefetch_slot_tokens=3072, lazy_unmap=True, stage_admission=True,
                                   stage_max_iters=32, hold_worker=True),
+        # 8 MiB physical handles behind the 2 MiB bookkeeping (phys_chunk_groups=4): one
+        # cuMemMap + cuMemSetAccess per four page-groups of a buffer
+        "sync_chunk4": dict(mode="sync", phys_chunk_groups=4),
+        "overlapped_chunk4": dict(mode="overlapped", phys_chunk_groups=4),
+        "overlapped_staged_chunk4": dict(mode="overlapped", prefetch_tokens=256, prefetch_slots=4,
+                                         prefetch_slot_tokens=3072, lazy_unmap=True, stage_admission=True,
+                                         stage_max_iters=32, hold_worker=True, phys_chunk_groups=4),
     }
     for mode, kw in variants.items():
         m = run(rows, g, clock="wall", page_group_size=MB2, pool_bytes=24 * GIB,
@@ -1391,7 +1398,15 @@ def main(argv=None):
                 "serving_staged": sv.get("overlapped_staged", {}).get("exposed_map_ms_per_iter"),
                 "serving_staged_p99": sv.get("overlapped_staged", {}).get("exposed_map_ms_p99"),
                 "serving_paged_layout_host": sv.get("paged_bs16", {}).get("exposed_map_ms_per_iter"),
+                "serving_reference_overlap_chunk4": sv.get("overlapped_chunk4", {}).get("exposed_map_ms_per_iter"),
+                "serving_staged_chunk4": sv.get("overlapped_staged_chunk4", {}).get("exposed_map_ms_per_iter"),
             }
+            # config-5 end to end: tokens/s of each vAttention loop over the paged-layout loop
+            pg = sv.get("paged_bs16", {}).get("tokens_per_s")
+            if pg:
+                line["serving_tokens_per_s_vs_paged"] = {
+                    k: round(v["tokens_per_s"] / pg, 3) for k, v in sv.items()
+                    if isinstance(v, dict) and v.get("tokens_per_s") and k != "paged_bs16"}
         print(json.dumps(line), flush=True)
     return 0
 

@@ -1714,7 +1714,7 @@ void Manager::counters(vattn_counters* o) const {
   o->lazy_unmaps = lazy_unmaps_;
   o->phys_chunk_groups = chunk_;
   o->phys_chunks_mapped = ch_mapped_;
-  o->phys_mapped_bytes = chunked() ? ch_mapped_bytes_ : (real() ? total_mapped_bytes_ + (int64_t)spec_.size() * t_ : 0);
+  o->phys_mapped_bytes = chunked() ? ch_mapped_bytes_ : (real() ? (mapped_ + (int64_t)spec_.size()) * t_ : 0);
 }
 
 void Manager::slot_state(int64_t* out) const {
