@@ -153,37 +153,6 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])     \
       : "memory")
 
-// 16-lane shapes (two softmax warps per lane quarter, SMW = 8): 16x256b.x8 gives each thread
-// rows (l, l + 8) of the warp's 16-lane window, l = lane / 4, columns 8k + 2(lane % 4) + {0, 1}
-// for k = 0..7 as r[4k + {0,1}] (row l) and r[4k + {2,3}] (row l + 8); 16x128b.x8 stores one
-// 32-bit column 4k + lane % 4 of rows l / l + 8 from r[2k] / r[2k + 1].
-#define TMEM_LD16_32(taddr, r)                                                                         \
-  asm volatile(                                                                                        \
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                       \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),           \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),    \
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),    \
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                            \
-      : "r"(taddr))
-#define TMEM_ST16_32(taddr, r)                                                                          \
-  asm volatile(                                                                                         \
-      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),         \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),    \
-      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),  \
-      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) \
-      : "memory")
-#define TMEM_ST16P(taddr, r)                                                                            \
-  asm volatile(                                                                                         \
-      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
-      "%15,%16};" ::"r"(taddr),                                                                         \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])     \
-      : "memory")
-
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -290,40 +259,6 @@ __device__ __forceinline__ void softmax_half(uint32_t tS, float2 sc2, float2 nm2
   }
 }
 
-// SMW = 8: 64 columns [tS, tS + 64) of the thread's two rows (16 values each): P packed into
-// pk[16] in 16x128b order, raw-score maxima into m0 / m1, pairwise sums into a0 / a1.
-__device__ __forceinline__ void softmax_half16(uint32_t tS, float sc, float nm0, float nm1, uint32_t* pk,
-                                               float& m0, float& m1, float2& a0, float2& a1) {
-  uint32_t r[32];
-  TMEM_LD16_32(tS, r);
-  tmem_wait_ld();
-  const float2 sc2 = make_float2(sc, sc), n0 = make_float2(nm0, nm0), n1 = make_float2(nm1, nm1);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float s00 = __uint_as_float(r[4 * k]), s01 = __uint_as_float(r[4 * k + 1]);
-    const float s10 = __uint_as_float(r[4 * k + 2]), s11 = __uint_as_float(r[4 * k + 3]);
-    m0 = max3(m0, s00, s01);
-    m1 = max3(m1, s10, s11);
-    const float2 x0 = __ffma2_rn(make_float2(s00, s01), sc2, n0);
-    const float2 x1 = __ffma2_rn(make_float2(s10, s11), sc2, n1);
-    const float p00 = ptx::fast_exp2(x0.x), p01 = ptx::fast_exp2(x0.y);
-    const float p10 = ptx::fast_exp2(x1.x), p11 = ptx::fast_exp2(x1.y);
-    a0 = __fadd2_rn(a0, make_float2(p00, p01));
-    a1 = __fadd2_rn(a1, make_float2(p10, p11));
-    pk[2 * k] = ptx::pack_bf16(p00, p01);
-    pk[2 * k + 1] = ptx::pack_bf16(p10, p11);
-  }
-}
-
-__device__ __forceinline__ float quad_max(float v) {
-  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
-  return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
-}
-__device__ __forceinline__ float quad_sum(float v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  return v + __shfl_xor_sync(0xffffffffu, v, 2);
-}
-
 // number of KV tiles a query tile starting at row q0 needs
 __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   if (q0 >= p.n_q) return 0;
@@ -336,271 +271,8 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
-// ===================== softmax, SMW = 8 (warps 0-7 tile A, 8-15 tile B) =====================
-// Warp w owns TMEM lanes 32 (w % 4) + 16 ((w / 4) % 2) + [0, 16) of tile w / 8; thread t holds rows
-// l = t / 4 and l + 8 of that window, 32 of their 128 columns (c = 8k + 2 (t % 4) + {0, 1}).  A
-// row's max and sum combine over the 4 threads t % 4 with two shuffles; nothing is exchanged
-// between warps.  Same online-softmax policy as SMW = 4: single pass against the running max
-// with the lazy 2^8 rescale, two-pass for first / masked tiles.
-template <bool VARLEN>
-__device__ __forceinline__ void softmax_w2(const Params& p, uint8_t* smem, uint64_t* s_full, uint64_t* p_full,
-                                           uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
-                                           int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
-                                           int nB, int n_kv, const CUtensorMap& omap) {
-  constexpr int D = 128;
-  using L = PfL<D, kKStages>;
-  const int x = warp / 8;
-  const int lw = 32 * (warp % 4) + 16 * ((warp / 4) % 2);   // first TMEM lane of the window
-  const int l = lane / 4, c4 = lane % 4;
-  const int row0 = lw + l, row1 = row0 + 8;                 // rows of the query tile
-  const int q0 = x == 0 ? q0A : q0B;
-  const int n = x == 0 ? nA : nB;
-  const int qp0 = q0 + row0, qp1 = q0 + row1;
-  const uint32_t lane_base = tmem + ((uint32_t)lw << 16);
-  const uint32_t tS = lane_base + x * 128;
-  const uint32_t tO = lane_base + 256 + x * D;
-  const float sc = p.scale_log2;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // l: this thread's partial row sums
-  if (p.rot_cos && n_kv > 0) {
-    // rotary: the first 128 threads of the tile's 256 rotate one query row each in shared memory
-    ptx::mbar_wait(q_full, 0);
-    const int li = (warp % 8) * 32 + lane;
-    const int qpos = q0 + li;
-    if (li < kBM && qpos < p.n_q) {
-      const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
-      const int64_t t = (int64_t)(qpos + p.q_off) * (p.rot_dim / 2);
-      const int nch = p.rot_dim / 8, half = p.rot_dim / 16;
-      for (int cc = 0; cc < nch; ++cc) {
-        if (!p.rot_inter && cc >= half) break;
-        const int pc = p.rot_inter ? cc : cc + half;
-        const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, li, cc & 7);
-        const uint32_t a1 = ptx::swz128(qt + (pc >> 3) * kHalf, li, pc & 7);
-        uint4 v0, v1;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(a0));
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(a1));
-        const uint4 r0 = ptx::rotary_chunk(v0, v1, cc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, p.rot_inter != 0);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(r0.x), "r"(r0.y), "r"(r0.z), "r"(r0.w));
-        if (!p.rot_inter) {
-          const uint4 r1 = ptx::rotary_chunk(v1, v0, pc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, false);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(r1.x), "r"(r1.y), "r"(r1.z), "r"(r1.w));
-        }
-      }
-    }
-    ptx::fence_proxy_async();
-    ptx::mbar_arrive(q_ready);
-  }
-  // O *= (f0 row l, f1 row l + 8) over all D columns of this thread's rows
-  auto rescale_o = [&](float f0, float f1) {
-#pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 64) {
-      uint32_t o[32];
-      TMEM_LD16_32(tO + c0, o);
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        o[4 * k] = __float_as_uint(__uint_as_float(o[4 * k]) * f0);
-        o[4 * k + 1] = __float_as_uint(__uint_as_float(o[4 * k + 1]) * f0);
-        o[4 * k + 2] = __float_as_uint(__uint_as_float(o[4 * k + 2]) * f1);
-        o[4 * k + 3] = __float_as_uint(__uint_as_float(o[4 * k + 3]) * f1);
-      }
-      TMEM_ST16_32(tO + c0, o);
-    }
-  };
-  for (int j = 0; j < n; ++j) {
-    if (lane == 0 && (warp % 8) == 0) PF_TRACE(x, j, 0);
-    ptx::mbar_wait(&s_full[x], j & 1);
-    if (lane == 0 && (warp % 8) == 0) PF_TRACE(x, j, 1);
-    fence_after();
-    const int k0 = j * kBN;
-    const int key_end0 = p.causal ? min(p.kv_len, qp0 + p.q_off + 1) : p.kv_len;
-    const int key_end1 = p.causal ? min(p.kv_len, qp1 + p.q_off + 1) : p.kv_len;
-    const bool need_mask = (k0 + kBN > key_end0) || (k0 + kBN > key_end1);
-    const bool warp_mask = __any_sync(0xffffffffu, need_mask);
-    if (!warp_mask && __all_sync(0xffffffffu, m0 != -INFINITY && m1 != -INFINITY)) {
-      // single pass against the running max, half a row (64 keys) at a time
-      float h0 = -INFINITY, h1 = -INFINITY;
-      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-      uint32_t pk[16];
-      softmax_half16(tS, sc, -m0, -m1, pk, h0, h1, a0, a1);
-      if (!__any_sync(0xffffffffu, h0 * sc > m0 + kRescaleThreshold || h1 * sc > m1 + kRescaleThreshold)) {
-        TMEM_ST16P(tS, pk);
-        float g0 = -INFINITY, g1 = -INFINITY;
-        float2 b0 = make_float2(0.f, 0.f), b1 = make_float2(0.f, 0.f);
-        softmax_half16(tS + 64, sc, -m0, -m1, pk, g0, g1, b0, b1);
-        if (!__any_sync(0xffffffffu, g0 * sc > m0 + kRescaleThreshold || g1 * sc > m1 + kRescaleThreshold)) {
-          TMEM_ST16P(tS + 32, pk);
-          l0 += (a0.x + a0.y) + (b0.x + b0.y);
-          l1 += (a1.x + a1.y) + (b1.x + b1.y);
-        } else {
-          // rare: keys 64..127 raised the max.  Row maxima over the quad, rescale O, l and the
-          // stored P of keys 0..63, recompute keys 64..127 from S (intact) against the new max.
-          const float mn0 = fmaxf(m0, quad_max(fmaxf(g0, h0)) * sc);
-          const float mn1 = fmaxf(m1, quad_max(fmaxf(g1, h1)) * sc);
-          const float f0 = ptx::fast_exp2(m0 - mn0), f1 = ptx::fast_exp2(m1 - mn1);
-          if (j > 0) rescale_o(f0, f1);
-          {
-            uint32_t pl[16];
-            asm volatile("tcgen05.ld.sync.aligned.16x128b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                         : "=r"(pl[0]), "=r"(pl[1]), "=r"(pl[2]), "=r"(pl[3]), "=r"(pl[4]), "=r"(pl[5]), "=r"(pl[6]),
-                           "=r"(pl[7]), "=r"(pl[8]), "=r"(pl[9]), "=r"(pl[10]), "=r"(pl[11]), "=r"(pl[12]), "=r"(pl[13]),
-                           "=r"(pl[14]), "=r"(pl[15])
-                         : "r"(tS));
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float f = (k & 1) ? f1 : f0;
-              __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&pl[k]);
-              const float2 fv = __bfloat1622float2(v);
-              pl[k] = ptx::pack_bf16(fv.x * f, fv.y * f);
-            }
-            TMEM_ST16P(tS, pl);
-          }
-          float d0 = -INFINITY, d1 = -INFINITY;
-          float2 c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f);
-          softmax_half16(tS + 64, sc, -mn0, -mn1, pk, d0, d1, c0, c1);
-          TMEM_ST16P(tS + 32, pk);
-          l0 = l0 * f0 + (a0.x + a0.y) * f0 + (c0.x + c0.y);
-          l1 = l1 * f1 + (a1.x + a1.y) * f1 + (c1.x + c1.y);
-          m0 = mn0;
-          m1 = mn1;
-        }
-        tmem_wait_st();
-        fence_before();
-        ptx::mbar_arrive(&p_full[x]);
-        if (lane == 0 && (warp % 8) == 0) PF_TRACE(x, j, 2);
-        continue;
-      }
-      // rare: the first half already raised the max: two-pass path below (nothing stored yet)
-    }
-    // pass 1: row maxima (masked where needed), combined over the quad
-    const int lim0 = key_end0 - k0, lim1 = key_end1 - k0;
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint32_t r[32];
-      TMEM_LD16_32(tS + 64 * h, r);
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = 64 * h + 8 * k + 2 * c4;
-        const float s00 = __uint_as_float(r[4 * k]), s01 = __uint_as_float(r[4 * k + 1]);
-        const float s10 = __uint_as_float(r[4 * k + 2]), s11 = __uint_as_float(r[4 * k + 3]);
-        mx0 = fmaxf(mx0, fmaxf(c < lim0 ? s00 : -INFINITY, c + 1 < lim0 ? s01 : -INFINITY));
-        mx1 = fmaxf(mx1, fmaxf(c < lim1 ? s10 : -INFINITY, c + 1 < lim1 ? s11 : -INFINITY));
-      }
-    }
-    mx0 = quad_max(mx0) * sc;
-    mx1 = quad_max(mx1) * sc;
-    const bool grow0 = (m0 == -INFINITY) ? (mx0 > -INFINITY) : (mx0 > m0 + kRescaleThreshold);
-    const bool grow1 = (m1 == -INFINITY) ? (mx1 > -INFINITY) : (mx1 > m1 + kRescaleThreshold);
-    if (__any_sync(0xffffffffu, grow0 || grow1)) {
-      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-      const float f0 = (m0 == -INFINITY) ? 0.f : ptx::fast_exp2(m0 - mn0);
-      const float f1 = (m1 == -INFINITY) ? 0.f : ptx::fast_exp2(m1 - mn1);
-      l0 *= f0;
-      l1 *= f1;
-      // O_x(j-1) is complete: S_x(j) was issued after PV_x(j-1) and has retired
-      if (j > 0 && __any_sync(0xffffffffu, f0 != 1.f || f1 != 1.f)) {
-        rescale_o(f0, f1);
-        tmem_wait_st();
-      }
-      m0 = mn0;
-      m1 = mn1;
-    }
-    // pass 2: P = exp2(S*scale - m) -> bf16 over the S columns already consumed
-    const float nm0 = m0 == -INFINITY ? 0.f : -m0, nm1 = m1 == -INFINITY ? 0.f : -m1;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint32_t r[32], pk[16];
-      TMEM_LD16_32(tS + 64 * h, r);
-      tmem_wait_ld();
-      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = 64 * h + 8 * k + 2 * c4;
-        const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1])),
-                                     make_float2(sc, sc), make_float2(nm0, nm0));
-        const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3])),
-                                     make_float2(sc, sc), make_float2(nm1, nm1));
-        float p00 = ptx::fast_exp2(x0.x), p01 = ptx::fast_exp2(x0.y);
-        float p10 = ptx::fast_exp2(x1.x), p11 = ptx::fast_exp2(x1.y);
-        if (warp_mask) {
-          p00 = c < lim0 ? p00 : 0.f;
-          p01 = c + 1 < lim0 ? p01 : 0.f;
-          p10 = c < lim1 ? p10 : 0.f;
-          p11 = c + 1 < lim1 ? p11 : 0.f;
-        }
-        a0 = __fadd2_rn(a0, make_float2(p00, p01));
-        a1 = __fadd2_rn(a1, make_float2(p10, p11));
-        pk[2 * k] = ptx::pack_bf16(p00, p01);
-        pk[2 * k + 1] = ptx::pack_bf16(p10, p11);
-      }
-      TMEM_ST16P(tS + 32 * h, pk);
-      l0 += a0.x + a0.y;
-      l1 += a1.x + a1.y;
-    }
-    tmem_wait_st();
-    fence_before();
-    ptx::mbar_arrive(&p_full[x]);
-    if (lane == 0 && (warp % 8) == 0) PF_TRACE(x, j, 2);
-  }
-  // ---- epilogue: O / l -> bf16 -> global (via the tile's Q buffer and a TMA store) ----
-  if (n > 0) {
-    ptx::mbar_wait(&o_final[x], 0);
-    fence_after();
-  }
-  l0 = quad_sum(l0);
-  l1 = quad_sum(l1);
-  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-  const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
-  const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
-  __nv_bfloat16* dst0 = p.out + ((int64_t)qp0 * p.hq + head) * D;
-  __nv_bfloat16* dst1 = p.out + ((int64_t)qp1 * p.hq + head) * D;
-  const bool live0 = qp0 < p.n_q, live1 = qp1 < p.n_q;
-#pragma unroll
-  for (int c0 = 0; c0 < D; c0 += 64) {
-    uint32_t o[32];
-    if (n > 0) {
-      TMEM_LD16_32(tO + c0, o);
-      tmem_wait_ld();
-    } else {
-#pragma unroll
-      for (int c = 0; c < 32; ++c) o[c] = 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int col = c0 + 8 * k + 2 * c4;              // this thread's two columns
-      const uint32_t v0 = ptx::pack_bf16(__uint_as_float(o[4 * k]) * inv0, __uint_as_float(o[4 * k + 1]) * inv0);
-      const uint32_t v1 = ptx::pack_bf16(__uint_as_float(o[4 * k + 2]) * inv1, __uint_as_float(o[4 * k + 3]) * inv1);
-      if (via_tma) {
-        const int cc = col / 8;
-        const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, row0, cc & 7) + 4 * c4;
-        const uint32_t a1 = ptx::swz128(qt + (cc >> 3) * kHalf, row1, cc & 7) + 4 * c4;
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a0), "r"(v0));
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a1), "r"(v1));
-      } else {
-        if (live0) *reinterpret_cast<uint32_t*>(dst0 + col) = v0;
-        if (live1) *reinterpret_cast<uint32_t*>(dst1 + col) = v1;
-      }
-    }
-  }
-  if (via_tma) {
-    ptx::fence_proxy_async();
-    asm volatile("bar.sync %0, 256;" ::"r"(1 + x) : "memory");   // the 8 warps of tile x
-    if (warp % 8 == 0 && lane == 0) {
-#pragma unroll
-      for (int h = 0; h < D / 64; ++h)
-        ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, head, q_row0 + q0);
-      ptx::tma_store_commit();
-      ptx::tma_store_wait_read();
-    }
-  }
-}
-
-// SMW = softmax warps per Q tile: 4 (one per TMEM lane quarter, 320 threads) or 8 (two per
-// quarter, each owning 16 lanes of it through the 16x256b / 16x128b TMEM shapes, 576 threads)
-template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false, int SMW = 4>
-__global__ void __launch_bounds__((2 * SMW + 2) * 32, 1)
+template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
+__global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
   // the paged comparison variant keeps one shared 2-deep K/V ring (K_j and V_j loaded together)
@@ -657,14 +329,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&s_full[x], 1);
-      ptx::mbar_init(&p_full[x], SMW * 32);
+      ptx::mbar_init(&p_full[x], kBM);
       ptx::mbar_init(&o_final[x], 1);
     }
-    ptx::mbar_init(q_ready, 2 * SMW * 32);
+    ptx::mbar_init(q_ready, 2 * kBM);
     ptx::fence_mbar_init();
   }
-  constexpr int kTmaWarp = 2 * SMW, kMmaWarp = 2 * SMW + 1;
-  if (warp == kMmaWarp) {
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      ptx::smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -674,7 +345,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kTmaWarp) {
+  if (warp == 8) {
     // ===================== TMA producer =====================
     if (lane == 0 && n_kv > 0) {
       ptx::prefetch_tmap(&qmap);
@@ -739,7 +410,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == 9) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0 && n_kv > 0) {
       const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
@@ -806,9 +477,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
       }
     }
-  } else if constexpr (SMW == 8) {
-    softmax_w2<VARLEN>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane, head, q_row0,
-                       q0A, q0B, nA, nB, n_kv, omap);
   } else {
     // ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
     const int x = warp / 4;
@@ -1041,7 +709,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   }
   fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == 9) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -1123,15 +791,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
   }
   constexpr int kS = pf::PfL<128>::kSmem;
-  static int smw = -1;
-  if (smw < 0) {
-    const char* e = getenv("VATTN_PF_SMW");    // softmax warps per Q tile: 4 or 8
-    smw = (e && atoi(e) == 8) ? 8 : 4;
-  }
-  if (poly == 0 && smw == 8) {
-    ensure_smem_attr<pf::prefill_kernel<0, false, 128, false, 8>>(kS);
-    pf::prefill_kernel<0, false, 128, false, 8><<<grid, 18 * 32, kS, st>>>(qmap, kmap, vmap, omap, p);
-  } else if (poly == 0) {
+  if (poly == 0) {
     ensure_smem_attr<pf::prefill_kernel<0>>(kS);
     pf::prefill_kernel<0><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
   } else if (poly == 1) {
