@@ -271,6 +271,258 @@ __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
   return last_key / kBN + 1;
 }
 
+// Arrive on a barrier of the CTA pair's leader (rank 0) when PAIR, else on the local one.
+template <bool PAIR>
+__device__ __forceinline__ void arrive_lead(uint64_t* bar) {
+  if constexpr (PAIR) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(ptx::smem_u32(bar)));
+    // default (.release.cta) semantics, as CUTLASS's umma_arrive_2x1SM_sm0: the P columns are
+    // ordered by tcgen05.wait::st + fence::before_thread_sync, and the leader's MMA reads them
+    // through the tensor core; a .cluster-scope release costs ~1000 cycles per arrival here
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+  } else {
+    ptx::mbar_arrive(bar);
+  }
+}
+
+// ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
+// One query row per thread (TMEM lane); used by the single-CTA kernel and by both CTAs of the
+// pair kernel (PAIR: P-ready / Q-ready arrivals go to the leader's barriers).
+template <int POLY, int D, bool VARLEN, bool PAIR, class L>
+__device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uint64_t* s_full, uint64_t* p_full,
+                                             uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
+                                             int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
+                                             int nB, int n_kv, const CUtensorMap& omap) {
+  const int x = warp / 4;
+  const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
+  const int q0 = x == 0 ? q0A : q0B;
+  const int n = x == 0 ? nA : nB;
+  const int qpos = q0 + row;
+  const uint32_t lane_base = tmem + (((warp % 4) * 32) << 16);
+  const uint32_t tS = lane_base + x * 128;
+  const uint32_t tO = lane_base + 256 + x * D;
+  float m_run = -INFINITY, l_run = 0.f;
+  if (p.rot_cos && n_kv > 0) {
+    // rotary: each thread rotates its own query row of tile x in the swizzled smem tile, then
+    // hands the tiles to the async proxy (tcgen05.mma reads Q from smem) and signals the issuer
+    ptx::mbar_wait(q_full, 0);
+    if (qpos < p.n_q) {
+      const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
+      const int64_t t = (int64_t)(qpos + p.q_off) * (p.rot_dim / 2);
+      const int nch = p.rot_dim / 8, half = p.rot_dim / 16;
+      for (int cc = 0; cc < nch; ++cc) {
+        if (!p.rot_inter && cc >= half) break;     // NeoX: the first-half chunk rotates both
+        const int pc = p.rot_inter ? cc : cc + half;
+        const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
+        const uint32_t a1 = ptx::swz128(qt + (pc >> 3) * kHalf, row, pc & 7);
+        uint4 v0, v1;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(a0));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(a1));
+        const uint4 r0 = ptx::rotary_chunk(v0, v1, cc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, p.rot_inter != 0);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(r0.x), "r"(r0.y), "r"(r0.z), "r"(r0.w));
+        if (!p.rot_inter) {
+          const uint4 r1 = ptx::rotary_chunk(v1, v0, pc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, false);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(r1.x), "r"(r1.y), "r"(r1.z), "r"(r1.w));
+        }
+      }
+    }
+    ptx::fence_proxy_async();
+    arrive_lead<PAIR>(q_ready);
+  }
+  for (int j = 0; j < n; ++j) {
+    if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
+    ptx::mbar_wait(&s_full[x], j & 1);
+    if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 1);
+    fence_after();
+    // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
+    // Only diagonal / tail tiles need the per-element mask; the others take the plain path.
+    const int k0 = j * kBN;
+    const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
+    const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
+    const bool warp_mask = __any_sync(0xffffffffu, need_mask);
+    if (!warp_mask && m_run != -INFINITY) {
+      // Single pass (common case): exponentiate against the running max while tracking the
+      // row max, half a row (64 keys) at a time; each half's P is stored only once its keys
+      // are known not to raise the max by more than 2^8 (then the stale max is kept, as the
+      // lazy rescale would).  S columns a half still needs are never overwritten early.
+      const float2 sc2f = make_float2(p.scale_log2, p.scale_log2);
+      const float2 nm2f = make_float2(-m_run, -m_run);
+      float m_lo = -INFINITY;
+      float2 acc_lo = make_float2(0.f, 0.f);
+      uint32_t pk[32];
+      softmax_half<POLY>(tS + 0, sc2f, nm2f, pk, m_lo, acc_lo);
+      if (!__any_sync(0xffffffffu, m_lo * p.scale_log2 > m_run + kRescaleThreshold)) {
+        TMEM_ST16(tS + 0, pk);
+        TMEM_ST16(tS + 16, (pk + 16));
+        float m_hi = -INFINITY;
+        float2 acc_hi = make_float2(0.f, 0.f);
+        softmax_half<POLY>(tS + 64, sc2f, nm2f, pk, m_hi, acc_hi);
+        const float mx_hi = m_hi * p.scale_log2;
+        if (!__any_sync(0xffffffffu, mx_hi > m_run + kRescaleThreshold)) {
+          TMEM_ST16(tS + 32, pk);
+          TMEM_ST16(tS + 48, (pk + 16));
+          l_run += (acc_lo.x + acc_lo.y) + (acc_hi.x + acc_hi.y);
+        } else {
+          // rare: keys 64..127 raised the max.  Rescale O and l, rescale the stored P of keys
+          // 0..63 in place, recompute keys 64..127 from S (intact) against the new max.
+          const float m_new = fmaxf(m_run, fmaxf(mx_hi, m_lo * p.scale_log2));
+          const float f = ptx::fast_exp2(m_run - m_new);
+          if (j > 0) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < D; c0 += 32) {
+              uint32_t o[32];
+              TMEM_LD32(tO + c0, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+              TMEM_ST32(tO + c0, o);
+            }
+          }
+          {
+            uint32_t pl[32];
+            TMEM_LD32(tS + 0, pl);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&pl[c]);
+              const float2 fv = __bfloat1622float2(v);
+              pl[c] = ptx::pack_bf16(fv.x * f, fv.y * f);
+            }
+            TMEM_ST32(tS + 0, pl);
+          }
+          float m_dummy = -INFINITY;
+          float2 acc_new = make_float2(0.f, 0.f);
+          softmax_half<POLY>(tS + 64, sc2f, make_float2(-m_new, -m_new), pk, m_dummy, acc_new);
+          TMEM_ST16(tS + 32, pk);
+          TMEM_ST16(tS + 48, (pk + 16));
+          l_run = l_run * f + (acc_lo.x + acc_lo.y) * f + (acc_new.x + acc_new.y);
+          m_run = m_new;
+        }
+        tmem_wait_st();
+        fence_before();
+        arrive_lead<PAIR>(&p_full[x]);
+        if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
+        continue;
+      }
+      // rare: the first half already raised the max: two-pass path below (nothing stored yet)
+    }
+    float mx = -INFINITY;
+    if (!warp_mask) {
+      float m3 = -INFINITY;
+#pragma unroll
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        uint32_t r[32];
+        TMEM_LD32(tS + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      }
+      mx = m3 * p.scale_log2;     // scale > 0: max commutes with the scaling
+    } else {
+#pragma unroll
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        uint32_t r[32];
+        TMEM_LD32(tS + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float v = (c0 + c < lim) ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, v);
+        }
+      }
+    }
+    // lazy rescale: keep the stale max unless it grows by more than 2^8 (warp-uniform decision)
+    const bool grow = (m_run == -INFINITY) ? (mx > -INFINITY) : (mx > m_run + kRescaleThreshold);
+    if (__any_sync(0xffffffffu, grow)) {
+      const float m_new = fmaxf(m_run, mx);
+      const float f = (m_run == -INFINITY) ? 0.f : ptx::fast_exp2(m_run - m_new);
+      l_run *= f;
+      if (j > 0 && __any_sync(0xffffffffu, f != 1.f)) {
+        // O_x(j-1) is complete: S_x(j) was issued after PV_x(j-1) and has retired
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t o[32];
+          TMEM_LD32(tO + c0, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+          TMEM_ST32(tO + c0, o);
+        }
+        tmem_wait_st();
+      }
+      m_run = m_new;
+    }
+    // pass 2: P = exp2(S*scale - m) -> bf16 into TMEM over the S columns already consumed.
+    // Packed f32x2 FMA/ADD (FFMA2/FADD2) halve the FMA-pipe instructions; MUFU does the exp2.
+    const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    const float2 nm2 = make_float2(neg_m, neg_m);
+    const float2 acc2 = warp_mask ? softmax_p_pass<true, POLY>(tS, sc2, nm2, lim)
+                                  : softmax_p_pass<false, POLY>(tS, sc2, nm2, lim);
+    const float lsum = acc2.x + acc2.y;
+    l_run += lsum;
+    tmem_wait_st();
+    fence_before();
+    arrive_lead<PAIR>(&p_full[x]);
+    if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
+  }
+  // ---- epilogue: O / l -> bf16 -> global ----
+  if (n > 0) {
+    ptx::mbar_wait(&o_final[x], 0);
+    fence_after();
+  }
+  const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+  // Full tiles (and any tile of a single-request launch: the map clips rows >= n_q) go out
+  // through shared memory and one TMA store: the tile's Q buffer is free once o_final landed
+  // (every MMA reading it has retired), and whole 128-byte rows reach L2 instead of the
+  // half-sector 16-byte stores of one row per thread.  Varlen tail tiles store directly so
+  // they cannot spill into the next request's rows.  A tile that sees no keys (n == 0) also
+  // stores its zeros directly: it never waited for its Q load, which may still be landing in
+  // that buffer (found under compute-sanitizer's slowed timing).
+  const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
+  const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
+  __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
+  const bool live = qpos < p.n_q;
+#pragma unroll
+  for (int c0 = 0; c0 < D; c0 += 32) {
+    uint32_t o[32];
+    if (n > 0) {
+      TMEM_LD32(tO + c0, o);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) o[c] = 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      uint4 v;
+      v.x = ptx::pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
+      v.y = ptx::pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
+      v.z = ptx::pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
+      v.w = ptx::pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
+      if (via_tma) {
+        const int cc = (c0 + c) / 8;
+        const uint32_t a = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+      } else if (live) {
+        *reinterpret_cast<uint4*>(dst + c0 + c) = v;
+      }
+    }
+  }
+  if (via_tma) {
+    ptx::fence_proxy_async();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");   // the 4 warps of tile x
+    if (warp % 4 == 0 && lane == 0) {
+#pragma unroll
+      for (int h = 0; h < D / 64; ++h)
+        ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, head, q_row0 + q0);
+      ptx::tma_store_commit();
+      ptx::tma_store_wait_read();
+    }
+  }
+}
+
 template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -478,234 +730,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       }
     }
   } else {
-    // ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
-    const int x = warp / 4;
-    const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
-    const int q0 = x == 0 ? q0A : q0B;
-    const int n = x == 0 ? nA : nB;
-    const int qpos = q0 + row;
-    const uint32_t lane_base = tmem + (((warp % 4) * 32) << 16);
-    const uint32_t tS = lane_base + x * 128;
-    const uint32_t tO = lane_base + 256 + x * D;
-    float m_run = -INFINITY, l_run = 0.f;
-    if (p.rot_cos && n_kv > 0) {
-      // rotary: each thread rotates its own query row of tile x in the swizzled smem tile, then
-      // hands the tiles to the async proxy (tcgen05.mma reads Q from smem) and signals the issuer
-      ptx::mbar_wait(q_full, 0);
-      if (qpos < p.n_q) {
-        const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
-        const int64_t t = (int64_t)(qpos + p.q_off) * (p.rot_dim / 2);
-        const int nch = p.rot_dim / 8, half = p.rot_dim / 16;
-        for (int cc = 0; cc < nch; ++cc) {
-          if (!p.rot_inter && cc >= half) break;     // NeoX: the first-half chunk rotates both
-          const int pc = p.rot_inter ? cc : cc + half;
-          const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
-          const uint32_t a1 = ptx::swz128(qt + (pc >> 3) * kHalf, row, pc & 7);
-          uint4 v0, v1;
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(a0));
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(a1));
-          const uint4 r0 = ptx::rotary_chunk(v0, v1, cc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, p.rot_inter != 0);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(r0.x), "r"(r0.y), "r"(r0.z), "r"(r0.w));
-          if (!p.rot_inter) {
-            const uint4 r1 = ptx::rotary_chunk(v1, v0, pc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, false);
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(r1.x), "r"(r1.y), "r"(r1.z), "r"(r1.w));
-          }
-        }
-      }
-      ptx::fence_proxy_async();
-      ptx::mbar_arrive(q_ready);
-    }
-    for (int j = 0; j < n; ++j) {
-      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
-      ptx::mbar_wait(&s_full[x], j & 1);
-      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 1);
-      fence_after();
-      // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
-      // Only diagonal / tail tiles need the per-element mask; the others take the plain path.
-      const int k0 = j * kBN;
-      const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
-      const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
-      const bool warp_mask = __any_sync(0xffffffffu, need_mask);
-      if (!warp_mask && m_run != -INFINITY) {
-        // Single pass (common case): exponentiate against the running max while tracking the
-        // row max, half a row (64 keys) at a time; each half's P is stored only once its keys
-        // are known not to raise the max by more than 2^8 (then the stale max is kept, as the
-        // lazy rescale would).  S columns a half still needs are never overwritten early.
-        const float2 sc2f = make_float2(p.scale_log2, p.scale_log2);
-        const float2 nm2f = make_float2(-m_run, -m_run);
-        float m_lo = -INFINITY;
-        float2 acc_lo = make_float2(0.f, 0.f);
-        uint32_t pk[32];
-        softmax_half<POLY>(tS + 0, sc2f, nm2f, pk, m_lo, acc_lo);
-        if (!__any_sync(0xffffffffu, m_lo * p.scale_log2 > m_run + kRescaleThreshold)) {
-          TMEM_ST16(tS + 0, pk);
-          TMEM_ST16(tS + 16, (pk + 16));
-          float m_hi = -INFINITY;
-          float2 acc_hi = make_float2(0.f, 0.f);
-          softmax_half<POLY>(tS + 64, sc2f, nm2f, pk, m_hi, acc_hi);
-          const float mx_hi = m_hi * p.scale_log2;
-          if (!__any_sync(0xffffffffu, mx_hi > m_run + kRescaleThreshold)) {
-            TMEM_ST16(tS + 32, pk);
-            TMEM_ST16(tS + 48, (pk + 16));
-            l_run += (acc_lo.x + acc_lo.y) + (acc_hi.x + acc_hi.y);
-          } else {
-            // rare: keys 64..127 raised the max.  Rescale O and l, rescale the stored P of keys
-            // 0..63 in place, recompute keys 64..127 from S (intact) against the new max.
-            const float m_new = fmaxf(m_run, fmaxf(mx_hi, m_lo * p.scale_log2));
-            const float f = ptx::fast_exp2(m_run - m_new);
-            if (j > 0) {
-#pragma unroll 1
-              for (int c0 = 0; c0 < D; c0 += 32) {
-                uint32_t o[32];
-                TMEM_LD32(tO + c0, o);
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-                TMEM_ST32(tO + c0, o);
-              }
-            }
-            {
-              uint32_t pl[32];
-              TMEM_LD32(tS + 0, pl);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&pl[c]);
-                const float2 fv = __bfloat1622float2(v);
-                pl[c] = ptx::pack_bf16(fv.x * f, fv.y * f);
-              }
-              TMEM_ST32(tS + 0, pl);
-            }
-            float m_dummy = -INFINITY;
-            float2 acc_new = make_float2(0.f, 0.f);
-            softmax_half<POLY>(tS + 64, sc2f, make_float2(-m_new, -m_new), pk, m_dummy, acc_new);
-            TMEM_ST16(tS + 32, pk);
-            TMEM_ST16(tS + 48, (pk + 16));
-            l_run = l_run * f + (acc_lo.x + acc_lo.y) * f + (acc_new.x + acc_new.y);
-            m_run = m_new;
-          }
-          tmem_wait_st();
-          fence_before();
-          ptx::mbar_arrive(&p_full[x]);
-          if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
-          continue;
-        }
-        // rare: the first half already raised the max: two-pass path below (nothing stored yet)
-      }
-      float mx = -INFINITY;
-      if (!warp_mask) {
-        float m3 = -INFINITY;
-#pragma unroll
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
-          uint32_t r[32];
-          TMEM_LD32(tS + c0, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) m3 = max3(m3, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-        }
-        mx = m3 * p.scale_log2;     // scale > 0: max commutes with the scaling
-      } else {
-#pragma unroll
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
-          uint32_t r[32];
-          TMEM_LD32(tS + c0, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float v = (c0 + c < lim) ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
-            mx = fmaxf(mx, v);
-          }
-        }
-      }
-      // lazy rescale: keep the stale max unless it grows by more than 2^8 (warp-uniform decision)
-      const bool grow = (m_run == -INFINITY) ? (mx > -INFINITY) : (mx > m_run + kRescaleThreshold);
-      if (__any_sync(0xffffffffu, grow)) {
-        const float m_new = fmaxf(m_run, mx);
-        const float f = (m_run == -INFINITY) ? 0.f : ptx::fast_exp2(m_run - m_new);
-        l_run *= f;
-        if (j > 0 && __any_sync(0xffffffffu, f != 1.f)) {
-          // O_x(j-1) is complete: S_x(j) was issued after PV_x(j-1) and has retired
-#pragma unroll 1
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t o[32];
-            TMEM_LD32(tO + c0, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-            TMEM_ST32(tO + c0, o);
-          }
-          tmem_wait_st();
-        }
-        m_run = m_new;
-      }
-      // pass 2: P = exp2(S*scale - m) -> bf16 into TMEM over the S columns already consumed.
-      // Packed f32x2 FMA/ADD (FFMA2/FADD2) halve the FMA-pipe instructions; MUFU does the exp2.
-      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-      const float2 nm2 = make_float2(neg_m, neg_m);
-      const float2 acc2 = warp_mask ? softmax_p_pass<true, POLY>(tS, sc2, nm2, lim)
-                                    : softmax_p_pass<false, POLY>(tS, sc2, nm2, lim);
-      const float lsum = acc2.x + acc2.y;
-      l_run += lsum;
-      tmem_wait_st();
-      fence_before();
-      ptx::mbar_arrive(&p_full[x]);
-      if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
-    }
-    // ---- epilogue: O / l -> bf16 -> global ----
-    if (n > 0) {
-      ptx::mbar_wait(&o_final[x], 0);
-      fence_after();
-    }
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    // Full tiles (and any tile of a single-request launch: the map clips rows >= n_q) go out
-    // through shared memory and one TMA store: the tile's Q buffer is free once o_final landed
-    // (every MMA reading it has retired), and whole 128-byte rows reach L2 instead of the
-    // half-sector 16-byte stores of one row per thread.  Varlen tail tiles store directly so
-    // they cannot spill into the next request's rows.  A tile that sees no keys (n == 0) also
-    // stores its zeros directly: it never waited for its Q load, which may still be landing in
-    // that buffer (found under compute-sanitizer's slowed timing).
-    const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
-    const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
-    __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
-    const bool live = qpos < p.n_q;
-#pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t o[32];
-      if (n > 0) {
-        TMEM_LD32(tO + c0, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) o[c] = 0u;
-      }
-#pragma unroll
-      for (int c = 0; c < 32; c += 8) {
-        uint4 v;
-        v.x = ptx::pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
-        v.y = ptx::pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
-        v.z = ptx::pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
-        v.w = ptx::pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
-        if (via_tma) {
-          const int cc = (c0 + c) / 8;
-          const uint32_t a = ptx::swz128(qt + (cc >> 3) * kHalf, row, cc & 7);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
-        } else if (live) {
-          *reinterpret_cast<uint4*>(dst + c0 + c) = v;
-        }
-      }
-    }
-    if (via_tma) {
-      ptx::fence_proxy_async();
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");   // the 4 warps of tile x
-      if (warp % 4 == 0 && lane == 0) {
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, head, q_row0 + q0);
-        ptx::tma_store_commit();
-        ptx::tma_store_wait_read();
-      }
-    }
+    softmax_role<POLY, D, VARLEN, false, L>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane,
+                                            head, q_row0, q0A, q0B, nA, nB, n_kv, omap);
   }
   fence_before();
   __syncthreads();
@@ -715,6 +741,270 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   }
 }
 
+
+
+// ===================== CTA-pair kernel (tcgen05 cta_group::2) =====================
+// Two CTAs of a cluster = two query heads of one GQA group over the same 256 query rows.  The
+// leader (rank 0) issues every MMA for both with M = 256 (rows 0-127 = leader's head, 128-255 =
+// peer's): each SM supplies its own Q tile as its half of A and HALF of the B operand (K: 64 of
+// the 128 keys of a tile; V: 64 of the 128 head-dim columns), and the hardware multicasts the B
+// halves between the pair.  Per SM and 128-key step that halves the B-operand reads and the TMA
+// writes of the single-CTA kernel, whose S MMAs are shared-memory bound.  S, P and O
+// of a head live in its own CTA's TMEM, so the softmax warps are the single-CTA ones.
+template <int D>
+struct PairL {
+  static_assert(D == 128, "the pair kernel is built for head_dim 128");
+  static constexpr int kKS = 4, kVS = 3;               // ring depths (stages of half tiles)
+  static constexpr int kTile = 2 * kHalf;              // one Q tile: 128 rows x 128 d (32 KB)
+  static constexpr int kKHalf = 64 * 128;              // K half-tile, one 64-d half: 64 keys x 128 B
+  static constexpr int kKStage = 2 * kKHalf;           // 16 KB
+  static constexpr int kVStage = kHalf;                // V half-tile: 128 keys x 64 d (16 KB)
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = 2 * kTile;
+  static constexpr int kVOff = kKOff + kKS * kKStage;
+  static constexpr int kBarOff = kVOff + kVS * kVStage;
+  static constexpr int kSmem = kBarOff + 256 + 1024;
+};
+
+__host__ __device__ constexpr uint32_t idesc2(bool b_mn_major) {   // M = 256 (pair), N = 128
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) |
+         ((uint32_t)(256 >> 4) << 24);
+}
+__device__ __forceinline__ void mma2_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma2_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+// completion of the leader's MMAs so far -> the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          ptx::smem_u32(bar))
+      : "memory");
+}
+// TMA load into this CTA's shared memory whose bytes complete on the LEADER's barrier
+__device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(ptx::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAITC:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra.uni DONEC;\n"
+      "bra.uni LAB_WAITC;\n"
+      "DONEC:\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool VARLEN = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+prefill_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                    const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
+  constexpr int D = 128;
+  using L = PairL<D>;
+  constexpr int KS = L::kKS, VS = L::kVS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  // *_full / p_full / q_ready are used in the leader only; *_empty, s_full, o_final in both
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;            // [KS]
+  uint64_t* v_full = bars + 5;            // [VS]
+  uint64_t* k_empty = bars + 8;           // [KS]
+  uint64_t* v_empty = bars + 12;          // [VS]
+  uint64_t* s_full = bars + 15;           // [2]
+  uint64_t* p_full = bars + 17;           // [2]
+  uint64_t* o_final = bars + 19;          // [2]
+  uint64_t* q_ready = bars + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int witem = blockIdx.y;            // pair kernel: heads along x (cluster), work along y
+  int pair = p.n_pairs - 1 - witem;
+  int q_row0 = 0;
+  const CUtensorMap* kmp = &kmap;
+  const CUtensorMap* vmp = &vmap;
+  if constexpr (VARLEN) {
+    const int4 w = p.work[witem];
+    const int4 r = p.reqs[w.x];
+    pair = w.y;
+    q_row0 = r.x;
+    p.n_q = r.y;
+    p.kv_len = r.z;
+    p.q_off = r.z - r.y;
+    p.out += (int64_t)r.x * p.hq * D;
+    kmp = p.maps + 2 * w.x;
+    vmp = kmp + 1;
+  }
+  const int head = blockIdx.x;
+  const int kvh = head / p.group;          // both heads of the pair share it (group even)
+  const int q0A = pair * 2 * kBM, q0B = q0A + kBM;
+  const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
+  const int n_kv = max(nA, nB);
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < KS; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&s_full[x], 1);
+      ptx::mbar_init(&p_full[x], 2 * kBM);         // both CTAs' softmax threads of tile x
+      ptx::mbar_init(&o_final[x], 1);
+    }
+    ptx::mbar_init(q_ready, 2 * 2 * kBM);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  cluster_sync();                          // barriers of both CTAs initialised, TMEM allocated
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ===================== TMA producer (both CTAs: own Q, own halves of K and V) ============
+    if (lane == 0 && n_kv > 0) {
+      ptx::prefetch_tmap(&qmap);
+      ptx::prefetch_tmap(kmp);
+      ptx::prefetch_tmap(vmp);
+      if (leader) ptx::mbar_arrive_expect_tx(q_full, 2 * 2 * L::kTile);
+#pragma unroll
+      for (int h = 0; h < D / 64; ++h) {
+        tma2_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0A);
+        tma2_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0B);
+      }
+      constexpr int ahead = KS - VS;       // K runs ahead of V
+      for (int j = 0; j < n_kv + ahead; ++j) {
+        if (j < n_kv) {
+          const int s = j % KS;
+          if (j >= KS) ptx::mbar_wait(&k_empty[s], ((j / KS) - 1) & 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&k_full[s], 2 * L::kKStage);
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h)   // keys [64 rank, 64 rank + 64) of tile j, d-half h
+            tma2_load_3d(smem + L::kKOff + s * L::kKStage + h * L::kKHalf, kmp, &k_full[s], h * 64, kvh,
+                         j * kBN + 64 * (int)rank);
+        }
+        const int jv = j - ahead;
+        if (jv >= 0) {
+          const int s = jv % VS;
+          if (jv >= VS) ptx::mbar_wait(&v_empty[s], ((jv / VS) - 1) & 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&v_full[s], 2 * L::kVStage);
+          // all 128 keys of tile jv, head-dim columns [64 rank, 64 rank + 64)
+          tma2_load_3d(smem + L::kVOff + s * L::kVStage, vmp, &v_full[s], 64 * (int)rank, kvh, jv * kBN);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ===================== MMA issuer (leader, one thread, for both CTAs) =====================
+    if (leader && lane == 0 && n_kv > 0) {
+      const uint32_t id_qk = idesc2(false), id_pv = idesc2(true);
+      const uint32_t sbase = ptx::smem_u32(smem);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
+      const int nX[2] = {nA, nB};
+      auto issue_s = [&](int x, int j) {   // S_x(j) = Q_x K_j^T (M = 256: this tile of both heads)
+        const int s = j % KS;
+        const uint32_t qa = sbase + L::kQOff + x * L::kTile;
+        const uint32_t kb = sbase + L::kKOff + s * L::kKStage;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma2_ss(tS[x], sdesc(qa + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024),
+                  sdesc(kb + (kk >> 2) * L::kKHalf + (kk & 3) * 32, 16, 1024), id_qk, kk > 0);
+        commit2(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
+        const int s = j % VS;
+        const uint32_t vb = sbase + L::kVOff + s * L::kVStage;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma2_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
+      };
+      mbar_wait_cluster(q_full, 0);
+      if (p.rot_cos) mbar_wait_cluster(q_ready, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int sv = j % VS;
+        if (j == 0) {
+          mbar_wait_cluster(&k_full[0], 0);
+          fence_after();
+          for (int x = 0; x < 2; ++x)
+            if (nX[x] > 0) issue_s(x, 0);
+          commit2(&k_empty[0]);
+        }
+        mbar_wait_cluster(&v_full[sv], (j / VS) & 1);
+        fence_after();
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nX[x]) continue;
+          PF_TRACE(2 + x, j, 0);
+          {   // P_x(j) from both CTAs' softmax warps
+            const uint32_t a = ptx::smem_u32(&p_full[x]);
+            asm volatile(
+                "{\n.reg .pred p;\nLAB_WAITPP:\n"
+                "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+                "@p bra.uni DONEPP;\nbra.uni LAB_WAITPP;\nDONEPP:\n}\n" ::"r"(a), "r"((uint32_t)(j & 1))
+                : "memory");
+          }
+          PF_TRACE(2 + x, j, 1);
+          fence_after();
+          issue_pv(x, j);
+          PF_TRACE(2 + x, j, 2);
+          if (j + 1 == nX[x]) {
+            commit2(&o_final[x]);
+          } else {
+            const int s1 = (j + 1) % KS;
+            mbar_wait_cluster(&k_full[s1], ((j + 1) / KS) & 1);
+            fence_after();
+            issue_s(x, j + 1);
+            PF_TRACE(2 + x, j, 3);
+          }
+        }
+        commit2(&v_empty[sv]);
+        if (j + 1 < n_kv) commit2(&k_empty[(j + 1) % KS]);
+      }
+    }
+  } else {
+    softmax_role<0, D, VARLEN, true, L>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane, head,
+                                        q_row0, q0A, q0B, nA, nB, n_kv, omap);
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();                          // the peer's shared memory / TMEM stay live until both are done
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
 
 }  // namespace pf
 
@@ -783,6 +1073,21 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
     check_rt(cudaGetLastError(), "prefill launch");
+    return;
+  }
+  static int pair_mode = -1;
+  if (pair_mode < 0) {
+    const char* e = getenv("VATTN_PF_PAIR");   // 1: CTA-pair kernel (cta_group::2) where it applies
+    pair_mode = e ? (atoi(e) != 0) : 0;
+  }
+  if (pair_mode && !(rot && rot->cos) && p.group % 2 == 0 && hq % 2 == 0) {
+    // the pair kernel's K half-tiles: boxes of 64 keys
+    cuuint32_t kb2[3] = {64, 1, 64};
+    const CUtensorMap kmap2 = make_map(reinterpret_cast<void*>(v.k_base + slot_off), 3, kd, ks, kb2);
+    constexpr int kS2 = pf::PairL<128>::kSmem;
+    ensure_smem_attr<pf::prefill_pair_kernel<false>>(kS2);
+    pf::prefill_pair_kernel<false><<<dim3(hq, p.n_pairs), pf::kThreads, kS2, st>>>(qmap, kmap2, vmap, omap, p);
+    check_rt(cudaGetLastError(), "prefill (pair) launch");
     return;
   }
   static int poly = -1;
