@@ -157,7 +157,20 @@ struct DecodeParams {
   uint32_t* err;
   int32_t n_slots, slot_cap;
   Rotary rot;                   // rotary embedding of q and k_new (fused mode only)
+  // split-K combine inside the cluster of a unit's splits (launched with cluster dims
+  // (num_splits, 1, 1)): partials stay in shared memory and are merged over DSMEM, no
+  // workspace round trip and no combine launch
+  int32_t cluster_combine;
 };
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(ptx::smem_u32(p)), "r"(rank));
+  return a;
+}
 
 
 // ---- fused head all-gather epilogue (gather.cu owns the buffers and the wait) ----
@@ -353,6 +366,10 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
         }
       }
     }
+    if (p.cluster_combine) {   // the consumers' two cluster barriers (partials ready / read)
+      cluster_sync_all();
+      cluster_sync_all();
+    }
     return;
   }
 
@@ -539,6 +556,10 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
   }
   asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
   const int64_t par_off = (p.sink.n_ranks && p.num_splits == 1) ? sink_parity_off(p.sink) : 0;
+  // cluster combine: this split's normalised partial [group][D] and lse [group] behind the scratch
+  static_assert(CW * 16 * D * 4 + 16 * D * 4 + 16 * 4 <= STAGES * L::kStageBytes, "cluster staging fits");
+  float* stg_o = scratch + CW * 16 * D;
+  float* stg_lse = stg_o + 16 * D;
   // 8 consecutive output elements per thread-iteration: 16-byte stores (local or P2P)
   for (int i = threadIdx.x; i < p.group * (D / 8); i += CW * 32) {
     const int r = i / (D / 8), c = (i % (D / 8)) * 8;
@@ -566,6 +587,11 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
       pk.w = ptx::pack_bf16(acc[6] * inv, acc[7] * inv);
       if (p.sink.n_ranks) sink_store(p.sink, par_off, b, head, c, D, pk);
       else *reinterpret_cast<uint4*>(p.out + ((int64_t)b * p.hq + head) * D + c) = pk;
+    } else if (p.cluster_combine) {
+      float4* dst = reinterpret_cast<float4*>(stg_o + r * D + c);
+      dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+      if (c == 0) stg_lse[r] = lsum > 0.f ? M + log2f(lsum) : -INFINITY;
     } else {
       const int64_t row = ((int64_t)b * p.hq + head) * p.num_splits + split;
       float4* dst = reinterpret_cast<float4*>(p.part_o + row * D + c);
@@ -573,6 +599,48 @@ __global__ void __launch_bounds__(decode_threads(CW), CW == 4 ? 2 : 1) decode_ke
       dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
       if (c == 0) p.part_lse[row] = lsum > 0.f ? M + log2f(lsum) : -INFINITY;
     }
+  }
+  if (p.cluster_combine) {
+    // Every split of this (row, KV head) is a CTA of this cluster; CTA `split` merges chunks
+    // split, split + S, ... of the group's output over DSMEM, with the same arithmetic as
+    // decode_combine_kernel (one batch of <= 16 splits against their max, in split order).
+    cluster_sync_all();
+    const int S = p.num_splits;
+    for (int i = split * (CW * 32) + threadIdx.x; i < p.group * (D / 8); i += S * CW * 32) {
+      const int r = i / (D / 8), c = (i % (D / 8)) * 8;
+      float l[8];
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        l[q] = -INFINITY;
+        if (q < S) asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(l[q]) : "r"(dsmem_addr(stg_lse + r, q)));
+        M = fmaxf(M, l[q]);
+      }
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= S) break;
+          const float w = exp2f(l[q] - M);
+          if (w == 0.f) continue;   // an empty split holds no partial
+          float4 a, bb;
+          const uint32_t ra = dsmem_addr(stg_o + r * D + c, q);
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(ra));
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(bb.x), "=f"(bb.y), "=f"(bb.z), "=f"(bb.w) : "r"(ra + 16));
+          acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+          acc[4] += w * bb.x; acc[5] += w * bb.y; acc[6] += w * bb.z; acc[7] += w * bb.w;
+          wsum += w;
+        }
+      }
+      const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+      uint4 pk;
+      pk.x = ptx::pack_bf16(acc[0] * inv, acc[1] * inv);
+      pk.y = ptx::pack_bf16(acc[2] * inv, acc[3] * inv);
+      pk.z = ptx::pack_bf16(acc[4] * inv, acc[5] * inv);
+      pk.w = ptx::pack_bf16(acc[6] * inv, acc[7] * inv);
+      *reinterpret_cast<uint4*>(p.out + ((int64_t)b * p.hq + kvh * p.group + r) * D + c) = pk;
+    }
+    cluster_sync_all();        // no CTA leaves while another still reads its partial
   }
   if (p.sink.n_ranks && p.num_splits == 1)
     sink_signal(p.sink, gridDim.x * gridDim.y * gridDim.z, CW * 32);
@@ -779,21 +847,38 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
     const char* e = getenv("VATTN_DEC_PDL");
     return !e || atoi(e) != 0;
   }();
+  // splits of a unit as one cluster, combined over DSMEM (VATTN_DEC_CLUSTER=0 disables)
+  static const bool cl_env = [] {
+    const char* e = getenv("VATTN_DEC_CLUSTER");
+    return !e || atoi(e) != 0;
+  }();
+  p.cluster_combine = (cl_env && p.num_splits >= 2 && p.num_splits <= 8 && p.sink.n_ranks == 0) ? 1 : 0;
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.num_splits, hkv, batch);
     cfg.blockDim = dim3(decode_threads(CW));
     cfg.dynamicSmemBytes = L::kBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr.val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchAttribute attr[2]{};
+    int na = 0;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (p.cluster_combine) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = p.num_splits;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     check_rt(cudaLaunchKernelEx(&cfg, kern, km, vm, p), "decode launch");
   }
   check_rt(cudaGetLastError(), "decode launch");
-  if (p.num_splits > 1) {
+  if (p.num_splits > 1 && !p.cluster_combine) {
     const int rows = batch * p.hq;
     const int per_block = 128 / (D / 4);
     cudaLaunchConfig_t cfg{};
