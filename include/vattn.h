@@ -170,6 +170,10 @@ typedef struct vattn_iteration_result {
 /* ---- lifecycle --------------------------------------------------------------------- */
 const char* vattn_last_error(void);
 int32_t vattn_abi_version(void);
+/* sizeof of the ABI structs, for binding checks: out[0..7] = vattn_config, vattn_counters,
+ * vattn_step_result, vattn_bg_result, vattn_iteration_result, vattn_cache_desc, vattn_rotary,
+ * vattn_latency_entry; returns how many were written (min(n, 8)) */
+int32_t vattn_abi_sizes(int64_t* out, int32_t n);
 vattn_status vattn_create(const vattn_config* cfg, vattn_t** out);
 vattn_status vattn_destroy(vattn_t* h);
 

@@ -86,6 +86,7 @@ BG_EXECUTE_PLAN, BG_EAGER, BG_RECLAIM, BG_CREDIT, ITER_DEFER, BG_PREFETCH = 1, 2
 SIGNATURES = {
     "vattn_last_error": (C.c_char_p, []),
     "vattn_abi_version": (c_i32, []),
+    "vattn_abi_sizes": (c_i32, [C.POINTER(c_i64), c_i32]),
     "vattn_create": (c_i32, [C.POINTER(Config), C.POINTER(c_vp)]),
     "vattn_destroy": (c_i32, [c_vp]),
     "vattn_alloc_reqid": (c_i32, [c_vp, P_i32]),

@@ -1909,6 +1909,16 @@ extern "C" {
 const char* vattn_last_error(void) { return vattn::g_last_error.c_str(); }
 int32_t vattn_abi_version(void) { return 1; }
 
+int32_t vattn_abi_sizes(int64_t* out, int32_t n) {
+  const int64_t sz[8] = {(int64_t)sizeof(vattn_config),       (int64_t)sizeof(vattn_counters),
+                         (int64_t)sizeof(vattn_step_result),  (int64_t)sizeof(vattn_bg_result),
+                         (int64_t)sizeof(vattn_iteration_result), (int64_t)sizeof(vattn_cache_desc),
+                         (int64_t)sizeof(vattn_rotary),       (int64_t)sizeof(vattn_latency_entry)};
+  const int32_t k = n < 8 ? n : 8;
+  for (int32_t i = 0; i < k && out; ++i) out[i] = sz[i];
+  return k;
+}
+
 vattn_status vattn_create(const vattn_config* cfg, vattn_t** out) {
   return guard([&] {
     if (!cfg || !out) throw Fail(VATTN_VALUE_ERROR, "null argument");

@@ -52,3 +52,17 @@ def test_abi_version():
 
     assert lib().vattn_abi_version() == 1
     assert lib().vattn_api_count() == 12
+
+
+def test_struct_layouts_match_the_header():
+    """The ctypes binding's structs have the C ABI's sizes (vattn_abi_sizes), so a field added
+    to include/vattn.h without the binding (or vice versa) fails here, on CPU."""
+    import ctypes as C
+
+    from paper_2405_04437_b200 import _abi
+
+    out = (C.c_int64 * 8)()
+    assert _abi.lib().vattn_abi_sizes(out, 8) == 8
+    mine = [C.sizeof(t) for t in (_abi.Config, _abi.Counters, _abi.StepResultC, _abi.BgResult,
+                                   _abi.IterationResult, _abi.CacheDesc, _abi.RotaryC, _abi.LatencyEntry)]
+    assert list(out) == mine
