@@ -7,7 +7,7 @@ import torch
 from paper_2405_04437_b200.attention import prefill_attention_raw
 
 dev = torch.device("cuda")
-mode = os.environ.get("VATTN_PF_PAIR", "0")
+mode = "pair" if os.environ.get("VATTN_PF_PAIR", "0") == "1" else ("v3" if os.environ.get("VATTN_PF_V3", "0") == "1" else "single")
 for S, hq, hkv, kv in ((256, 32, 4, 256), (512, 8, 2, 600), (1000, 32, 8, 1000), (3000, 32, 4, 3100), (4096, 32, 8, 4096)):
     g = torch.Generator(device=dev).manual_seed(S)
     k = torch.randn(1, kv, hkv, 128, device=dev, dtype=torch.bfloat16, generator=g)
@@ -24,7 +24,7 @@ for S, hq, hkv, kv in ((256, 32, 4, 256), (512, 8, 2, 600), (1000, 32, 8, 1000),
     s.masked_fill_(mask, float("-inf"))
     ref = torch.matmul(torch.softmax(s, -1), vf).permute(1, 0, 2)
     err = ((out.float() - ref).abs().max() / ref.abs().max()).item()
-    print(f"PAIR={mode} S={S} hq={hq} hkv={hkv} kv={kv}: max-normalised err {err:.2e} {'OK' if err <= 2e-2 else 'FAIL'}", flush=True)
+    print(f"{mode} S={S} hq={hq} hkv={hkv} kv={kv}: max-normalised err {err:.2e} {'OK' if err <= 2e-2 else 'FAIL'}", flush=True)
 for S, hq, hkv in (() if "--parity-only" in sys.argv else ((16384, 32, 4), (4096, 32, 8), (65536, 32, 4))):
     k = torch.randn(1, S, hkv, 128, device=dev, dtype=torch.bfloat16)
     v = torch.randn(1, S, hkv, 128, device=dev, dtype=torch.bfloat16)
@@ -38,4 +38,4 @@ for S, hq, hkv in (() if "--parity-only" in sys.argv else ((16384, 32, 4), (4096
     for _ in range(n): prefill_attention_raw(q, k, v, 0, S, out=out)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
-    print(f"PAIR={mode} S={S}: {ms:.3f} ms {2.0 * S * S * 128 * hq / ms / 1e9:.0f} TFLOP/s", flush=True)
+    print(f"{mode} S={S}: {ms:.3f} ms {2.0 * S * S * 128 * hq / ms / 1e9:.0f} TFLOP/s", flush=True)
