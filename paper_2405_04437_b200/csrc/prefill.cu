@@ -153,37 +153,6 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])     \
       : "memory")
 
-// 16-lane shapes (two softmax warps per lane quarter, prefill_v3): 16x256b.x8 gives each thread
-// rows (l, l + 8) of the warp's 16-lane window, l = lane / 4, columns 8k + 2(lane % 4) + {0, 1}
-// for k = 0..7 as r[4k + {0,1}] (row l) and r[4k + {2,3}] (row l + 8); 16x128b.x8 stores one
-// 32-bit column 4k + lane % 4 of rows l / l + 8 from r[2k] / r[2k + 1].
-#define TMEM_LD16_32(taddr, r)                                                                         \
-  asm volatile(                                                                                        \
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                       \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),           \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),    \
-        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),    \
-        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                            \
-      : "r"(taddr))
-#define TMEM_ST16_32(taddr, r)                                                                          \
-  asm volatile(                                                                                         \
-      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),         \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),    \
-      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),  \
-      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) \
-      : "memory")
-#define TMEM_ST16P(taddr, r)                                                                            \
-  asm volatile(                                                                                         \
-      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"   \
-      "%15,%16};" ::"r"(taddr),                                                                         \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),          \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])     \
-      : "memory")
-
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -289,41 +258,6 @@ __device__ __forceinline__ void softmax_half(uint32_t tS, float2 sc2, float2 nm2
     }
   }
 }
-
-// prefill_v3: 64 columns [tS, tS + 64) of the thread's two rows (16 values each): P packed into
-// pk[16] in 16x128b order, raw-score maxima into m0 / m1, pairwise sums into a0 / a1.
-__device__ __forceinline__ void softmax_half16(uint32_t tS, float sc, float nm0, float nm1, uint32_t* pk,
-                                               float& m0, float& m1, float2& a0, float2& a1) {
-  uint32_t r[32];
-  TMEM_LD16_32(tS, r);
-  tmem_wait_ld();
-  const float2 sc2 = make_float2(sc, sc), n0 = make_float2(nm0, nm0), n1 = make_float2(nm1, nm1);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float s00 = __uint_as_float(r[4 * k]), s01 = __uint_as_float(r[4 * k + 1]);
-    const float s10 = __uint_as_float(r[4 * k + 2]), s11 = __uint_as_float(r[4 * k + 3]);
-    m0 = max3(m0, s00, s01);
-    m1 = max3(m1, s10, s11);
-    const float2 x0 = __ffma2_rn(make_float2(s00, s01), sc2, n0);
-    const float2 x1 = __ffma2_rn(make_float2(s10, s11), sc2, n1);
-    const float p00 = ptx::fast_exp2(x0.x), p01 = ptx::fast_exp2(x0.y);
-    const float p10 = ptx::fast_exp2(x1.x), p11 = ptx::fast_exp2(x1.y);
-    a0 = __fadd2_rn(a0, make_float2(p00, p01));
-    a1 = __fadd2_rn(a1, make_float2(p10, p11));
-    pk[2 * k] = ptx::pack_bf16(p00, p01);
-    pk[2 * k + 1] = ptx::pack_bf16(p10, p11);
-  }
-}
-
-__device__ __forceinline__ float quad_max(float v) {
-  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
-  return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
-}
-__device__ __forceinline__ float quad_sum(float v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  return v + __shfl_xor_sync(0xffffffffu, v, 2);
-}
-
 
 // number of KV tiles a query tile starting at row q0 needs
 __device__ __forceinline__ int kv_tiles_for(const Params& p, int q0) {
@@ -1073,400 +1007,6 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_const
 }
 
 
-// ===================== v3: one 128-row tile per CTA, S and P double-buffered =====================
-// The ping-pong kernel above aliases P on S, so S(j+1) of a tile waits for PV(j), and the
-// per-tile chain softmax -> PV -> S sets its period.  Here a CTA owns ONE query tile
-// and TMEM holds two S buffers, O and two P buffers (512 columns): S(j+2) is issued into S[j%2]
-// as soon as the softmax has stored P(j) (it no longer reads S[j%2]), so the tensor core computes
-// the next scores while the softmax works, and the softmax never waits for a PV.  Eight softmax
-// warps (two per TMEM lane quarter, 16-lane tcgen05.ld/st shapes) share the tile's rows so each
-// sub-partition runs two of them.  TMEM: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448)
-// P1 [448,512).  Warps 0-7 softmax, 8 TMA, 9 MMA issuer.
-struct V3L {
-  static constexpr int kKS = 3, kVS = 3;
-  static constexpr int kTile = 2 * kHalf;             // 128 rows x 128 d
-  static constexpr int kQOff = 0;
-  static constexpr int kKOff = kTile;
-  static constexpr int kVOff = kKOff + kKS * kTile;
-  static constexpr int kBarOff = kVOff + kVS * kTile;
-  static constexpr int kSmem = kBarOff + 256 + 1024;
-};
-
-template <bool VARLEN = false>
-__global__ void __launch_bounds__(kThreads, 1)
-prefill_v3_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-                  const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
-  constexpr int D = 128;
-  using L = V3L;
-  constexpr int KS = L::kKS, VS = L::kVS;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;            // [KS]
-  uint64_t* v_full = bars + 4;            // [VS]
-  uint64_t* k_empty = bars + 7;           // [KS]
-  uint64_t* v_empty = bars + 10;          // [VS]
-  uint64_t* s_full = bars + 13;           // [2] S buffer b holds S(j), j % 2 == b
-  uint64_t* p_full = bars + 15;           // [2] P buffer b holds P(j); S buffer b is free again
-  uint64_t* pv_done = bars + 17;          // [2] PV(j) from P buffer b retired (P[b] free, O current)
-  uint64_t* o_final = bars + 19;
-  uint64_t* q_ready = bars + 20;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int witem = p.head_fast ? blockIdx.y : blockIdx.x;
-  int blk = p.n_pairs - 1 - witem;         // n_pairs = number of 128-row tiles here; heaviest first
-  int q_row0 = 0;
-  const CUtensorMap* kmp = &kmap;
-  const CUtensorMap* vmp = &vmap;
-  if constexpr (VARLEN) {
-    const int4 w = p.work[witem];
-    const int4 r = p.reqs[w.x];
-    blk = w.y;
-    q_row0 = r.x;
-    p.n_q = r.y;
-    p.kv_len = r.z;
-    p.q_off = r.z - r.y;
-    p.out += (int64_t)r.x * p.hq * D;
-    kmp = p.maps + 2 * w.x;
-    vmp = kmp + 1;
-  }
-  const int head = p.head_fast ? blockIdx.x : blockIdx.y;
-  const int kvh = head / p.group;
-  const int q0 = blk * kBM;
-  const int n = kv_tiles_for(p, q0);
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
-    for (int s = 0; s < KS; ++s) {
-      ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < VS; ++s) {
-      ptx::mbar_init(&v_full[s], 1);
-      ptx::mbar_init(&v_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&s_full[b], 1);
-      ptx::mbar_init(&p_full[b], 8 * 32);
-      ptx::mbar_init(&pv_done[b], 1);
-    }
-    ptx::mbar_init(o_final, 1);
-    ptx::mbar_init(q_ready, 8 * 32);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     ptx::smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    // ===================== TMA producer =====================
-    if (lane == 0 && n > 0) {
-      ptx::prefetch_tmap(&qmap);
-      ptx::prefetch_tmap(kmp);
-      ptx::prefetch_tmap(vmp);
-      ptx::mbar_arrive_expect_tx(q_full, L::kTile);
-#pragma unroll
-      for (int h = 0; h < D / 64; ++h)
-        ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0);
-      // K runs ahead of V by one tile (S(j+2) is issued before PV(j+1) needs V(j+1))
-      for (int j = 0; j < n + 1; ++j) {
-        if (j < n) {
-          const int s = j % KS;
-          if (j >= KS) ptx::mbar_wait(&k_empty[s], ((j / KS) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&k_full[s], L::kTile);
-#pragma unroll
-          for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh, j * kBN);
-        }
-        const int jv = j - 1;
-        if (jv >= 0) {
-          const int s = jv % VS;
-          if (jv >= VS) ptx::mbar_wait(&v_empty[s], ((jv / VS) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
-#pragma unroll
-          for (int h = 0; h < D / 64; ++h)
-            ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh, jv * kBN);
-        }
-      }
-    }
-  } else if (warp == 9) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0 && n > 0) {
-      const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
-      const uint32_t sbase = ptx::smem_u32(smem);
-      const uint32_t tO = tmem + 256;
-      auto issue_s = [&](int j) {          // S[j % 2] = Q K_j^T
-        const int s = j % KS;
-        const uint32_t qa = sbase + L::kQOff;
-        const uint32_t kb = sbase + L::kKOff + s * L::kTile;
-        const uint32_t tS = tmem + 128 * (j & 1);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          mma_ss(tS, sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
-        }
-        mma_commit(&s_full[j & 1]);
-        mma_commit(&k_empty[s]);
-      };
-      ptx::mbar_wait(q_full, 0);
-      if (p.rot_cos) ptx::mbar_wait(q_ready, 0);
-      for (int j = 0; j < 2 && j < n; ++j) {
-        ptx::mbar_wait(&k_full[j % KS], (j / KS) & 1);
-        fence_after();
-        issue_s(j);
-      }
-      for (int j = 0; j < n; ++j) {
-        const int sv = j % VS;
-        ptx::mbar_wait(&v_full[sv], (j / VS) & 1);
-        PF_TRACE(2, j, 0);
-        ptx::mbar_wait_poll(&p_full[j & 1], (j >> 1) & 1);
-        PF_TRACE(2, j, 1);
-        fence_after();
-        const uint32_t tP = tmem + 384 + 64 * (j & 1);
-        const uint32_t vb = sbase + L::kVOff + sv * L::kTile;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          mma_ts(tO, tP + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&pv_done[j & 1]);
-        mma_commit(&v_empty[sv]);
-        PF_TRACE(2, j, 2);
-        if (j + 2 < n) {                  // S buffer j % 2 was released with P(j)
-          const int s2 = (j + 2) % KS;
-          ptx::mbar_wait(&k_full[s2], ((j + 2) / KS) & 1);
-          fence_after();
-          issue_s(j + 2);
-          PF_TRACE(2, j, 3);
-        }
-      }
-      mma_commit(o_final);
-    }
-  } else {
-    // ===================== softmax: 8 warps, 16 rows each =====================
-    const int lw = 32 * (warp % 4) + 16 * (warp / 4);        // first TMEM lane of the window
-    const int l = lane / 4, c4 = lane % 4;
-    const int row0 = lw + l, row1 = row0 + 8;
-    const int qp0 = q0 + row0, qp1 = q0 + row1;
-    const uint32_t lane_base = tmem + ((uint32_t)lw << 16);
-    const uint32_t tO = lane_base + 256;
-    const float sc = p.scale_log2;
-    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    if (p.rot_cos && n > 0) {
-      ptx::mbar_wait(q_full, 0);
-      const int li = warp * 32 + lane;           // warps 0-3 rotate one row each
-      const int qpos = q0 + li;
-      if (li < kBM && qpos < p.n_q) {
-        const uint32_t qt = ptx::smem_u32(smem + L::kQOff);
-        const int64_t t = (int64_t)(qpos + p.q_off) * (p.rot_dim / 2);
-        const int nch = p.rot_dim / 8, half = p.rot_dim / 16;
-        for (int cc = 0; cc < nch; ++cc) {
-          if (!p.rot_inter && cc >= half) break;
-          const int pc = p.rot_inter ? cc : cc + half;
-          const uint32_t a0 = ptx::swz128(qt + (cc >> 3) * kHalf, li, cc & 7);
-          const uint32_t a1 = ptx::swz128(qt + (pc >> 3) * kHalf, li, pc & 7);
-          uint4 v0, v1;
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(a0));
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(a1));
-          const uint4 r0 = ptx::rotary_chunk(v0, v1, cc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, p.rot_inter != 0);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(r0.x), "r"(r0.y), "r"(r0.z), "r"(r0.w));
-          if (!p.rot_inter) {
-            const uint4 r1 = ptx::rotary_chunk(v1, v0, pc, p.rot_cos + t, p.rot_sin + t, p.rot_dim, false);
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(r1.x), "r"(r1.y), "r"(r1.z), "r"(r1.w));
-          }
-        }
-      }
-      ptx::fence_proxy_async();
-      ptx::mbar_arrive(q_ready);
-    }
-    // O *= (f0 row l, f1 row l + 8); O must be current: PV(j-1) retired
-    auto rescale_o = [&](int j, float f0, float f1) {
-      if (j == 0) return;
-      ptx::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-      fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 64) {
-        uint32_t o[32];
-        TMEM_LD16_32(tO + c0, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          o[4 * k] = __float_as_uint(__uint_as_float(o[4 * k]) * f0);
-          o[4 * k + 1] = __float_as_uint(__uint_as_float(o[4 * k + 1]) * f0);
-          o[4 * k + 2] = __float_as_uint(__uint_as_float(o[4 * k + 2]) * f1);
-          o[4 * k + 3] = __float_as_uint(__uint_as_float(o[4 * k + 3]) * f1);
-        }
-        TMEM_ST16_32(tO + c0, o);
-      }
-    };
-    for (int j = 0; j < n; ++j) {
-      const int b = j & 1;
-      const uint32_t tS = lane_base + 128 * b;
-      const uint32_t tP = lane_base + 384 + 64 * b;
-      if (lane == 0 && warp == 0) PF_TRACE(0, j, 0);
-      ptx::mbar_wait(&s_full[b], (j >> 1) & 1);
-      if (lane == 0 && warp == 0) PF_TRACE(0, j, 1);
-      fence_after();
-      // P buffer b is free once PV(j-2) retired (it almost always has by now)
-      if (j >= 2) ptx::mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);
-      const int k0 = j * kBN;
-      const int key_end0 = p.causal ? min(p.kv_len, qp0 + p.q_off + 1) : p.kv_len;
-      const int key_end1 = p.causal ? min(p.kv_len, qp1 + p.q_off + 1) : p.kv_len;
-      const bool need_mask = (k0 + kBN > key_end0) || (k0 + kBN > key_end1);
-      const bool warp_mask = __any_sync(0xffffffffu, need_mask);
-      bool done = false;
-      if (!warp_mask && __all_sync(0xffffffffu, m0 != -INFINITY && m1 != -INFINITY)) {
-        float h0 = -INFINITY, h1 = -INFINITY;
-        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-        uint32_t pk[16];
-        softmax_half16(tS, sc, -m0, -m1, pk, h0, h1, a0, a1);
-        if (!__any_sync(0xffffffffu, h0 * sc > m0 + kRescaleThreshold || h1 * sc > m1 + kRescaleThreshold)) {
-          TMEM_ST16P(tP, pk);
-          float g0 = -INFINITY, g1 = -INFINITY;
-          float2 e0 = make_float2(0.f, 0.f), e1 = make_float2(0.f, 0.f);
-          softmax_half16(tS + 64, sc, -m0, -m1, pk, g0, g1, e0, e1);
-          if (!__any_sync(0xffffffffu, g0 * sc > m0 + kRescaleThreshold || g1 * sc > m1 + kRescaleThreshold)) {
-            TMEM_ST16P(tP + 32, pk);
-            l0 += (a0.x + a0.y) + (e0.x + e0.y);
-            l1 += (a1.x + a1.y) + (e1.x + e1.y);
-            done = true;
-          }
-          // else: rare, keys 64..127 raised the max: redo the tile two-pass (S is intact)
-        }
-      }
-      if (!done) {
-        // two-pass: row maxima (masked where needed) over the quad, lazy rescale, then P
-        const int lim0 = key_end0 - k0, lim1 = key_end1 - k0;
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t r[32];
-          TMEM_LD16_32(tS + 64 * h, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int c = 64 * h + 8 * k + 2 * c4;
-            const float s00 = __uint_as_float(r[4 * k]), s01 = __uint_as_float(r[4 * k + 1]);
-            const float s10 = __uint_as_float(r[4 * k + 2]), s11 = __uint_as_float(r[4 * k + 3]);
-            mx0 = fmaxf(mx0, fmaxf(c < lim0 ? s00 : -INFINITY, c + 1 < lim0 ? s01 : -INFINITY));
-            mx1 = fmaxf(mx1, fmaxf(c < lim1 ? s10 : -INFINITY, c + 1 < lim1 ? s11 : -INFINITY));
-          }
-        }
-        mx0 = quad_max(mx0) * sc;
-        mx1 = quad_max(mx1) * sc;
-        const bool grow0 = (m0 == -INFINITY) ? (mx0 > -INFINITY) : (mx0 > m0 + kRescaleThreshold);
-        const bool grow1 = (m1 == -INFINITY) ? (mx1 > -INFINITY) : (mx1 > m1 + kRescaleThreshold);
-        if (__any_sync(0xffffffffu, grow0 || grow1)) {
-          const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-          const float f0 = (m0 == -INFINITY) ? 0.f : ptx::fast_exp2(m0 - mn0);
-          const float f1 = (m1 == -INFINITY) ? 0.f : ptx::fast_exp2(m1 - mn1);
-          l0 *= f0;
-          l1 *= f1;
-          if (__any_sync(0xffffffffu, f0 != 1.f || f1 != 1.f)) rescale_o(j, f0, f1);
-          m0 = mn0;
-          m1 = mn1;
-        }
-        const float nm0 = m0 == -INFINITY ? 0.f : -m0, nm1 = m1 == -INFINITY ? 0.f : -m1;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t r[32], pk[16];
-          TMEM_LD16_32(tS + 64 * h, r);
-          tmem_wait_ld();
-          float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int c = 64 * h + 8 * k + 2 * c4;
-            const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1])),
-                                         make_float2(sc, sc), make_float2(nm0, nm0));
-            const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3])),
-                                         make_float2(sc, sc), make_float2(nm1, nm1));
-            float p00 = ptx::fast_exp2(x0.x), p01 = ptx::fast_exp2(x0.y);
-            float p10 = ptx::fast_exp2(x1.x), p11 = ptx::fast_exp2(x1.y);
-            if (warp_mask) {
-              p00 = c < lim0 ? p00 : 0.f;
-              p01 = c + 1 < lim0 ? p01 : 0.f;
-              p10 = c < lim1 ? p10 : 0.f;
-              p11 = c + 1 < lim1 ? p11 : 0.f;
-            }
-            a0 = __fadd2_rn(a0, make_float2(p00, p01));
-            a1 = __fadd2_rn(a1, make_float2(p10, p11));
-            pk[2 * k] = ptx::pack_bf16(p00, p01);
-            pk[2 * k + 1] = ptx::pack_bf16(p10, p11);
-          }
-          TMEM_ST16P(tP + 32 * h, pk);
-          l0 += a0.x + a0.y;
-          l1 += a1.x + a1.y;
-        }
-      }
-      tmem_wait_st();
-      fence_before();
-      ptx::mbar_arrive(&p_full[b]);
-      if (lane == 0 && warp == 0) PF_TRACE(0, j, 2);
-    }
-    // ---- epilogue: O / l -> bf16 -> global (via the Q buffer and a TMA store) ----
-    if (n > 0) {
-      ptx::mbar_wait(o_final, 0);
-      fence_after();
-    }
-    l0 = quad_sum(l0);
-    l1 = quad_sum(l1);
-    const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-    const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
-    const uint32_t qt = ptx::smem_u32(smem + L::kQOff);
-    __nv_bfloat16* dst0 = p.out + ((int64_t)qp0 * p.hq + head) * D;
-    __nv_bfloat16* dst1 = p.out + ((int64_t)qp1 * p.hq + head) * D;
-    const bool live0 = qp0 < p.n_q, live1 = qp1 < p.n_q;
-#pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 64) {
-      uint32_t o[32];
-      if (n > 0) {
-        TMEM_LD16_32(tO + c0, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) o[c] = 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int col = c0 + 8 * k + 2 * c4;
-        const uint32_t v0 = ptx::pack_bf16(__uint_as_float(o[4 * k]) * inv0, __uint_as_float(o[4 * k + 1]) * inv0);
-        const uint32_t v1 = ptx::pack_bf16(__uint_as_float(o[4 * k + 2]) * inv1, __uint_as_float(o[4 * k + 3]) * inv1);
-        if (via_tma) {
-          const int cc = col / 8;
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ptx::swz128(qt + (cc >> 3) * kHalf, row0, cc & 7) + 4 * c4), "r"(v0));
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ptx::swz128(qt + (cc >> 3) * kHalf, row1, cc & 7) + 4 * c4), "r"(v1));
-        } else {
-          if (live0) *reinterpret_cast<uint32_t*>(dst0 + col) = v0;
-          if (live1) *reinterpret_cast<uint32_t*>(dst1 + col) = v1;
-        }
-      }
-    }
-    if (via_tma) {
-      ptx::fence_proxy_async();
-      asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 softmax warps
-      if (warp == 0 && lane == 0) {
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          ptx::tma_store_3d(&omap, smem + L::kQOff + h * kHalf, h * 64, head, q_row0 + q0);
-        ptx::tma_store_commit();
-        ptx::tma_store_wait_read();
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
 }  // namespace pf
 
 static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
@@ -1534,21 +1074,6 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
     check_rt(cudaGetLastError(), "prefill launch");
-    return;
-  }
-  static int v3_mode = -1;
-  if (v3_mode < 0) {
-    const char* e = getenv("VATTN_PF_V3");     // 1: one tile per CTA, double-buffered S / P
-    v3_mode = e ? (atoi(e) != 0) : 0;
-  }
-  if (v3_mode) {
-    const int n_tiles = (n_q + pf::kBM - 1) / pf::kBM;
-    p.n_pairs = n_tiles;                        // the v3 grid counts 128-row tiles
-    const dim3 g3 = pf::pf_grid(p, n_tiles, hq);
-    constexpr int kS3 = pf::V3L::kSmem;
-    ensure_smem_attr<pf::prefill_v3_kernel<false>>(kS3);
-    pf::prefill_v3_kernel<false><<<g3, pf::kThreads, kS3, st>>>(qmap, kmap, vmap, omap, p);
-    check_rt(cudaGetLastError(), "prefill (v3) launch");
     return;
   }
   static int pair_mode = -1;
