@@ -204,7 +204,7 @@ class Manager {
   bool deferral_safe(const int64_t* seq, int32_t n, int64_t eager_k) const;
   void reset_credits() { std::fill(plan_credit_.begin(), plan_credit_.end(), 0); }
 
-  void mark_use(cudaStream_t st);
+  void mark_use(cudaStream_t st, bool explicit_mark = true);
   // Device-side read guard: rows each slot may be read at (backed page-groups), published to the
   // device for the decode / append kernels, which clamp to it and record a violation in a
   // host-mapped word instead of faulting the context; check_device_errors() raises it.
@@ -398,7 +398,10 @@ class Manager {
   // or trim must wait for decode on stream A and prefill on stream B alike).
   std::mutex use_mu_;
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> use_events_;
+  std::vector<char> use_dirty_;                     // launches on stream i since its last record
+  std::unordered_set<unsigned long long> open_captures_;   // captures with launches, no mark yet
   std::atomic<bool> use_recorded_{false};
+  cudaEvent_t use_event_locked(cudaStream_t st, size_t* idx);
   bool fenced_ = false;
   // read guard (publish_rows): device copy of every slot's readable rows, its pinned staging
   // buffer and host shadow, a private stream for the copy, and the host-mapped violation words
@@ -1079,11 +1082,30 @@ void Manager::fence_unmap() {
   if (fenced_) return;
   flush_access();
   if (use_recorded_) {
+    // Launches only flag their stream (a per-launch event record would sit between consecutive
+    // kernels and cancel their programmatic dependent launch); the record happens here, so it
+    // covers every kernel queued on the stream so far.  A graph captured without a closing
+    // mark_use may be replayed on any stream: then only a device-wide sync is safe.
     std::vector<cudaEvent_t> evs;
+    bool device_sync = false;
     {
       std::lock_guard<std::mutex> lk(use_mu_);
-      for (auto& se : use_events_) evs.push_back(se.second);
+      device_sync = !open_captures_.empty();
+      for (size_t i = 0; i < use_events_.size(); ++i) {
+        if (use_dirty_[i]) {
+          cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+          check_rt(cudaStreamIsCapturing(use_events_[i].first, &cs), "cudaStreamIsCapturing(fence)");
+          if (cs == cudaStreamCaptureStatusNone) {
+            check_rt(cudaEventRecord(use_events_[i].second, use_events_[i].first), "cudaEventRecord(fence)");
+            use_dirty_[i] = 0;
+          } else {
+            device_sync = true;      // its earlier eager work cannot be marked now
+          }
+        }
+        evs.push_back(use_events_[i].second);
+      }
     }
+    if (device_sync) check_rt(cudaDeviceSynchronize(), "cudaDeviceSynchronize(unmap fence)");
     for (cudaEvent_t e : evs) check_rt(cudaEventSynchronize(e), "cudaEventSynchronize(unmap fence)");
   }
   fenced_ = true;
@@ -1216,28 +1238,51 @@ void Manager::chunk_unref(int32_t b, int64_t off) {
   ch_cv_.notify_all();
 }
 
-void Manager::mark_use(cudaStream_t st) {
-  if (!real()) return;
-  // Inside a CUDA-graph capture a plain record only expresses a cross-stream dependency; an
-  // external record becomes a graph node, so every replay re-arms the unmap fence.
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  check_rt(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
-  std::lock_guard<std::mutex> lk(use_mu_);
+cudaEvent_t Manager::use_event_locked(cudaStream_t st, size_t* idx) {
+  for (size_t i = 0; i < use_events_.size(); ++i)
+    if (use_events_[i].first == st) {
+      *idx = i;
+      return use_events_[i].second;
+    }
   cudaEvent_t ev = nullptr;
-  for (auto& se : use_events_)
-    if (se.first == st) ev = se.second;
-  if (!ev) {
-    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;   // first use may be inside a capture
-    check_rt(cudaThreadExchangeStreamCaptureMode(&mode), "cudaThreadExchangeStreamCaptureMode");
-    const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaThreadExchangeStreamCaptureMode(&mode);
-    check_rt(e, "cudaEventCreate(use)");
-    use_events_.emplace_back(st, ev);
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;   // first use may be inside a capture
+  check_rt(cudaThreadExchangeStreamCaptureMode(&mode), "cudaThreadExchangeStreamCaptureMode");
+  const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  check_rt(e, "cudaEventCreate(use)");
+  use_events_.emplace_back(st, ev);
+  use_dirty_.push_back(0);
+  *idx = use_events_.size() - 1;
+  return ev;
+}
+
+// Unmap fence bookkeeping.  A kernel launch through the manager (explicit_mark = false) only flags
+// its stream, or, inside a graph capture, the capture; fence_unmap records the stream's event
+// when it needs it.  An explicit mark (vattn_mark_use) records now: inside a capture that is an
+// external event node (every replay re-arms the fence) and it covers the capture's launches so
+// far, so a captured region should end with one.
+void Manager::mark_use(cudaStream_t st, bool explicit_mark) {
+  if (!real()) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long cap_id = 0;
+  check_rt(cudaStreamGetCaptureInfo(st, &cs, &cap_id), "cudaStreamGetCaptureInfo");
+  const bool capturing = cs == cudaStreamCaptureStatusActive;
+  std::lock_guard<std::mutex> lk(use_mu_);
+  size_t i = 0;
+  cudaEvent_t ev = use_event_locked(st, &i);
+  if (!explicit_mark) {
+    if (capturing) open_captures_.insert(cap_id);
+    else use_dirty_[i] = 1;
+    use_recorded_ = true;
+    return;
   }
-  if (cs == cudaStreamCaptureStatusActive)
+  if (capturing) {
     check_rt(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal), "cudaEventRecord(use, graph)");
-  else
+    open_captures_.erase(cap_id);
+  } else {
     check_rt(cudaEventRecord(ev, st), "cudaEventRecord(use)");
+    use_dirty_[i] = 0;
+  }
   use_recorded_ = true;
 }
 
@@ -2085,7 +2130,7 @@ vattn_status vattn_check_errors(vattn_t* h) {
 
 vattn_status vattn_mark_use(vattn_t* h, void* stream) {
   if (!h || !h->m) { vattn::set_last_error("null handle"); return VATTN_BAD_STATE; }
-  return guard([&] { h->m->mark_use((cudaStream_t)stream); });
+  return guard([&] { h->m->mark_use((cudaStream_t)stream, true); });
 }
 
 vattn_status vattn_counters_get(vattn_t* h, vattn_counters* out) {
@@ -2174,7 +2219,7 @@ vattn_status vattn_kv_append(vattn_t* h, int32_t layer, const void* k_new, const
     const vattn::CacheView v = h->m->layer_view(layer);
     vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
                             (cudaStream_t)stream);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2195,7 +2240,7 @@ vattn_status vattn_decode(vattn_t* h, int32_t layer, const void* q, void* out, i
     decode_pdl_hint(h, (cudaStream_t)stream, layer, false);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2217,7 +2262,7 @@ vattn_status vattn_decode_append(vattn_t* h, int32_t layer, const void* q, const
     decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2233,7 +2278,7 @@ vattn_status vattn_kv_append_rotary(vattn_t* h, int32_t layer, const void* k_new
     const vattn::Rotary rot{rotary->cos, rotary->sin, rotary->rotary_dim, rotary->interleaved};
     vattn::launch_kv_append(h->m->ks, layer, v, k_new, v_new, batch, n_new, seqlens, batch_idx,
                             (cudaStream_t)stream, &rot);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2249,7 +2294,7 @@ vattn_status vattn_prefill_varlen(vattn_t* h, int32_t layer, const void* q, void
     for (int32_t i = 0; i < n_req; ++i) h->m->check_prefill_rows(slots[i], kv_len[i]);
     vattn::launch_prefill_varlen(v, q, out, h->m->hq_local(), n_req, q_start, n_q, slots, kv_len, scale,
                                  causal != 0, (cudaStream_t)stream);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2266,7 +2311,7 @@ vattn_status vattn_prefill_rotary(vattn_t* h, int32_t layer, const void* q, void
     h->m->check_prefill_rows(slot, kv_len);
     vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
                           causal != 0, (cudaStream_t)stream, &rot);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2290,7 +2335,7 @@ vattn_status vattn_decode_append_rotary(vattn_t* h, int32_t layer, const void* q
     decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, out, batch, hq, cache_seqlens, batch_idx, scale, num_splits,
                          ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, nullptr, &rot);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2313,7 +2358,7 @@ vattn_status vattn_decode_gather(vattn_t* h, int32_t layer, const void* q, const
     decode_pdl_hint(h, (cudaStream_t)stream, layer, k_new != nullptr);
     vattn::launch_decode(h->m->ks, layer, v, q, nullptr, batch, hq, cache_seqlens, batch_idx, scale,
                          num_splits, ws, ws_bytes, (cudaStream_t)stream, k_new, v_new, &s);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
@@ -2328,7 +2373,7 @@ vattn_status vattn_prefill(vattn_t* h, int32_t layer, const void* q, void* out, 
     h->m->check_prefill_rows(slot, kv_len);
     vattn::launch_prefill(h->m->ks, layer, v, q, out, n_q, h->m->hq_local(), slot, kv_len, scale,
                           causal != 0, (cudaStream_t)stream);
-    h->m->mark_use((cudaStream_t)stream);
+    h->m->mark_use((cudaStream_t)stream, false);
   });
 }
 
