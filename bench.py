@@ -282,7 +282,7 @@ def bench_decode(args, world, rank, local):
     hkv, hq, d = g.kv_heads_per_worker, g.q_heads_per_worker, g.head_dim
     steps, warm = args.steps, args.warmup
     # pool: every slot at ctx + all the steps this run takes (warm-up, timed, e2e), + slack
-    groups = math.ceil((ctx + steps + warm + 1 + max(3, min(steps, 20)) + 2) * g.per_token_layer_bytes / MB2)
+    groups = math.ceil((ctx + steps + warm + 1 + max(3, min(steps, 20)) + 4) * g.per_token_layer_bytes / MB2)
     pool = (groups * B + B // 8 + 1) * 2 * N * MB2   # every slot's groups + a little slack (fewer cuMemCreate at init)
     mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool, eager_groups=0,
                                           reclaim_threshold=0.0), backend="cuda", device=local)
@@ -464,17 +464,78 @@ def bench_decode(args, world, rank, local):
         one_step(None, q_d, kn_d, vn_d, out, pre_layer=pre_layer, post_layer=post_layer)
         stream.wait_stream(d2h_s)                       # the step ends when its outputs are on the host
 
-    e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    s0.record(stream)
-    for _ in range(e2e_steps):
+    if use_graph:
+        # Graph path: the copies are pipelined ACROSS steps instead of per layer (a per-layer
+        # event wait between two decode launches cancels their programmatic dependent launch):
+        # step i's q/k/v land in buffer set i % 2 while step i - 1 computes, and step i's outputs
+        # go to the host while step i + 1 computes.  Every step still moves its own inputs H2D
+        # and its outputs D2H inside the timed region.
+        qb, knb, vnb, ob = ([torch.empty_like(t) for _ in range(2)] for t in (q, kn, vn, out))
+        gr2 = []
+        for par in range(2):
+            g2 = torch.cuda.CUDAGraph()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(g2, stream=cap, capture_error_mode="thread_local"):
+                launch_layers(None, qb[par], knb[par], vnb[par], ob[par], torch.cuda.current_stream())
+                state["pos"].add_(1)
+                mgr.mark_use()
+            gr2.append(g2)
+        torch.cuda.synchronize()
+        in_ev = [torch.cuda.Event() for _ in range(2)]
+        comp_ev = [torch.cuda.Event() for _ in range(2)]
+        out_ev = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+
+        def h2d(par):
+            if used[par]:
+                h2d_s.wait_event(comp_ev[par])          # step i - 2 finished reading buffer set par
+            with torch.cuda.stream(h2d_s):
+                qb[par].copy_(qh, non_blocking=True)
+                knb[par].copy_(knh, non_blocking=True)
+                vnb[par].copy_(vnh, non_blocking=True)
+            in_ev[par].record(h2d_s)
+
+        def run_e2e(n_steps):
+            h2d(0)
+            for i in range(n_steps):
+                par = i % 2
+                if i + 1 < n_steps:
+                    h2d(1 - par)
+                stream.wait_event(in_ev[par])
+                if used[par]:
+                    stream.wait_event(out_ev[par])       # step i - 2's outputs left buffer par
+                one_step(None, graph=gr2[par])
+                comp_ev[par].record(stream)
+                used[par] = True
+                d2h_s.wait_event(comp_ev[par])
+                with torch.cuda.stream(d2h_s):
+                    outh.copy_(ob[par], non_blocking=True)
+                out_ev[par].record(d2h_s)
+            stream.wait_stream(d2h_s)
+
+        run_e2e(2)
+        torch.cuda.synchronize()
+        barrier()
+        used[0] = used[1] = False
+        s0.record(stream)
+        run_e2e(e2e_steps)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps)
+        e2e_pipeline = "inputs of step i+1 H2D and outputs of step i-1 D2H under step i's compute (graph replay per step)"
+    else:
         e2e_step()
-    s1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps)
-    h2d = qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2
-    d2h = outh.numel() * 2
+        torch.cuda.synchronize()
+        barrier()
+        s0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps)
+        e2e_pipeline = "per-layer H2D / D2H overlapping neighbouring layers (eager launches)"
+    h2d_bytes = qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2
+    d2h_bytes = outh.numel() * 2
     gather_cmp = head_gather_compare(mgr, q, out, pos, idx, splits, world, local) if world > 1 else None
     st = mgr.driver_stats()
     result = {
@@ -501,8 +562,8 @@ def bench_decode(args, world, rank, local):
                      "copy_peak_this_box_gbs": box_copy, "frac_of_this_box_copy_peak": achieved / box_copy,
                      "algorithmic_bytes": dec_bytes, "kernel": kernel_name,
                      "peak_source": pk["source"], "traffic_source": traffic_src},
-        "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms, "pipeline": e2e_pipeline},
         "clocks": clk,
         "gpu_launches": steps * N * ((2 if args.unfused and hg is None else 1) + (1 if splits > 1 else 0)
                                      + (1 if hg is not None else 0)),

@@ -919,7 +919,11 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
     const char* e = getenv("VATTN_DEC_CLUSTER");
     return !e || atoi(e) != 0;
   }();
-  p.cluster_combine = (cl_env && p.num_splits >= 2 && p.num_splits <= 8 && p.sink.n_ranks == 0) ? 1 : 0;
+  // clusters of up to 8 splits (portable size).  16-CTA non-portable clusters were measured much
+  // slower (B 1 x 32K, 16 splits: 49 vs 28 us with the combine kernel): the scheduler has to find
+  // 16 free SMs of one GPC for each cluster.
+  const bool cl = cl_env && p.num_splits >= 2 && p.num_splits <= 8 && p.sink.n_ranks == 0;
+  p.cluster_combine = cl ? 1 : 0;
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.num_splits, hkv, batch);

@@ -27,6 +27,6 @@ def test_cluster_combine_bit_identical_to_combine_kernel():
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     a, b = _run("1"), _run("0")
-    assert len(a) == 6 and a == b, (a, b)
+    assert len(a) == 8 and a == b, (a, b)
     for ln in a:
         assert float(ln.rsplit("err ", 1)[1]) <= 2e-2, ln

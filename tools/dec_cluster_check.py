@@ -8,7 +8,7 @@ from oracle.attention import decode_ref, max_rel_err
 from paper_2405_04437_b200.attention import decode_attention_raw, decode_attention_append_raw
 
 dev = torch.device("cuda")
-for B, hq, hkv, D, L, S in ((3, 32, 8, 128, 1000, 2), (2, 8, 2, 64, 3000, 3), (4, 32, 8, 128, 5000, 5),
+for B, hq, hkv, D, L, S in ((3, 32, 8, 128, 1000, 2), (2, 8, 2, 64, 3000, 3), (4, 32, 8, 128, 5000, 5), (1, 32, 8, 128, 32768, 16), (2, 32, 8, 128, 20000, 12),
                             (1, 32, 8, 128, 32768, 8), (64, 4, 1, 128, 4097, 2), (2, 56, 8, 128, 700, 8)):
     g = torch.Generator(device=dev).manual_seed(B * 1000 + S)
     kc = torch.randn(B, L + 8, hkv, D, device=dev, dtype=torch.bfloat16, generator=g)
