@@ -296,16 +296,11 @@ __device__ __forceinline__ void arrive_lead(uint64_t* bar) {
 // ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
 // One query row per thread (TMEM lane); used by the single-CTA kernel and by both CTAs of the
 // pair kernel (PAIR: P-ready / Q-ready arrivals go to the leader's barriers).
-// Persistent kernel (o_free != nullptr): the phases of s_full / o_final continue across work
-// items (s_base = tiles of this Q tile before this item, o_par = parity of this item's o_final),
-// O goes out with direct stores (the Q buffer already holds the next item's Q), and o_free is
-// arrived once O has been read out of TMEM so the next item's first PV may overwrite it.
 template <int POLY, int D, bool VARLEN, bool PAIR, class L>
 __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uint64_t* s_full, uint64_t* p_full,
                                              uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
                                              int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
-                                             int nB, int n_kv, const CUtensorMap& omap, uint32_t s_base = 0,
-                                             uint32_t o_par = 0, uint64_t* o_free = nullptr) {
+                                             int nB, int n_kv, const CUtensorMap& omap) {
   const int x = warp / 4;
   const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
   const int q0 = x == 0 ? q0A : q0B;
@@ -344,7 +339,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
   for (int j = 0; j < n; ++j) {
     if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
-    ptx::mbar_wait(&s_full[x], (s_base + j) & 1);
+    ptx::mbar_wait(&s_full[x], j & 1);
     if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 1);
     fence_after();
     // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
@@ -481,7 +476,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
   // ---- epilogue: O / l -> bf16 -> global ----
   if (n > 0) {
-    ptx::mbar_wait(&o_final[x], o_par & 1);
+    ptx::mbar_wait(&o_final[x], 0);
     fence_after();
   }
   const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -492,7 +487,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   // they cannot spill into the next request's rows.  A tile that sees no keys (n == 0) also
   // stores its zeros directly: it never waited for its Q load, which may still be landing in
   // that buffer (found under compute-sanitizer's slowed timing).
-  const bool via_tma = o_free == nullptr && n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
+  const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
   const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
   __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
   const bool live = qpos < p.n_q;
@@ -502,10 +497,6 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     if (n > 0) {
       TMEM_LD32(tO + c0, o);
       tmem_wait_ld();
-      if (o_free != nullptr && c0 + 32 == D) {   // all of O read: the next item may overwrite it
-        fence_before();
-        ptx::mbar_arrive(&o_free[x]);
-      }
     } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) o[c] = 0u;
@@ -772,217 +763,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 }
 
 
-
-// ===================== persistent variant: one CTA per SM walks the work list =====================
-// Same warp roles and pipeline as prefill_kernel, but a CTA keeps its TMEM, barriers and rings
-// across work items (256-row pairs of one head), so item i+1's Q load, first K/V tiles and first
-// S MMAs run under item i's epilogue instead of after a CTA exit and launch.  Items are taken in
-// the heaviest-first order of the non-persistent grid, dealt to the CTAs in snake order (round r:
-// CTA c gets item r*G + c, reversed on odd rounds), which balances the triangular causal work.
-// Ring indices and barrier phases run on across items; the Q buffer is released (q_empty) once
-// an item's last S MMA retired, and O (o_free) once its epilogue read O out of TMEM.
-__device__ __forceinline__ int persist_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
-
-__global__ void __launch_bounds__(kThreads, 1)
-prefill_persist_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-                       const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p,
-                       int n_items) {
-  constexpr int D = 128;
-  constexpr int KS = kKStages;
-  using L = PfL<D, KS>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;            // [KS]
-  uint64_t* v_full = bars + 5;            // [kStages]
-  uint64_t* k_empty = bars + 7;           // [KS]
-  uint64_t* v_empty = bars + 11;          // [kStages]
-  uint64_t* s_full = bars + 13;           // [2]
-  uint64_t* p_full = bars + 15;           // [2]
-  uint64_t* o_final = bars + 17;          // [2]
-  uint64_t* q_empty = bars + 19;
-  uint64_t* o_free = bars + 20;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c = blockIdx.x, G = gridDim.x;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(q_empty, 1);
-    for (int st = 0; st < KS; ++st) {
-      ptx::mbar_init(&k_full[st], 1);
-      ptx::mbar_init(&k_empty[st], 1);
-    }
-    for (int st = 0; st < kStages; ++st) {
-      ptx::mbar_init(&v_full[st], 1);
-      ptx::mbar_init(&v_empty[st], 1);
-    }
-    for (int x = 0; x < 2; ++x) {
-      ptx::mbar_init(&s_full[x], 1);
-      ptx::mbar_init(&p_full[x], kBM);
-      ptx::mbar_init(&o_final[x], 1);
-      ptx::mbar_init(&o_free[x], kBM);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     ptx::smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // item w -> (head, 256-row pair), heaviest first with heads varying fastest (head_fast order)
-  auto decode_item = [&](int w, int& head, int& q0A, int& nA, int& nB) {
-    head = w % p.hq;
-    const int pair = p.n_pairs - 1 - w / p.hq;
-    q0A = pair * 2 * kBM;
-    nA = kv_tiles_for(p, q0A);
-    nB = kv_tiles_for(p, q0A + kBM);
-  };
-
-  if (warp == 8) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      ptx::prefetch_tmap(&qmap);
-      ptx::prefetch_tmap(&kmap);
-      ptx::prefetch_tmap(&vmap);
-      int kt = 0, qi = 0;                  // K/V tiles and Q loads issued so far
-      constexpr int ahead = KS - kStages;
-      for (int r = 0;; ++r) {
-        const int w = persist_item(r, c, G);
-        if (w >= n_items) break;
-        int head, q0A, nA, nB;
-        decode_item(w, head, q0A, nA, nB);
-        const int n_kv = max(nA, nB);
-        const int kvh = head / p.group;
-        if (n_kv == 0) continue;
-        if (qi > 0) ptx::mbar_wait(q_empty, (qi - 1) & 1);
-        ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h) {
-          ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q0A);
-          ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q0A + kBM);
-        }
-        ++qi;
-        for (int j = 0; j < n_kv + ahead; ++j) {
-          if (j < n_kv) {
-            const int t = kt + j, st = t % KS;
-            if (t >= KS) ptx::mbar_wait(&k_empty[st], ((t / KS) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&k_full[st], L::kTile);
-#pragma unroll
-            for (int h = 0; h < D / 64; ++h)
-              ptx::tma_load_3d(smem + L::kKOff + st * L::kTile + h * kHalf, &kmap, &k_full[st], h * 64, kvh, j * kBN);
-          }
-          const int jv = j - ahead;
-          if (jv >= 0) {
-            const int t = kt + jv, st = t % kStages;
-            if (t >= kStages) ptx::mbar_wait(&v_empty[st], ((t / kStages) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&v_full[st], L::kTile);
-#pragma unroll
-            for (int h = 0; h < D / 64; ++h)
-              ptx::tma_load_3d(smem + L::kVOff + st * L::kTile + h * kHalf, &vmap, &v_full[st], h * 64, kvh, jv * kBN);
-          }
-        }
-        kt += n_kv;
-      }
-    }
-  } else if (warp == 9) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
-      const uint32_t sbase = ptx::smem_u32(smem);
-      const uint32_t tS[2] = {tmem + 0, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
-      int kt = 0, qi = 0;
-      uint32_t cntS[2] = {0, 0}, cntO[2] = {0, 0};   // tiles / items with tiles, per Q tile
-      for (int r = 0;; ++r) {
-        const int w = persist_item(r, c, G);
-        if (w >= n_items) break;
-        int head, q0A, nA, nB;
-        decode_item(w, head, q0A, nA, nB);
-        const int n_kv = max(nA, nB);
-        if (n_kv == 0) continue;
-        const int nX[2] = {nA, nB};
-        auto issue_s = [&](int x, int j) {
-          const int st = (kt + j) % KS;
-          const uint32_t qa = sbase + L::kQOff + x * L::kTile;
-          const uint32_t kb = sbase + L::kKOff + st * L::kTile;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-            mma_ss(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
-          }
-          mma_commit(&s_full[x]);
-        };
-        ptx::mbar_wait(q_full, qi & 1);
-        for (int j = 0; j < n_kv; ++j) {
-          const int t = kt + j, sv = t % kStages;
-          if (j == 0) {
-            ptx::mbar_wait(&k_full[t % KS], (t / KS) & 1);
-            fence_after();
-            for (int x = 0; x < 2; ++x)
-              if (nX[x] > 0) issue_s(x, 0);
-            mma_commit(&k_empty[t % KS]);
-          }
-          ptx::mbar_wait(&v_full[sv], (t / kStages) & 1);
-          fence_after();
-          for (int x = 0; x < 2; ++x) {
-            if (j >= nX[x]) continue;
-            ptx::mbar_wait_poll(&p_full[x], (cntS[x] + j) & 1);
-            if (j == 0 && cntO[x] > 0) ptx::mbar_wait(&o_free[x], (cntO[x] - 1) & 1);   // previous O read out
-            fence_after();
-            const uint32_t vb = sbase + L::kVOff + sv * L::kTile;
-#pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)
-              mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
-            if (j + 1 == nX[x]) {
-              mma_commit(&o_final[x]);
-            } else {
-              const int t1 = t + 1;
-              ptx::mbar_wait(&k_full[t1 % KS], (t1 / KS) & 1);
-              fence_after();
-              issue_s(x, j + 1);
-            }
-          }
-          mma_commit(&v_empty[sv]);
-          if (j + 1 < n_kv) mma_commit(&k_empty[(t + 1) % KS]);
-        }
-        mma_commit(q_empty);                 // Q no longer read once these MMAs retire
-        for (int x = 0; x < 2; ++x) {
-          cntS[x] += nX[x];
-          cntO[x] += nX[x] > 0 ? 1u : 0u;
-        }
-        kt += n_kv;
-        ++qi;
-      }
-    }
-  } else {
-    const int x = warp / 4;
-    uint32_t cntS = 0, cntO = 0;
-    for (int r = 0;; ++r) {
-      const int w = persist_item(r, c, G);
-      if (w >= n_items) break;
-      int head, q0A, nA, nB;
-      decode_item(w, head, q0A, nA, nB);
-      const int n_kv = max(nA, nB);
-      softmax_role<0, D, false, false, L>(p, smem, s_full, p_full, o_final, q_full, nullptr, tmem, warp, lane, head, 0,
-                                          q0A, q0A + kBM, nA, nB, n_kv, omap, cntS, cntO, o_free);
-      const int n = x == 0 ? nA : nB;
-      cntS += n;
-      cntO += n > 0 ? 1u : 0u;
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
 
 // ===================== CTA-pair kernel (tcgen05 cta_group::2) =====================
 // Two CTAs of a cluster = two query heads of one GQA group over the same 256 query rows.  The
@@ -1315,26 +1095,6 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
     check_rt(cudaGetLastError(), "prefill launch");
-    return;
-  }
-  static int persist_mode = -1;
-  if (persist_mode < 0) {
-    const char* e = getenv("VATTN_PF_PERSIST");   // 1: persistent CTAs walking the work list
-    persist_mode = e ? (atoi(e) != 0) : 0;
-  }
-  if (persist_mode && !(rot && rot->cos) && p.head_fast) {
-    const int n_items = p.n_pairs * hq;
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      check_rt(cudaGetDevice(&dev), "cudaGetDevice");
-      check_rt(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-    }
-    const int G = std::min(n_items, sms);
-    constexpr int kSP = pf::PfL<128>::kSmem;
-    ensure_smem_attr<pf::prefill_persist_kernel>(kSP);
-    pf::prefill_persist_kernel<<<G, pf::kThreads, kSP, st>>>(qmap, kmap, vmap, omap, p, n_items);
-    check_rt(cudaGetLastError(), "prefill (persistent) launch");
     return;
   }
   static int pair_mode = -1;

@@ -7,7 +7,7 @@ import torch
 from paper_2405_04437_b200.attention import prefill_attention_raw
 
 dev = torch.device("cuda")
-mode = "pair" if os.environ.get("VATTN_PF_PAIR", "0") == "1" else ("persist" if os.environ.get("VATTN_PF_PERSIST", "0") == "1" else "single")
+mode = "pair" if os.environ.get("VATTN_PF_PAIR", "0") == "1" else "single"
 for S, hq, hkv, kv in ((256, 32, 4, 256), (512, 8, 2, 600), (1000, 32, 8, 1000), (3000, 32, 4, 3100), (4096, 32, 8, 4096)):
     g = torch.Generator(device=dev).manual_seed(S)
     k = torch.randn(1, kv, hkv, 128, device=dev, dtype=torch.bfloat16, generator=g)
