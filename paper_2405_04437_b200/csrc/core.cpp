@@ -1113,8 +1113,11 @@ void Manager::fence_unmap() {
 
 void Manager::real_unmap(int32_t b, int64_t off) {
   if (chunked()) {
+    // the read guard shrinks now, so kernels still queued on the old row count must finish
+    // first even if the chunk stays mapped (found by test_gpu_unmap_fence [eager-4])
+    fence_unmap();
     shrink_rows(off);
-    chunk_unref(b, off);        // fences and unmaps only when the chunk's last group goes
+    chunk_unref(b, off);        // unmaps only when the chunk's last group goes
     return;
   }
   fence_unmap();

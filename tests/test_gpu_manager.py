@@ -193,8 +193,9 @@ def test_decode_through_manager_l8_shape_with_growth():
     mgr.close()
 
 
-@pytest.mark.parametrize("spec_slots,lazy", [(0, False), (2, False), (0, True), (2, True)])
-def test_physical_prefetch_keeps_logical_state_and_data(spec_slots, lazy):
+@pytest.mark.parametrize("spec_slots,lazy,chunk", [(0, False, 1), (2, False, 1), (0, True, 1), (2, True, 1),
+                                                   (2, True, 4), (0, False, 4)])
+def test_physical_prefetch_keeps_logical_state_and_data(spec_slots, lazy, chunk):
     """Prefetch (and speculative eager) maps pages ahead of the reference schedule; the logical
     state must equal the oracle's after every call and kernels must read/write the adopted pages
     correctly."""
@@ -209,7 +210,8 @@ def test_physical_prefetch_keeps_logical_state_and_data(spec_slots, lazy):
     g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=4, n_q_heads_total=32)
     pool = 24 * 4 * MB2
     mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=pool), prefetch_tokens=1500,
-                         prefetch_slots=spec_slots, prefetch_slot_tokens=1800, lazy_unmap=lazy)
+                         prefetch_slots=spec_slots, prefetch_slot_tokens=1800, lazy_unmap=lazy,
+                         phys_chunk_groups=chunk)
     om = OracleManager(Geometry(2, 8, 128, 2, 4096, 4), MB2, pool_bytes=pool)
     rng = random.Random(0)
     gen = torch.Generator().manual_seed(9)

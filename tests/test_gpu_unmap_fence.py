@@ -25,8 +25,9 @@ def _sleep(stream):
     check(lib().vattn_compute_proxy(SLEEP_NS, C.c_void_p(stream.cuda_stream)))
 
 
-@pytest.mark.parametrize("mode", ["eager", "graph_unmarked", "graph_marked_other_stream"])
-def test_reclaim_waits_for_queued_decode(mode):
+@pytest.mark.parametrize("mode,chunk", [("eager", 1), ("graph_unmarked", 1), ("graph_marked_other_stream", 1),
+                                        ("eager", 4), ("graph_marked_other_stream", 4)])
+def test_reclaim_waits_for_queued_decode(mode, chunk):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
@@ -34,7 +35,8 @@ def test_reclaim_waits_for_queued_decode(mode):
 
     dev = torch.device("cuda")
     g = ModelGeometry(1, 8, 128, 2, max_context=8192, max_batch=2, n_q_heads_total=32)
-    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, reclaim_threshold=0.0))
+    mgr = KVCacheManager(g, ManagerConfig(page_group_size=MB2, pool_bytes=64 * MB2, reclaim_threshold=0.0),
+                         phys_chunk_groups=chunk)
     try:
         r = mgr.alloc_reqid()
         lens = [0, 0]
