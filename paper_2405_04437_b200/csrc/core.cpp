@@ -1155,8 +1155,9 @@ void Manager::chunk_ref(int32_t b, int64_t off) {
   const Driver& d = driver();
   CUresult e = CUDA_SUCCESS;
   double t_create = 0, t_map = 0, t_acc = 0;
+  const bool fresh = h == 0;              // no recycled handle of this size: create one
   const double t0 = now_us();
-  if (!h) e = d.MemCreate(&h, (size_t)bytes, &prop_, 0);
+  if (fresh) e = d.MemCreate(&h, (size_t)bytes, &prop_, 0);
   const double t1 = now_us();
   const CUdeviceptr va = va_[b] + (CUdeviceptr)(c * chunk_ * t_);
   bool mapped = false;
@@ -1181,7 +1182,7 @@ void Manager::chunk_ref(int32_t b, int64_t off) {
     check_cu(e, "cuMemCreate/cuMemMap/cuMemSetAccess(chunk)");
   }
   ch.h = h;
-  if (t_create > 1e-3) {      // a fresh handle (free list was empty)
+  if (fresh) {
     real_create_us_ += t_create;
     real_creates_ += 1;
   }
