@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import math
 import os
 import statistics
@@ -180,7 +181,9 @@ def traffic_lookup(kernel: str, shape: str, algorithmic_bytes: float):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if not tf.exists():
         return None, "no profiles/ncu_traffic.json"
-    ent = json.loads(tf.read_text()).get(f"{kernel}|{shape}")
+    # the capture is of the decode kernel itself: drop the split-merge part of the label
+    kernel_key = re.sub(r" \(cluster combine\)| \+ decode_combine_kernel<\d+>", "", kernel)
+    ent = json.loads(tf.read_text()).get(f"{kernel_key}|{shape}")
     if not ent:
         return None, f"no ncu capture of {kernel} at {shape}"
     t = ent["traffic_bytes"]
@@ -565,7 +568,7 @@ def bench_decode(args, world, rank, local):
         "e2e": {"value": B / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms, "pipeline": e2e_pipeline},
         "clocks": clk,
-        "gpu_launches": steps * N * ((2 if args.unfused and hg is None else 1) + (1 if splits > 1 else 0)
+        "gpu_launches": steps * N * ((2 if args.unfused and hg is None else 1) + (1 if splits > 8 else 0)
                                      + (1 if hg is not None else 0)),
         "head_gather_mode": args.gather if world > 1 else "none (1 GPU)",
         "decode_kernel_mode": "unfused append+decode" if args.unfused else "fused append+decode (k=/v= semantics)",

@@ -1149,12 +1149,19 @@ int32_t vattn_decode_kernel_name(int32_t batch, int32_t hkv, int32_t max_seqlen,
     if (num_splits <= 0) num_splits = vattn::auto_splits(batch * hkv, max_seqlen);
     num_splits = std::min(num_splits, vattn::kMaxSplits);
     char tmp[96];
+    static const bool cl_env = [] {
+      const char* e = getenv("VATTN_DEC_CLUSTER");
+      return !e || atoi(e) != 0;
+    }();
+    // 2-8 splits merge inside their cluster (no combine kernel), more go through the combine kernel
+    const char* tail = num_splits <= 1 ? ""
+                       : (cl_env && num_splits <= 8) ? " (cluster combine)"
+                       : (head_dim == 128 ? " + decode_combine_kernel<128>" : " + decode_combine_kernel<64>");
     if (head_dim == 128) {
       const vattn::DecodeChoice ch = vattn::choose_decode(batch, hkv, num_splits);
-      snprintf(tmp, sizeof tmp, "decode_kernel<128,%d,false,%d>%s", ch.stages, ch.cw,
-               num_splits > 1 ? " + decode_combine_kernel<128>" : "");
+      snprintf(tmp, sizeof tmp, "decode_kernel<128,%d,false,%d>%s", ch.stages, ch.cw, tail);
     } else {
-      snprintf(tmp, sizeof tmp, "decode_kernel<64,6,false,4>%s", num_splits > 1 ? " + decode_combine_kernel<64>" : "");
+      snprintf(tmp, sizeof tmp, "decode_kernel<64,6,false,4>%s", tail);
     }
     if (buf && cap > 0) {
       strncpy(buf, tmp, (size_t)cap - 1);
