@@ -1094,7 +1094,13 @@ void Manager::fence_unmap() {
       for (size_t i = 0; i < use_events_.size(); ++i) {
         if (use_dirty_[i]) {
           cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-          check_rt(cudaStreamIsCapturing(use_events_[i].first, &cs), "cudaStreamIsCapturing(fence)");
+          if (cudaStreamIsCapturing(use_events_[i].first, &cs) != cudaSuccess) {
+            // the stream was destroyed after its launches (its work may still run): sync all
+            cudaGetLastError();
+            device_sync = true;
+            use_dirty_[i] = 0;
+            continue;
+          }
           if (cs == cudaStreamCaptureStatusNone) {
             check_rt(cudaEventRecord(use_events_[i].second, use_events_[i].first), "cudaEventRecord(fence)");
             use_dirty_[i] = 0;
