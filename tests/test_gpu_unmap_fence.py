@@ -26,7 +26,7 @@ def _sleep(stream):
 
 
 @pytest.mark.parametrize("mode,chunk", [("eager", 1), ("graph_unmarked", 1), ("graph_marked_other_stream", 1),
-                                        ("eager", 4), ("graph_marked_other_stream", 4)])
+                                        ("eager", 4), ("graph_marked_other_stream", 4), ("eager_dead_stream", 1)])
 def test_reclaim_waits_for_queued_decode(mode, chunk):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
@@ -55,6 +55,14 @@ def test_reclaim_waits_for_queued_decode(mode, chunk):
             s = torch.cuda.current_stream()
             _sleep(s)
             decode_attention(mgr, 0, q, seq, idx, out=out)
+        elif mode == "eager_dead_stream":     # launched on a stream that is gone before the fence
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                _sleep(s)
+                decode_attention(mgr, 0, q, seq, idx, out=out)
+            del s
+            import gc
+            gc.collect()
         else:
             cap = torch.cuda.Stream()
             cap.wait_stream(torch.cuda.current_stream())
