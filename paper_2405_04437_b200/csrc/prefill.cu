@@ -116,26 +116,6 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
-// converged-warp forms (every lane executes them, elect.sync picks the issuing lane): the MMA
-// stream is straight-line code with uniform operands instead of a per-MMA divergence loop
-__device__ __forceinline__ void mma_ss_e(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
-  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-                   ptx::smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    ptx::smem_u32(bar))
@@ -550,7 +530,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
 }
 
-template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false, bool WM = false>
+template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
@@ -701,17 +681,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     }
   } else if (warp == 9) {
     // ===================== MMA issuer (one thread) =====================
-    auto MMA_SS = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-      if constexpr (WM) mma_ss_e(d, a, b, id, acc); else mma_ss(d, a, b, id, acc);
-    };
-    auto MMA_TS = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
-      if constexpr (WM) mma_ts_e(d, a, b, id, acc); else mma_ts(d, a, b, id, acc);
-    };
-    auto COMMIT = [&](uint64_t* bar) {
-      if constexpr (WM) mma_commit_e(bar); else mma_commit(bar);
-    };
-    // WM: the whole warp runs the loop converged and sleeps in try_wait (suspend hint) on P
-    if ((WM || lane == 0) && n_kv > 0) {
+    if (lane == 0 && n_kv > 0) {
       const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
       const uint32_t sbase = ptx::smem_u32(smem);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
@@ -724,16 +694,16 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          MMA_SS(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
+          mma_ss(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
         }
-        COMMIT(&s_full[x]);
+        mma_commit(&s_full[x]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
         const int s = j % kStages;
         const uint32_t vb = sbase + L::kVOff + s * L::kTile;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
-          MMA_TS(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
       };
       ptx::mbar_wait(q_full, 0);
       if (p.rot_cos) ptx::mbar_wait(q_ready, 0);
@@ -744,7 +714,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
           fence_after();
           for (int x = 0; x < 2; ++x)
             if (nX[x] > 0) issue_s(x, 0);
-          if (SPLIT) COMMIT(&k_empty[0]);
+          if (SPLIT) mma_commit(&k_empty[0]);
         }
         ptx::mbar_wait(&v_full[s], (j / kStages) & 1);
         fence_after();
@@ -752,14 +722,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
           if (j >= nX[x]) continue;
           PF_TRACE(2 + x, j, 0);
           // polled without a suspend hint: the issuer wakes sooner (measured 1229 vs 1220 TF)
-          if constexpr (WM) ptx::mbar_wait(&p_full[x], j & 1);
-          else ptx::mbar_wait_poll(&p_full[x], j & 1);
+          ptx::mbar_wait_poll(&p_full[x], j & 1);
           PF_TRACE(2 + x, j, 1);
           fence_after();
           issue_pv(x, j);
           PF_TRACE(2 + x, j, 2);
           if (j + 1 == nX[x]) {
-            COMMIT(&o_final[x]);
+            mma_commit(&o_final[x]);
           } else {
             // S_x(j+1) needs K_{j+1}
             const int s1 = (j + 1) % KS;
@@ -770,10 +739,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
           }
         }
         if (SPLIT) {
-          COMMIT(&v_empty[s]);                               // V_j: its last PV was issued
-          if (j + 1 < n_kv) COMMIT(&k_empty[(j + 1) % KS]);  // K_{j+1}: both its S issued
+          mma_commit(&v_empty[s]);                               // V_j: its last PV was issued
+          if (j + 1 < n_kv) mma_commit(&k_empty[(j + 1) % KS]);  // K_{j+1}: both its S issued
         } else {
-          COMMIT(&k_empty[s]);   // K_j / V_j fully consumed once these MMAs retire
+          mma_commit(&k_empty[s]);   // K_j / V_j fully consumed once these MMAs retire
         }
       }
     }
@@ -1149,18 +1118,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
   }
   constexpr int kS = pf::PfL<128>::kSmem;
-  static int wm = -1;
-  if (wm < 0) {
-    const char* e = getenv("VATTN_PF_WM");   // converged-warp MMA issue (experiment)
-    wm = e ? (atoi(e) != 0) : 0;
-  }
-  if (wm && poly == 0) {
-    ensure_smem_attr<pf::prefill_kernel<0, false, 128, false, true>>(kS);
-    pf::prefill_kernel<0, false, 128, false, true><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
-  } else if (wm && poly == 1) {
-    ensure_smem_attr<pf::prefill_kernel<1, false, 128, false, true>>(kS);
-    pf::prefill_kernel<1, false, 128, false, true><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
-  } else if (poly == 0) {
+  if (poly == 0) {
     ensure_smem_attr<pf::prefill_kernel<0>>(kS);
     pf::prefill_kernel<0><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
   } else if (poly == 1) {
