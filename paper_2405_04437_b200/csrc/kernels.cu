@@ -1009,7 +1009,13 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   const int group = hq / hkv;
   if (group > 16) throw Fail(VATTN_UNSUPPORTED, "GQA group larger than 16");
   if (batch <= 0) return;
-  if (num_splits <= 0) num_splits = auto_splits(batch * hkv, max_len);
+  if (num_splits <= 0) {
+    static const int forced = [] {          // VATTN_DEC_SPLITS: fixed split count (experiments)
+      const char* e = getenv("VATTN_DEC_SPLITS");
+      return e ? atoi(e) : 0;
+    }();
+    num_splits = forced > 0 ? forced : auto_splits(batch * hkv, max_len);
+  }
   num_splits = std::min(num_splits, kMaxSplits);
   DecodeParams p{};
   p.q = reinterpret_cast<const __nv_bfloat16*>(q);
