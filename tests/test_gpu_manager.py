@@ -34,14 +34,15 @@ def test_cuda_backend_bookkeeping_matches_reference(fixture):
         a.close()
 
 
+@pytest.mark.parametrize("release", [False, True], ids=["recycle", "release"])
 @pytest.mark.parametrize("fixture", GPU_FIXTURES[::3], ids=[f["name"] for f in GPU_FIXTURES[::3]])
-def test_cuda_backend_chunked_bookkeeping_matches_reference(fixture):
+def test_cuda_backend_chunked_bookkeeping_matches_reference(fixture, release):
     """phys_chunk_groups=4: four consecutive 2 MiB groups of a buffer share one 8 MiB physical
     handle.  The logical state after every reference call is unchanged (bit-exact replay); the
     driver sees at most as many cuMemMap calls as the 2 MiB mode, and the mapped chunks cover
     every logically mapped group."""
     _cuda()
-    a = CoreAdapter(fixture, backend="cuda", phys_chunk_groups=4)
+    a = CoreAdapter(fixture, backend="cuda", phys_chunk_groups=4, release_physical=release)
     try:
         replay(fixture, a)
         st = a.m.driver_stats()
