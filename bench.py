@@ -977,6 +977,20 @@ def extra_long_decode(local, cases=((1, 32768), (1, 131072), (8, 32768), (8, 131
 
         us = _time_ms(contiguous, iters=8) * 1e3
         row = {"us": us, "gbs": byt / (us * 1e-6) / 1e9, "num_splits": decode_num_splits(B, hkv, L)}
+        # the same launches replayed from a CUDA graph (one call per cache copy): device time per
+        # call without the ~17 us host enqueue that paces the eager loop at small B
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cap, capture_error_mode="thread_local"):
+            for i in range(ncopy):
+                k, v = kv[i]
+                decode_attention_raw(q, k, v, seq)
+        gus = _time_ms(gr.replay, iters=8) * 1e3 / ncopy
+        del gr
+        row["us_graph"] = gus
+        row["gbs_graph"] = byt / (gus * 1e-6) / 1e9
         for bs in (16, 256):
             nb = L // bs
             perm = torch.randperm(B * nb, device=dev, generator=gen)
