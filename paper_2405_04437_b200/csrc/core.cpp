@@ -350,7 +350,7 @@ class Manager {
   };
   std::unordered_map<int64_t, Chunk> chunks_;                                        // ch_mu_
   std::unordered_map<int64_t, std::vector<CUmemGenericAllocationHandle>> ch_free_;  // by bytes
-  std::mutex ch_mu_;
+  mutable std::mutex ch_mu_;
   std::condition_variable ch_cv_;
   std::atomic<uint64_t> next_token_{0};
   int64_t ch_mapped_ = 0, ch_mapped_bytes_ = 0;
@@ -1768,8 +1768,14 @@ void Manager::counters(vattn_counters* o) const {
   o->spec_pages = (int64_t)spec_.size();
   o->lazy_unmaps = lazy_unmaps_;
   o->phys_chunk_groups = chunk_;
-  o->phys_chunks_mapped = ch_mapped_;
-  o->phys_mapped_bytes = chunked() ? ch_mapped_bytes_ : (real() ? (mapped_ + (int64_t)spec_.size()) * t_ : 0);
+  if (chunked()) {
+    std::lock_guard<std::mutex> lc(ch_mu_);   // lock order pf_mu_ -> ch_mu_, as in dev_precreate
+    o->phys_chunks_mapped = ch_mapped_;
+    o->phys_mapped_bytes = ch_mapped_bytes_;
+  } else {
+    o->phys_chunks_mapped = 0;
+    o->phys_mapped_bytes = real() ? (mapped_ + (int64_t)spec_.size()) * t_ : 0;
+  }
 }
 
 void Manager::slot_state(int64_t* out) const {
