@@ -66,3 +66,27 @@ def test_struct_layouts_match_the_header():
     mine = [C.sizeof(t) for t in (_abi.Config, _abi.Counters, _abi.StepResultC, _abi.BgResult,
                                    _abi.IterationResult, _abi.CacheDesc, _abi.RotaryC, _abi.LatencyEntry)]
     assert list(out) == mine
+
+
+def test_phys_chunk_groups_plumbing_on_the_shadow_backend():
+    """phys_chunk_groups reaches the core through the binding (counters echo it); the shadow
+    backend has no physical memory, so its logical state is the reference's either way."""
+    import pytest
+
+    from paper_2405_04437_b200 import KVCacheManager, ManagerConfig, ModelGeometry
+
+    g = ModelGeometry(2, 8, 128, 2, max_context=4096, max_batch=2)
+    states = []
+    for chunk in (1, 4):
+        m = KVCacheManager(g, ManagerConfig(page_group_size=2 << 20, pool_bytes=64 << 20), backend="shadow",
+                           phys_chunk_groups=chunk)
+        c = m._counters()
+        assert c.phys_chunk_groups == chunk and c.phys_mapped_bytes == 0
+        r = m.alloc_reqid()
+        assert m.step([3000 if i == r else 0 for i in range(2)]).ok
+        states.append(m.parity_state())
+        m.close()
+    assert states[0] == states[1]
+    with pytest.raises(ValueError):
+        KVCacheManager(g, ManagerConfig(page_group_size=2 << 20, pool_bytes=64 << 20), backend="shadow",
+                       phys_chunk_groups=0)
