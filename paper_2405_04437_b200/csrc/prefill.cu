@@ -116,26 +116,6 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
-// Lean issue forms for a converged MMA warp: one elected lane issues; the operands are the whole
-// warp's (identical) values, which the compiler can keep in uniform registers
-__device__ __forceinline__ void mma_ss_u(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_ts_u(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit_u(uint64_t* bar) {
-  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-                   ptx::smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    ptx::smem_u32(bar))
@@ -550,7 +530,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
 }
 
-template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false, bool LEAN = false>
+template <int POLY, bool PAGED = false, int D = 128, bool VARLEN = false>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap omap, Params p) {
@@ -697,69 +677,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                                &v_full[s], h * 64, kvh, within, blk);
           }
         }
-      }
-    }
-  } else if (LEAN && warp == 9) {
-    // ===================== MMA issuer, lean (whole warp converged) =====================
-    // TMEM base is column 0 (the CTA's only allocation takes all 512 columns; checked below), so
-    // the accumulator addresses are constants; descriptors are base + constant offsets.
-    if (n_kv > 0) {
-      if (tmem != 0) __trap();
-      const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
-      const uint32_t sbase = ptx::smem_u32(smem);
-      const uint64_t qd0 = sdesc(sbase + L::kQOff, 16, 1024);
-      const uint64_t kd0 = sdesc(sbase + L::kKOff, 16, 1024);
-      const uint64_t vd0 = sdesc(sbase + L::kVOff, kHalf, 1024);
-      const int nX[2] = {nA, nB};
-      auto issue_s = [&](int x, int j) {   // S_x(j) = Q_x K_j^T
-        const uint64_t qd = qd0 + (uint64_t)((x * L::kTile) >> 4);
-        const uint64_t kd = kd0 + (uint64_t)(((j % KS) * L::kTile) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * kHalf + (kk & 3) * 32) >> 4;
-          mma_ss_u(128u * x, qd + off, kd + off, id_qk, kk > 0);
-        }
-        mma_commit_u(&s_full[x]);
-      };
-      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
-        const uint64_t vd = vd0 + (uint64_t)(((j % kStages) * L::kTile) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          mma_ts_u(256u + D * x, 128u * x + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), id_pv,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-      };
-      ptx::mbar_wait(q_full, 0);
-      if (p.rot_cos) ptx::mbar_wait(q_ready, 0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int s = j % kStages;
-        if (j == 0) {
-          ptx::mbar_wait(&k_full[0], 0);
-          fence_after();
-          for (int x = 0; x < 2; ++x)
-            if (nX[x] > 0) issue_s(x, 0);
-          mma_commit_u(&k_empty[0]);
-        }
-        ptx::mbar_wait(&v_full[s], (j / kStages) & 1);
-        fence_after();
-        for (int x = 0; x < 2; ++x) {
-          if (j >= nX[x]) continue;
-          PF_TRACE(2 + x, j, 0);
-          ptx::mbar_wait(&p_full[x], j & 1);
-          PF_TRACE(2 + x, j, 1);
-          fence_after();
-          issue_pv(x, j);
-          PF_TRACE(2 + x, j, 2);
-          if (j + 1 == nX[x]) {
-            mma_commit_u(&o_final[x]);
-          } else {
-            ptx::mbar_wait(&k_full[(j + 1) % KS], ((j + 1) / KS) & 1);
-            fence_after();
-            issue_s(x, j + 1);
-            PF_TRACE(2 + x, j, 3);
-          }
-        }
-        mma_commit_u(&v_empty[s]);
-        if (j + 1 < n_kv) mma_commit_u(&k_empty[(j + 1) % KS]);
       }
     }
   } else if (warp == 9) {
@@ -1201,18 +1118,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     poly = e ? std::max(0, std::min(3, atoi(e))) : 0;
   }
   constexpr int kS = pf::PfL<128>::kSmem;
-  static int lean = -1;
-  if (lean < 0) {
-    const char* e = getenv("VATTN_PF_LEAN");   // lean converged MMA issue (experiment)
-    lean = e ? (atoi(e) != 0) : 0;
-  }
-  if (lean && poly <= 2) {
-#define PF_LEAN(PO)                                                                                \
-  ensure_smem_attr<pf::prefill_kernel<PO, false, 128, false, true>>(kS);                           \
-  pf::prefill_kernel<PO, false, 128, false, true><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
-    if (poly == 0) { PF_LEAN(0) } else if (poly == 1) { PF_LEAN(1) } else { PF_LEAN(2) }
-#undef PF_LEAN
-  } else if (poly == 0) {
+  if (poly == 0) {
     ensure_smem_attr<pf::prefill_kernel<0>>(kS);
     pf::prefill_kernel<0><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
   } else if (poly == 1) {
