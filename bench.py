@@ -539,7 +539,12 @@ def bench_decode(args, world, rank, local):
         e2e_pipeline = "per-layer H2D / D2H overlapping neighbouring layers (eager launches)"
     h2d_bytes = qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2
     d2h_bytes = outh.numel() * 2
-    gather_cmp = head_gather_compare(mgr, q, out, pos, idx, splits, world, local) if world > 1 else None
+    gather_cmp = None
+    if world > 1:
+        try:   # a diagnostic: it must not void the headline line
+            gather_cmp = head_gather_compare(mgr, q, out, pos, idx, splits, world, local)
+        except Exception as e:
+            gather_cmp = {"error": repr(e)[:300]}
     st = mgr.driver_stats()
     result = {
         "metric": "decode_attn_tokens_per_s",
