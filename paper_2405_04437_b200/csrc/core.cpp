@@ -1229,7 +1229,6 @@ void Manager::chunk_unref(int32_t b, int64_t off) {
     ch_cv_.notify_all();
     throw;
   }
-  if (e == CUDA_SUCCESS && release_physical_) e = driver().MemRelease(h);
   lk.lock();
   ch.busy = false;
   if (e != CUDA_SUCCESS) {
@@ -1239,13 +1238,22 @@ void Manager::chunk_unref(int32_t b, int64_t off) {
     check_cu(e, "cuMemUnmap(chunk)");
   }
   ch.h = 0;
-  if (!release_physical_) ch_free_[bytes].push_back(h);
-  else real_releases_ += 1;
+  CUresult er = CUDA_SUCCESS;
+  if (!release_physical_) {
+    ch_free_[bytes].push_back(h);
+  } else {
+    er = driver().MemRelease(h);   // unmapped either way; a failed release only leaks the handle
+    if (er == CUDA_SUCCESS) real_releases_ += 1;
+  }
   real_unmap_us_ += t_unmap;
   real_unmaps_ += 1;
   ch_mapped_ -= 1;
   ch_mapped_bytes_ -= bytes;
   ch_cv_.notify_all();
+  if (er != CUDA_SUCCESS) {
+    lk.unlock();
+    check_cu(er, "cuMemRelease(chunk)");
+  }
 }
 
 cudaEvent_t Manager::use_event_locked(cudaStream_t st, size_t* idx) {
