@@ -218,7 +218,7 @@ __device__ __forceinline__ float2 softmax_p_pass(uint32_t tS, float2 sc2, float2
 
 #ifdef VATTN_PF_TRACE
 // debug timeline of CTA (0, 0): [role][j][event] clock64 stamps (build with -DVATTN_PF_TRACE)
-__device__ unsigned long long g_pf_trace[4][160][4];
+__device__ unsigned long long g_pf_trace[4][160][8];
 // per-CTA record of the last traced launch: [globaltimer start, end, smid, kv tiles]
 __device__ unsigned long long g_pf_cta[8192][4];
 __device__ __forceinline__ unsigned long long pf_gtime() {
