@@ -220,7 +220,9 @@ __device__ __forceinline__ float2 softmax_p_pass(uint32_t tS, float2 sc2, float2
 // debug timeline of CTA (0, 0): [role][j][event] clock64 stamps (build with -DVATTN_PF_TRACE)
 __device__ unsigned long long g_pf_trace[4][160][8];
 // per-CTA record of the last traced launch: [globaltimer start, end, smid, kv tiles]
-__device__ unsigned long long g_pf_cta[8192][4];
+// [0] start (work item known), [1] end of work, [2] smid, [3] kv tiles, [4] kernel entry,
+// [5] prologue done (barriers, TMEM), [6] TMEM released (exit)
+__device__ unsigned long long g_pf_cta[8192][12];
 __device__ __forceinline__ unsigned long long pf_gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -553,6 +555,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#ifdef VATTN_PF_TRACE
+  if (threadIdx.x == 0 && blockIdx.y * gridDim.x + blockIdx.x < 8192)
+    g_pf_cta[blockIdx.y * gridDim.x + blockIdx.x][4] = pf_gtime();
+#endif
   const int witem = p.head_fast ? blockIdx.y : blockIdx.x;
   int pair = p.n_pairs - 1 - witem;        // heaviest (latest) query rows first
   int q_row0 = 0;                          // packed row of this request's query row 0
@@ -613,6 +619,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef VATTN_PF_TRACE
+  if (threadIdx.x == 0 && cta_lin < 8192) g_pf_cta[cta_lin][5] = pf_gtime();
+#endif
 
   if (warp == 8) {
     // ===================== TMA producer =====================
@@ -755,10 +764,23 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   if (threadIdx.x == 0 && cta_lin < 8192) g_pf_cta[cta_lin][1] = pf_gtime();
 #endif
   fence_before();
+#ifdef VATTN_PF_TRACE
+  if (threadIdx.x == 0 && cta_lin < 8192) g_pf_cta[cta_lin][8] = pf_gtime();
+  if (threadIdx.x == 32 * 9 && cta_lin < 8192) g_pf_cta[cta_lin][10] = pf_gtime();
+#endif
   __syncthreads();
+#ifdef VATTN_PF_TRACE
+  if (threadIdx.x == 0 && cta_lin < 8192) g_pf_cta[cta_lin][9] = pf_gtime();
+#endif
   if (warp == 9) {
+#ifdef VATTN_PF_TRACE
+    if (lane == 0 && cta_lin < 8192) g_pf_cta[cta_lin][7] = pf_gtime();
+#endif
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+#ifdef VATTN_PF_TRACE
+    if (lane == 0 && cta_lin < 8192) g_pf_cta[cta_lin][6] = pf_gtime();
+#endif
   }
 }
 

@@ -15,7 +15,7 @@ for S, hq, hkv in ((16384, 32, 4), (4096, 32, 8)):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); prefill_attention_raw(q, k, v, 0, S); e1.record(); torch.cuda.synchronize()
-    buf = np.zeros((8192, 4), dtype=np.uint64)
+    buf = np.zeros((8192, 12), dtype=np.uint64)
     raw.vattn_debug_prefill_cta(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)))
     n = hq * ((S + 255) // 256)
     b = buf[:n].astype(np.int64)
