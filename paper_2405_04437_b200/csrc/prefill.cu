@@ -298,11 +298,16 @@ __device__ __forceinline__ void arrive_lead(uint64_t* bar) {
 // ===================== softmax warpgroups (A: warps 0-3, B: warps 4-7) =====================
 // One query row per thread (TMEM lane); used by the single-CTA kernel and by both CTAs of the
 // pair kernel (PAIR: P-ready / Q-ready arrivals go to the leader's barriers).
+// Persistent kernel (o_free != nullptr): s_full / o_final phases continue across work items
+// (s_base = tiles this Q tile ran before this item, o_par = items with tiles before it), O goes
+// out with direct stores (the Q buffer may already hold the next item's Q), and o_free is
+// arrived once O has been read out of TMEM so the next item's first PV may overwrite it.
 template <int POLY, int D, bool VARLEN, bool PAIR, class L>
 __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uint64_t* s_full, uint64_t* p_full,
                                              uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
                                              int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
-                                             int nB, int n_kv, const CUtensorMap& omap) {
+                                             int nB, int n_kv, const CUtensorMap& omap, uint32_t s_base = 0,
+                                             uint32_t o_par = 0, uint64_t* o_free = nullptr) {
   const int x = warp / 4;
   const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
   const int q0 = x == 0 ? q0A : q0B;
@@ -341,7 +346,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
   for (int j = 0; j < n; ++j) {
     if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 0);
-    ptx::mbar_wait(&s_full[x], j & 1);
+    ptx::mbar_wait(&s_full[x], (s_base + j) & 1);
     if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 1);
     fence_after();
     // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
@@ -478,7 +483,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   }
   // ---- epilogue: O / l -> bf16 -> global ----
   if (n > 0) {
-    ptx::mbar_wait(&o_final[x], 0);
+    ptx::mbar_wait(&o_final[x], o_par & 1);
     fence_after();
   }
   const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -489,7 +494,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   // they cannot spill into the next request's rows.  A tile that sees no keys (n == 0) also
   // stores its zeros directly: it never waited for its Q load, which may still be landing in
   // that buffer (found under compute-sanitizer's slowed timing).
-  const bool via_tma = n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
+  const bool via_tma = o_free == nullptr && n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
   const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
   __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
   const bool live = qpos < p.n_q;
@@ -499,6 +504,10 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     if (n > 0) {
       TMEM_LD32(tO + c0, o);
       tmem_wait_ld();
+      if (o_free != nullptr && c0 + 32 == D) {   // all of O read: the next item may overwrite it
+        fence_before();
+        ptx::mbar_arrive(&o_free[x]);
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) o[c] = 0u;
@@ -781,6 +790,235 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #ifdef VATTN_PF_TRACE
     if (lane == 0 && cta_lin < 8192) g_pf_cta[cta_lin][6] = pf_gtime();
 #endif
+  }
+}
+
+
+
+// ===================== persistent varlen kernel: one CTA per SM walks the work list =============
+// Short prompts give CTAs of 1-4 KV tiles, where a CTA's fixed costs (launch, barrier / TMEM
+// setup, two dependent loads for its work item, the Q and first K/V latencies, the epilogue)
+// rival its work (tools/prefill_cta_timeline_varlen.py).  Here a CTA keeps TMEM,
+// barriers and the K / V rings across items (head, request, 256-row pair): item i+1's Q load,
+// first K / V tiles and first S MMAs run under item i's softmax tail and epilogue.  Items are
+// the normal grid's (head-fastest, heaviest-first) order dealt to the CTAs in snake order.  Ring
+// indices and barrier phases run on across items; Q is released (q_empty) once an item's last S
+// MMA retired and O (o_free) once the epilogue read it out of TMEM.  D = 128, no rotary.
+__device__ __forceinline__ int persist_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
+
+struct VarItem {
+  int head, q_row0, q0A, nA, nB;
+  const CUtensorMap* kmp;
+  Params p;      // the launch's Params with this item's request fields (n_q, kv_len, q_off, out)
+};
+
+__device__ __forceinline__ VarItem varlen_item(const Params& p, int w) {
+  VarItem it;
+  const int4 wk = p.work[w / p.hq];
+  const int4 rq = p.reqs[wk.x];
+  it.head = w % p.hq;
+  it.q_row0 = rq.x;
+  it.p = p;
+  it.p.n_q = rq.y;
+  it.p.kv_len = rq.z;
+  it.p.q_off = rq.z - rq.y;
+  it.p.out = p.out + (int64_t)rq.x * p.hq * 128;
+  it.q0A = wk.y * 2 * kBM;
+  it.nA = kv_tiles_for(it.p, it.q0A);
+  it.nB = kv_tiles_for(it.p, it.q0A + kBM);
+  it.kmp = p.maps + 2 * wk.x;
+  return it;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_persist_varlen_kernel(const __grid_constant__ CUtensorMap qmap, Params p, int n_items) {
+  constexpr int D = 128;
+  constexpr int KS = kKStages;
+  using L = PfL<D, KS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;            // [KS]
+  uint64_t* v_full = bars + 5;            // [kStages]
+  uint64_t* k_empty = bars + 7;           // [KS]
+  uint64_t* v_empty = bars + 11;          // [kStages]
+  uint64_t* s_full = bars + 13;           // [2]
+  uint64_t* p_full = bars + 15;           // [2]
+  uint64_t* o_final = bars + 17;          // [2]
+  uint64_t* q_empty = bars + 19;
+  uint64_t* o_free = bars + 20;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c = blockIdx.x, G = gridDim.x;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int st = 0; st < KS; ++st) {
+      ptx::mbar_init(&k_full[st], 1);
+      ptx::mbar_init(&k_empty[st], 1);
+    }
+    for (int st = 0; st < kStages; ++st) {
+      ptx::mbar_init(&v_full[st], 1);
+      ptx::mbar_init(&v_empty[st], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&s_full[x], 1);
+      ptx::mbar_init(&p_full[x], kBM);
+      ptx::mbar_init(&o_final[x], 1);
+      ptx::mbar_init(&o_free[x], kBM);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      ptx::prefetch_tmap(&qmap);
+      int kt = 0, qi = 0;                  // K/V tiles and Q loads issued so far
+      constexpr int ahead = KS - kStages;
+      for (int r = 0;; ++r) {
+        const int w = persist_item(r, c, G);
+        if (w >= n_items) break;
+        const VarItem it = varlen_item(p, w);
+        const int n_kv = max(it.nA, it.nB);
+        if (n_kv == 0) continue;
+        const int kvh = it.head / p.group;
+        const CUtensorMap* kmp = it.kmp;
+        const CUtensorMap* vmp = it.kmp + 1;
+        ptx::prefetch_tmap(kmp);
+        ptx::prefetch_tmap(vmp);
+        if (qi > 0) ptx::mbar_wait(q_empty, (qi - 1) & 1);
+        ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) {
+          ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, it.head, it.q_row0 + it.q0A);
+          ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, it.head,
+                           it.q_row0 + it.q0A + kBM);
+        }
+        ++qi;
+        for (int j = 0; j < n_kv + ahead; ++j) {
+          if (j < n_kv) {
+            const int t = kt + j, st = t % KS;
+            if (t >= KS) ptx::mbar_wait(&k_empty[st], ((t / KS) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&k_full[st], L::kTile);
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_3d(smem + L::kKOff + st * L::kTile + h * kHalf, kmp, &k_full[st], h * 64, kvh, j * kBN);
+          }
+          const int jv = j - ahead;
+          if (jv >= 0) {
+            const int t = kt + jv, st = t % kStages;
+            if (t >= kStages) ptx::mbar_wait(&v_empty[st], ((t / kStages) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&v_full[st], L::kTile);
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              ptx::tma_load_3d(smem + L::kVOff + st * L::kTile + h * kHalf, vmp, &v_full[st], h * 64, kvh, jv * kBN);
+          }
+        }
+        kt += n_kv;
+      }
+    }
+  } else if (warp == 9) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      const uint32_t id_qk = idesc(false), id_pv = idesc(true, D);
+      const uint32_t sbase = ptx::smem_u32(smem);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
+      int kt = 0, qi = 0;
+      uint32_t cntS[2] = {0, 0}, cntO[2] = {0, 0};   // tiles / items with tiles, per Q tile
+      for (int r = 0;; ++r) {
+        const int w = persist_item(r, c, G);
+        if (w >= n_items) break;
+        const VarItem it = varlen_item(p, w);
+        const int n_kv = max(it.nA, it.nB);
+        if (n_kv == 0) continue;
+        const int nX[2] = {it.nA, it.nB};
+        auto issue_s = [&](int x, int j) {
+          const int st = (kt + j) % KS;
+          const uint32_t qa = sbase + L::kQOff + x * L::kTile;
+          const uint32_t kb = sbase + L::kKOff + st * L::kTile;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+            mma_ss(tS[x], sdesc(qa + off, 16, 1024), sdesc(kb + off, 16, 1024), id_qk, kk > 0);
+          }
+          mma_commit(&s_full[x]);
+        };
+        ptx::mbar_wait(q_full, qi & 1);
+        for (int j = 0; j < n_kv; ++j) {
+          const int t = kt + j, sv = t % kStages;
+          if (j == 0) {
+            ptx::mbar_wait(&k_full[t % KS], (t / KS) & 1);
+            fence_after();
+            for (int x = 0; x < 2; ++x)
+              if (nX[x] > 0) issue_s(x, 0);
+            mma_commit(&k_empty[t % KS]);
+          }
+          ptx::mbar_wait(&v_full[sv], (t / kStages) & 1);
+          fence_after();
+          for (int x = 0; x < 2; ++x) {
+            if (j >= nX[x]) continue;
+            ptx::mbar_wait_poll(&p_full[x], (cntS[x] + j) & 1);
+            if (j == 0 && cntO[x] > 0) ptx::mbar_wait(&o_free[x], (cntO[x] - 1) & 1);   // previous O read out
+            fence_after();
+            const uint32_t vb = sbase + L::kVOff + sv * L::kTile;
+#pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk)
+              mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
+            if (j + 1 == nX[x]) {
+              mma_commit(&o_final[x]);
+            } else {
+              const int t1 = t + 1;
+              ptx::mbar_wait(&k_full[t1 % KS], (t1 / KS) & 1);
+              fence_after();
+              issue_s(x, j + 1);
+            }
+          }
+          mma_commit(&v_empty[sv]);
+          if (j + 1 < n_kv) mma_commit(&k_empty[(t + 1) % KS]);
+        }
+        mma_commit(q_empty);                 // Q no longer read once these MMAs retire
+        for (int x = 0; x < 2; ++x) {
+          cntS[x] += nX[x];
+          cntO[x] += nX[x] > 0 ? 1u : 0u;
+        }
+        kt += n_kv;
+        ++qi;
+      }
+    }
+  } else {
+    const int x = warp / 4;
+    uint32_t cntS = 0, cntO = 0;
+    for (int r = 0;; ++r) {
+      const int w = persist_item(r, c, G);
+      if (w >= n_items) break;
+      const VarItem it = varlen_item(p, w);
+      const int n_kv = max(it.nA, it.nB);
+      softmax_role<0, D, true, false, L>(it.p, smem, s_full, p_full, o_final, q_full, nullptr, tmem, warp, lane,
+                                         it.head, it.q_row0, it.q0A, it.q0A + kBM, it.nA, it.nB, n_kv, qmap, cntS,
+                                         cntO, o_free);
+      const int n = x == 0 ? it.nA : it.nB;
+      cntS += n;
+      cntO += n > 0 ? 1u : 0u;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -1156,6 +1394,16 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   check_rt(cudaGetLastError(), "prefill launch");
 }
 
+static int num_sms_cached() {
+  static const int sms = [] {
+    int d = 0, n = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
+  return sms;
+}
+
 // Several requests' prefills in one launch (flash_attn_varlen_func-style packing of the query
 // rows): q [total, Hq, D] packed, request i's rows at q_start[i] .. + n_q[i], attending over rows
 // [0, kv_len[i]) of slot slots[i].  The host builds each request's K/V tensor maps (rooted at its
@@ -1251,6 +1499,26 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   p.maps = reinterpret_cast<const CUtensorMap*>(dbuf);
   p.reqs = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b);
   p.work = reinterpret_cast<const int4*>(static_cast<uint8_t*>(dbuf) + maps_b + reqs_b);
+  // Persistent CTAs when the items are many and short (measured, tools/pf_persist_varlen_check.py:
+  // 64 x 128 1.28x, 32 x 256 1.18x, 16 x 512 1.13x, 8 x 2048 1.08x, 4 x 3072 1.05x, bit-equal;
+  // 2 x 8192 and 1 x 16384 (33 / 65 KV tiles per item) on par).  VATTN_PF_PERSIST=0 / 1 forces.
+  static const int persist_env = [] {
+    const char* e = getenv("VATTN_PF_PERSIST");
+    return e ? atoi(e) : -1;
+  }();
+  int64_t tiles = 0;
+  for (const auto& w_ : work) tiles += w_.first;
+  const bool persist = persist_env >= 0 ? persist_env != 0
+                                        : (int64_t)work.size() * hq > num_sms_cached() && tiles <= 24 * (int64_t)work.size();
+  if (D == 128 && persist) {
+    const int n_items = (int)work.size() * hq;
+    const int G = std::min(n_items, num_sms_cached());
+    ensure_smem_attr<pf::prefill_persist_varlen_kernel>(pf::PfL<128>::kSmem);
+    pf::prefill_persist_varlen_kernel<<<G, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, p, n_items);
+    check_rt(cudaGetLastError(), "prefill (varlen, persistent) launch");
+    check_rt(cudaEventRecord(ring.done[k], st), "varlen slot event");
+    return;
+  }
   const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), hq);
   if (D == 128) {
     ensure_smem_attr<pf::prefill_kernel<0, false, 128, true>>(pf::PfL<128>::kSmem);

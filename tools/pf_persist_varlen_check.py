@@ -1,0 +1,56 @@
+"""Persistent varlen prefill (VATTN_PF_PERSIST=1) vs the one-CTA-per-item kernel: bit-equal
+outputs on several prompt mixes, and timings.  Each setting runs in its own process."""
+import os, subprocess, sys, json
+
+CHILD = r'''
+import sys, json, torch, hashlib
+sys.path.insert(0, ".")
+from paper_2405_04437_b200.attention import prefill_attention_varlen_raw
+dev = torch.device("cuda")
+cases = {"16x512": [512] * 16, "32x256": [256] * 32, "8x2048": [2048] * 8,
+         "mixed": [100, 700, 1500, 3000, 64, 2048, 1, 333], "prefix": [300, 1000, 17],
+         "64x128": [128] * 64, "4x3072": [3072] * 4, "2x8192": [8192] * 2, "1x16384": [16384],
+         "serve8": [2900, 180, 1210, 2400, 640, 3050, 95, 1777], "noncausal": [200, 900, 1600, 40] * 4}
+res = {}
+for name, lens in cases.items():
+    n = len(lens)
+    L = max(lens) + (512 if name == "prefix" else 0)
+    g = torch.Generator(device=dev).manual_seed(n * 7 + L)
+    k = torch.randn(n, L, 8, 128, device=dev, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(n, L, 8, 128, device=dev, dtype=torch.bfloat16, generator=g)
+    tot = sum(lens)
+    q = torch.randn(tot, 32, 128, device=dev, dtype=torch.bfloat16, generator=g)
+    o = torch.empty_like(q)
+    kvl = [l + (512 if name == "prefix" else 0) for l in lens]
+    call = lambda: prefill_attention_varlen_raw(q, k, v, lens, list(range(n)), kv_lens=kvl, out=o,
+                                                causal=(name != "noncausal"))
+    for _ in range(3): call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20): call()
+    e1.record(); torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / 20
+    res[name] = {"us": us, "sha": hashlib.sha1(o.view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16],
+                 "finite": bool(torch.isfinite(o.float()).all())}
+print("RESULT " + json.dumps(res))
+'''
+
+def run(persist):
+    env = dict(os.environ, VATTN_PF_PERSIST=str(persist))
+    r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
+    for line in r.stdout.splitlines():
+        if line.startswith("RESULT "):
+            return json.loads(line[7:])
+    print(r.stdout[-2000:], r.stderr[-3000:])
+    return None
+
+quick = "--quick" in sys.argv
+a, b = run(0), run(1)
+ok = True
+for k in a:
+    same = a[k]["sha"] == b[k]["sha"]
+    ok &= same and b[k]["finite"]
+    print(f"{k:8s} grid {a[k]['us']:8.1f} us   persistent {b[k]['us']:8.1f} us   x{a[k]['us'] / b[k]['us']:.2f}   "
+          f"bit-equal {same}")
+print("ALL BIT-EQUAL" if ok else "MISMATCH")
