@@ -883,50 +883,65 @@ prefill_persist_varlen_kernel(const __grid_constant__ CUtensorMap qmap, Params p
 
   if (warp == 8) {
     // ===================== TMA producer =====================
+    // Per item: the first K / V stages first (their previous occupants belong to earlier items, so
+    // they are released without this item's MMAs), then Q once the previous item's last S MMA
+    // retired, then the rest of the K / V stream.  The next item's descriptor (two dependent
+    // loads) is fetched while the current one streams.
     if (lane == 0) {
       ptx::prefetch_tmap(&qmap);
       int kt = 0, qi = 0;                  // K/V tiles and Q loads issued so far
       constexpr int ahead = KS - kStages;
-      for (int r = 0;; ++r) {
-        const int w = persist_item(r, c, G);
-        if (w >= n_items) break;
-        const VarItem it = varlen_item(p, w);
+      int w = persist_item(0, c, G);
+      VarItem it{};
+      if (w < n_items) it = varlen_item(p, w);
+      for (int r = 0; w < n_items; ++r) {
+        const int w_next = persist_item(r + 1, c, G);
+        VarItem nxt{};
+        if (w_next < n_items) nxt = varlen_item(p, w_next);
         const int n_kv = max(it.nA, it.nB);
-        if (n_kv == 0) continue;
-        const int kvh = it.head / p.group;
-        const CUtensorMap* kmp = it.kmp;
-        const CUtensorMap* vmp = it.kmp + 1;
-        ptx::prefetch_tmap(kmp);
-        ptx::prefetch_tmap(vmp);
-        if (qi > 0) ptx::mbar_wait(q_empty, (qi - 1) & 1);
-        ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h) {
-          ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, it.head, it.q_row0 + it.q0A);
-          ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, it.head,
-                           it.q_row0 + it.q0A + kBM);
-        }
-        ++qi;
-        for (int j = 0; j < n_kv + ahead; ++j) {
-          if (j < n_kv) {
+        if (n_kv > 0) {
+          const int kvh = it.head / p.group;
+          const CUtensorMap* kmp = it.kmp;
+          const CUtensorMap* vmp = it.kmp + 1;
+          ptx::prefetch_tmap(kmp);
+          ptx::prefetch_tmap(vmp);
+          auto load_k = [&](int j) {
             const int t = kt + j, st = t % KS;
             if (t >= KS) ptx::mbar_wait(&k_empty[st], ((t / KS) - 1) & 1);
             ptx::mbar_arrive_expect_tx(&k_full[st], L::kTile);
 #pragma unroll
             for (int h = 0; h < D / 64; ++h)
               ptx::tma_load_3d(smem + L::kKOff + st * L::kTile + h * kHalf, kmp, &k_full[st], h * 64, kvh, j * kBN);
-          }
-          const int jv = j - ahead;
-          if (jv >= 0) {
+          };
+          auto load_v = [&](int jv) {
             const int t = kt + jv, st = t % kStages;
             if (t >= kStages) ptx::mbar_wait(&v_empty[st], ((t / kStages) - 1) & 1);
             ptx::mbar_arrive_expect_tx(&v_full[st], L::kTile);
 #pragma unroll
             for (int h = 0; h < D / 64; ++h)
               ptx::tma_load_3d(smem + L::kVOff + st * L::kTile + h * kHalf, vmp, &v_full[st], h * 64, kvh, jv * kBN);
+          };
+          const int k_early = min(n_kv, KS), v_early = min(n_kv, kStages);
+          for (int j = 0; j < k_early; ++j) load_k(j);
+          for (int jv = 0; jv < v_early; ++jv) load_v(jv);
+          if (qi > 0) ptx::mbar_wait(q_empty, (qi - 1) & 1);
+          ptx::mbar_arrive_expect_tx(q_full, 2 * L::kTile);
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h) {
+            ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, it.head, it.q_row0 + it.q0A);
+            ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, it.head,
+                             it.q_row0 + it.q0A + kBM);
           }
+          ++qi;
+          for (int j = k_early; j < n_kv + ahead; ++j) {
+            if (j < n_kv) load_k(j);
+            const int jv = j - ahead;
+            if (jv >= v_early && jv < n_kv) load_v(jv);
+          }
+          kt += n_kv;
         }
-        kt += n_kv;
+        w = w_next;
+        it = nxt;
       }
     }
   } else if (warp == 9) {
@@ -938,13 +953,18 @@ prefill_persist_varlen_kernel(const __grid_constant__ CUtensorMap qmap, Params p
       const uint32_t tO[2] = {tmem + 256, tmem + 256 + D};
       int kt = 0, qi = 0;
       uint32_t cntS[2] = {0, 0}, cntO[2] = {0, 0};   // tiles / items with tiles, per Q tile
-      for (int r = 0;; ++r) {
-        const int w = persist_item(r, c, G);
-        if (w >= n_items) break;
-        const VarItem it = varlen_item(p, w);
-        const int n_kv = max(it.nA, it.nB);
+      int w = persist_item(0, c, G);
+      VarItem it{};
+      if (w < n_items) it = varlen_item(p, w);
+      for (int r = 0; w < n_items; ++r, w = persist_item(r, c, G)) {
+        const int w_next = persist_item(r + 1, c, G);
+        VarItem nxt{};
+        if (w_next < n_items) nxt = varlen_item(p, w_next);   // next item's descriptor, fetched early
+        const VarItem cur = it;
+        it = nxt;
+        const int n_kv = max(cur.nA, cur.nB);
         if (n_kv == 0) continue;
-        const int nX[2] = {it.nA, it.nB};
+        const int nX[2] = {cur.nA, cur.nB};
         auto issue_s = [&](int x, int j) {
           const int st = (kt + j) % KS;
           const uint32_t qa = sbase + L::kQOff + x * L::kTile;
