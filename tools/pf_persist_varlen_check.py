@@ -12,6 +12,7 @@ cases = {"16x512": [512] * 16, "32x256": [256] * 32, "8x2048": [2048] * 8,
          "64x128": [128] * 64, "4x3072": [3072] * 4, "2x8192": [8192] * 2, "1x16384": [16384],
          "serve8": [2900, 180, 1210, 2400, 640, 3050, 95, 1777], "noncausal": [200, 900, 1600, 40] * 4}
 res = {}
+later = []
 for name, lens in cases.items():
     n = len(lens)
     L = max(lens) + (512 if name == "prefix" else 0)
@@ -33,6 +34,15 @@ for name, lens in cases.items():
     us = e0.elapsed_time(e1) * 1e3 / 20
     res[name] = {"us": us, "sha": hashlib.sha1(o.view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16],
                  "finite": bool(torch.isfinite(o.float()).all())}
+    if name in ("mixed", "prefix", "noncausal"):    # a few requests against the fp32 oracle, after
+        offs = [0]                                  # the timings (CPU work perturbs them)
+        for l in lens: offs.append(offs[-1] + l)
+        later.append((name, [(q[offs[i]:offs[i + 1]].cpu(), k[i, :kvl[i]].cpu(), v[i, :kvl[i]].cpu(),
+                              o[offs[i]:offs[i + 1]].cpu()) for i in (0, 1, len(lens) - 1)]))
+from oracle.attention import prefill_ref, max_rel_err
+for name, reqs in later:
+    res[name]["oracle_err"] = max(max_rel_err(oo, prefill_ref(qq, kk, vv, causal=(name != "noncausal")))
+                                  for qq, kk, vv, oo in reqs)
 print("RESULT " + json.dumps(res))
 '''
 
@@ -51,6 +61,10 @@ ok = True
 for k in a:
     same = a[k]["sha"] == b[k]["sha"]
     ok &= same and b[k]["finite"]
+    oe = b[k].get("oracle_err")
+    if oe is not None:
+        ok &= oe <= 2e-2
     print(f"{k:8s} grid {a[k]['us']:8.1f} us   persistent {b[k]['us']:8.1f} us   x{a[k]['us'] / b[k]['us']:.2f}   "
-          f"bit-equal {same}")
+          f"bit-equal {same}" + (f"   oracle max_rel_err {oe:.2e}" if oe is not None else ""))
 print("ALL BIT-EQUAL" if ok else "MISMATCH")
+sys.exit(0 if ok else 1)
