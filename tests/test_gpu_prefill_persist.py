@@ -1,6 +1,7 @@
 """GPU: the persistent varlen prefill kernel (one CTA per SM walking the work list)
-is bit-identical to the one-CTA-per-item kernel, and within 2e-2 of the fp32 oracle, on short, long, mixed, prefixed and non-causal
-prompt mixes.  Each kernel choice runs in its own process (VATTN_PF_PERSIST is read once)."""
+is bit-identical to the one-CTA-per-item kernel on short, long, mixed, prefixed and non-causal
+prompt mixes, and within 2e-2 of the fp32 oracle on three requests of the mixed, prefixed and
+non-causal ones.  Each kernel choice runs in its own process (VATTN_PF_PERSIST is read once)."""
 
 import subprocess
 import sys
