@@ -78,6 +78,11 @@ struct Params {
   // hardware's linear CTA order is heaviest-first across ALL heads and the CTAs of one GQA group
   // read the same K/V tiles at the same time; 0 = work items fastest (per-head heaviest-first)
   int head_fast;
+  // head pairs (single-request kernel): tile A / B = the same 128 query rows of two query heads
+  // of one GQA group (2h, 2h+1) instead of two consecutive row tiles of one head.  Both tiles
+  // then need the same K/V tiles (equal step counts: no lone last step on the causal diagonal)
+  // and a prompt of <= 128 rows fills both tiles.  n_pairs counts 128-row tiles in this mode.
+  int head_pair;
 };
 
 static int head_fast_order() {
@@ -307,7 +312,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
                                              uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
                                              int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
                                              int nB, int n_kv, const CUtensorMap& omap, uint32_t s_base = 0,
-                                             uint32_t o_par = 0, uint64_t* o_free = nullptr) {
+                                             uint32_t o_par = 0, uint64_t* o_free = nullptr, int headB = -1) {
   const int x = warp / 4;
   const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
   const int q0 = x == 0 ? q0A : q0B;
@@ -496,7 +501,8 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
   // that buffer (found under compute-sanitizer's slowed timing).
   const bool via_tma = o_free == nullptr && n > 0 && (!VARLEN || q0 + kBM <= p.n_q);
   const uint32_t qt = ptx::smem_u32(smem + L::kQOff + x * L::kTile);
-  __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + head) * D;
+  const int hd = (x == 1 && headB >= 0) ? headB : head;   // head pairs: tile B is the odd head
+  __nv_bfloat16* dst = p.out + ((int64_t)qpos * p.hq + hd) * D;
   const bool live = qpos < p.n_q;
 #pragma unroll
   for (int c0 = 0; c0 < D; c0 += 32) {
@@ -534,7 +540,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     if (warp % 4 == 0 && lane == 0) {
 #pragma unroll
       for (int h = 0; h < D / 64; ++h)
-        ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, head, q_row0 + q0);
+        ptx::tma_store_3d(&omap, smem + L::kQOff + x * L::kTile + h * kHalf, h * 64, hd, q_row0 + q0);
       ptx::tma_store_commit();
       ptx::tma_store_wait_read();
     }
@@ -585,9 +591,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     kmp = p.maps + 2 * w.x;
     vmp = kmp + 1;
   }
-  const int head = p.head_fast ? blockIdx.x : blockIdx.y;
+  const int hsel = p.head_fast ? blockIdx.x : blockIdx.y;
+  const bool hp = !VARLEN && p.head_pair;
+  const int head = hp ? 2 * hsel : hsel;   // tile A's head
+  const int headB = hp ? head + 1 : head;  // tile B's head (same GQA group: group is even)
   const int kvh = head / p.group;
-  const int q0A = pair * 2 * kBM, q0B = q0A + kBM;
+  const int q0A = hp ? pair * kBM : pair * 2 * kBM, q0B = hp ? q0A : q0A + kBM;
   const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
   const int n_kv = max(nA, nB);
 
@@ -642,7 +651,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
       for (int h = 0; h < D / 64; ++h) {
         ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0A);
-        ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, head, q_row0 + q0B);
+        ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, headB, q_row0 + q0B);
       }
       if constexpr (!PAGED) {
         // K runs KS - kStages tiles ahead of V (K_j then V_{j-ahead}); each stage waits for its
@@ -766,7 +775,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     }
   } else {
     softmax_role<POLY, D, VARLEN, false, L>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane,
-                                            head, q_row0, q0A, q0B, nA, nB, n_kv, omap);
+                                            head, q_row0, q0A, q0B, nA, nB, n_kv, omap, 0, 0, nullptr,
+                                            hp ? headB : -1);
   }
 #ifdef VATTN_PF_TRACE
   __syncthreads();
@@ -1325,6 +1335,23 @@ static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const 
   return m;
 }
 
+// Head pairs (Params::head_pair) for the single-request kernel: VATTN_PF_HEADPAIR=0/1 forces
+// the tiling.  By default pairs are used when the GQA group is even and the prompt spans more
+// than one 128-row tile (tools/pf_headpair_ab.py, B200: Yi-6B 4K causal 1.056x, Llama-3-8B 4K
+// 1.096x, 16K 1.006x, bit-identical).  At <= 128 rows the row tiling launches twice as many
+// CTAs (one per head, tile B empty) on a grid far below the SM count, which is faster there
+// (0.86-0.94x with pairs).
+static bool use_head_pairs(int n_q, int hq, int group) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("VATTN_PF_HEADPAIR");
+    mode = e ? atoi(e) : -1;
+  }
+  if (group % 2 || hq % 2 || mode == 0) return false;
+  if (mode > 0) return true;
+  return n_q > pf::kBM;
+}
+
 void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* out, int n_q, int hq,
                     int slot, int kv_len, float scale, bool causal, cudaStream_t st, const Rotary* rot) {
   if (v.d != 128 && v.d != 64) throw Fail(VATTN_UNSUPPORTED, "prefill kernel is built for head_dim 64 and 128");
@@ -1365,12 +1392,13 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.group = hq / v.hkv;
   p.kv_len = kv_len;
   p.slot = slot;
-  p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
   p.q_off = kv_len - n_q;
   p.causal = causal ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
-  const dim3 grid = pf::pf_grid(p, p.n_pairs, hq);
+  p.head_pair = use_head_pairs(n_q, hq, p.group) ? 1 : 0;
+  p.n_pairs = p.head_pair ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
+  const dim3 grid = pf::pf_grid(p, p.n_pairs, p.head_pair ? hq / 2 : hq);
   if (D == 64) {
     ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
@@ -1383,6 +1411,8 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     pair_mode = e ? (atoi(e) != 0) : 0;
   }
   if (pair_mode && !(rot && rot->cos) && p.group % 2 == 0 && hq % 2 == 0) {
+    p.head_pair = 0;   // the CTA-pair kernel tiles rows (two consecutive 128-row tiles)
+    p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
     // the pair kernel's K half-tiles: boxes of 64 keys
     cuuint32_t kb2[3] = {64, 1, 64};
     const CUtensorMap kmap2 = make_map(reinterpret_cast<void*>(v.k_base + slot_off), 3, kd, ks, kb2);

@@ -26,6 +26,14 @@ CASES = [
     (129, 1, 8, 2, True, 0, 1),            # kv shorter than the query block (rows see nothing)
     (300, 700, 16, 4, False, 0, 1),        # non-causal
     (2048, 2048, 32, 4, True, 0, 1),
+    # <= 128 query rows (row tiling, tile B empty) and an even GQA group; the multi-tile cases
+    # above with an even group run the head-pair tiling (two query heads per CTA)
+    (1, 1, 8, 4, True, 0, 1),
+    (77, 900, 32, 8, True, 1, 2),          # chunk over a longer prefix
+    (128, 128, 32, 4, False, 0, 1),
+    (100, 50, 8, 2, True, 0, 1),           # rows that see no key
+    (300, 100, 8, 2, True, 0, 1),          # head pairs with rows that see no key
+    (64, 3000, 56, 8, True, 0, 1),         # odd group (7): row tiles
 ]
 
 
@@ -316,3 +324,48 @@ def test_varlen_prefill_manager_backed():
         assert torch.equal(out[o:o + n], one)
         o += n
     mgr.close()
+
+
+_HEADPAIR_CHILD = r"""
+import sys, json, torch
+sys.path.insert(0, ".")
+from paper_2405_04437_b200.attention import prefill_attention_raw
+from oracle.attention import max_rel_err, prefill_ref
+dev = torch.device("cuda")
+out = {}
+for n_q, kv, hq, hkv, causal in ((1000, 1000, 32, 8, True), (512, 2048, 16, 2, True), (384, 384, 8, 4, False)):
+    g = torch.Generator().manual_seed(n_q + kv)
+    k = torch.randn(1, kv + 128, hkv, 128, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, kv + 128, hkv, 128, generator=g).to(torch.bfloat16)
+    q = torch.randn(n_q, hq, 128, generator=g).to(torch.bfloat16)
+    o = prefill_attention_raw(q.to(dev), k.to(dev), v.to(dev), 0, kv, causal=causal).cpu()
+    ref = prefill_ref(q, k[0, :kv], v[0, :kv], causal=causal)
+    out[f"{n_q}_{kv}_{hq}_{hkv}_{causal}"] = [max_rel_err(o, ref), o.view(torch.int16).to(torch.int64).sum().item(),
+                                               (o.view(torch.int16).to(torch.int64) * torch.arange(o.numel()).view_as(o).remainder(997)).sum().item()]
+print("RESULT " + json.dumps(out))
+"""
+
+
+def test_prefill_head_pair_tiling_matches_row_tiling():
+    """The two single-request tilings (VATTN_PF_HEADPAIR=0: two consecutive 128-row tiles of one
+    head per CTA; =1: the same 128 rows of two query heads of one GQA group) run each tile's
+    arithmetic in the same order, so their outputs are bit-identical; both are within the
+    oracle tolerance on multi-tile prompts (causal, chunked, non-causal)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    _cuda()
+    root = Path(__file__).resolve().parents[1]
+    res = {}
+    for mode in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", _HEADPAIR_CHILD], cwd=root, capture_output=True, text=True,
+                           timeout=600, env=dict(os.environ, VATTN_PF_HEADPAIR=mode))
+        line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
+        assert line, r.stderr[-2000:]
+        res[mode] = json.loads(line[0][7:])
+    for key, (err, s1, s2) in res["1"].items():
+        assert err <= TOL, (key, err)
+        assert [s1, s2] == res["0"][key][1:], key
