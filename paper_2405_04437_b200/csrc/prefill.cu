@@ -592,7 +592,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     vmp = kmp + 1;
   }
   const int hsel = p.head_fast ? blockIdx.x : blockIdx.y;
-  const bool hp = !VARLEN && p.head_pair;
+  const bool hp = p.head_pair != 0;
   const int head = hp ? 2 * hsel : hsel;   // tile A's head
   const int headB = hp ? head + 1 : head;  // tile B's head (same GQA group: group is even)
   const int kvh = head / p.group;
@@ -817,25 +817,28 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 __device__ __forceinline__ int persist_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
 
 struct VarItem {
-  int head, q_row0, q0A, nA, nB;
+  int head, headB, q_row0, q0A, q0B, nA, nB;
   const CUtensorMap* kmp;
   Params p;      // the launch's Params with this item's request fields (n_q, kv_len, q_off, out)
 };
 
 __device__ __forceinline__ VarItem varlen_item(const Params& p, int w) {
   VarItem it;
-  const int4 wk = p.work[w / p.hq];
+  const int hper = p.head_pair ? p.hq / 2 : p.hq;   // items per work entry
+  const int4 wk = p.work[w / hper];
   const int4 rq = p.reqs[wk.x];
-  it.head = w % p.hq;
+  it.head = p.head_pair ? 2 * (w % hper) : w % hper;
+  it.headB = p.head_pair ? it.head + 1 : it.head;
   it.q_row0 = rq.x;
   it.p = p;
   it.p.n_q = rq.y;
   it.p.kv_len = rq.z;
   it.p.q_off = rq.z - rq.y;
   it.p.out = p.out + (int64_t)rq.x * p.hq * 128;
-  it.q0A = wk.y * 2 * kBM;
+  it.q0A = p.head_pair ? wk.y * kBM : wk.y * 2 * kBM;
+  it.q0B = p.head_pair ? it.q0A : it.q0A + kBM;
   it.nA = kv_tiles_for(it.p, it.q0A);
-  it.nB = kv_tiles_for(it.p, it.q0A + kBM);
+  it.nB = kv_tiles_for(it.p, it.q0B);
   it.kmp = p.maps + 2 * wk.x;
   return it;
 }
@@ -939,8 +942,8 @@ prefill_persist_varlen_kernel(const __grid_constant__ CUtensorMap qmap, Params p
 #pragma unroll
           for (int h = 0; h < D / 64; ++h) {
             ptx::tma_load_3d(smem + L::kQOff + h * kHalf, &qmap, q_full, h * 64, it.head, it.q_row0 + it.q0A);
-            ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, it.head,
-                             it.q_row0 + it.q0A + kBM);
+            ptx::tma_load_3d(smem + L::kQOff + L::kTile + h * kHalf, &qmap, q_full, h * 64, it.headB,
+                             it.q_row0 + it.q0B);
           }
           ++qi;
           for (int j = k_early; j < n_kv + ahead; ++j) {
@@ -1037,8 +1040,8 @@ prefill_persist_varlen_kernel(const __grid_constant__ CUtensorMap qmap, Params p
       const VarItem it = varlen_item(p, w);
       const int n_kv = max(it.nA, it.nB);
       softmax_role<0, D, true, false, L>(it.p, smem, s_full, p_full, o_final, q_full, nullptr, tmem, warp, lane,
-                                         it.head, it.q_row0, it.q0A, it.q0A + kBM, it.nA, it.nB, n_kv, qmap, cntS,
-                                         cntO, o_free);
+                                         it.head, it.q_row0, it.q0A, it.q0B, it.nA, it.nB, n_kv, qmap, cntS,
+                                         cntO, o_free, p.head_pair ? it.headB : -1);
       const int n = x == 0 ? it.nA : it.nB;
       cntS += n;
       cntO += n > 0 ? 1u : 0u;
@@ -1341,7 +1344,10 @@ static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const 
 // 1.096x, 16K 1.006x, bit-identical).  At <= 128 rows the row tiling launches twice as many
 // CTAs (one per head, tile B empty) on a grid far below the SM count, which is faster there
 // (0.86-0.94x with pairs).
-static bool use_head_pairs(int n_q, int hq, int group) {
+static int num_sms_cached();
+// rows_items / pair_items: CTAs (work items) of the launch under each tiling.  Pairs never have
+// more; they are taken when they keep the count or still fill every SM.
+static bool use_head_pairs(int64_t rows_items, int64_t pair_items, int hq, int group) {
   static int mode = -2;
   if (mode == -2) {
     const char* e = getenv("VATTN_PF_HEADPAIR");
@@ -1349,7 +1355,7 @@ static bool use_head_pairs(int n_q, int hq, int group) {
   }
   if (group % 2 || hq % 2 || mode == 0) return false;
   if (mode > 0) return true;
-  return n_q > pf::kBM;
+  return pair_items >= rows_items || pair_items >= num_sms_cached();
 }
 
 void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* out, int n_q, int hq,
@@ -1396,7 +1402,8 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.causal = causal ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
-  p.head_pair = use_head_pairs(n_q, hq, p.group) ? 1 : 0;
+  p.head_pair = use_head_pairs((int64_t)hq * ((n_q + 2 * pf::kBM - 1) / (2 * pf::kBM)),
+                               (int64_t)(hq / 2) * ((n_q + pf::kBM - 1) / pf::kBM), hq, p.group) ? 1 : 0;
   p.n_pairs = p.head_pair ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
   const dim3 grid = pf::pf_grid(p, p.n_pairs, p.head_pair ? hq / 2 : hq);
   if (D == 64) {
@@ -1476,6 +1483,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   std::vector<CUtensorMap> maps(2 * (size_t)n_req);
   std::vector<int4> reqs(n_req);
   std::vector<std::pair<int, int4>> work;   // (kv tiles, item)
+  int64_t rows_items = 0, pair_items = 0;
   for (int i = 0; i < n_req; ++i) {
     if (slots[i] < 0 || slots[i] >= v.n_slots) throw Fail(VATTN_VALUE_ERROR, "slot out of range");
     if (kv_len[i] < 0 || kv_len[i] > v.slot_tokens) throw Fail(VATTN_VALUE_ERROR, "kv_len out of range");
@@ -1489,9 +1497,15 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
     maps[2 * i] = make_map(reinterpret_cast<void*>(v.k_base + off), 3, kd, ks, kb);
     maps[2 * i + 1] = make_map(reinterpret_cast<void*>(v.v_base + off), 3, kd, ks, kb);
     reqs[i] = make_int4(q_start[i], n_q[i], kv_len[i], 0);
-    const int pairs = (n_q[i] + 2 * pf::kBM - 1) / (2 * pf::kBM);
+    rows_items += (int64_t)hq * ((n_q[i] + 2 * pf::kBM - 1) / (2 * pf::kBM));
+    pair_items += (int64_t)(hq / 2) * ((n_q[i] + pf::kBM - 1) / pf::kBM);
+  }
+  const bool hp = use_head_pairs(rows_items, pair_items, hq, hq / v.hkv);
+  const int rows_per_item = hp ? pf::kBM : 2 * pf::kBM;
+  for (int i = 0; i < n_req; ++i) {
+    const int pairs = (n_q[i] + rows_per_item - 1) / rows_per_item;
     for (int pr = 0; pr < pairs; ++pr) {
-      const int q_last = std::min((pr + 1) * 2 * pf::kBM, n_q[i]) - 1;
+      const int q_last = std::min((pr + 1) * rows_per_item, n_q[i]) - 1;
       const int last_key = causal ? std::min(kv_len[i] - 1, q_last + kv_len[i] - n_q[i]) : kv_len[i] - 1;
       work.push_back({last_key < 0 ? 0 : last_key / pf::kBN + 1, make_int4(i, pr, 0, 0)});
     }
@@ -1543,6 +1557,8 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.hq = hq;
   p.group = hq / v.hkv;
+  p.head_pair = hp ? 1 : 0;
+  const int heads_per_item = hp ? hq / 2 : hq;   // CTAs (items) per work entry
   p.causal = causal ? 1 : 0;
   if (scale <= 0.f) scale = 1.f / sqrtf((float)D);
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -1559,9 +1575,10 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
   int64_t tiles = 0;
   for (const auto& w_ : work) tiles += w_.first;
   const bool persist = persist_env >= 0 ? persist_env != 0
-                                        : (int64_t)work.size() * hq > num_sms_cached() && tiles <= 24 * (int64_t)work.size();
+                                        : (int64_t)work.size() * heads_per_item > num_sms_cached() &&
+                                              tiles <= 24 * (int64_t)work.size();
   if (D == 128 && persist) {
-    const int n_items = (int)work.size() * hq;
+    const int n_items = (int)work.size() * heads_per_item;
     const int G = std::min(n_items, num_sms_cached());
     ensure_smem_attr<pf::prefill_persist_varlen_kernel>(pf::PfL<128>::kSmem);
     pf::prefill_persist_varlen_kernel<<<G, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, p, n_items);
@@ -1569,7 +1586,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
     check_rt(cudaEventRecord(ring.done[k], st), "varlen slot event");
     return;
   }
-  const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), hq);
+  const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), heads_per_item);
   if (D == 128) {
     ensure_smem_attr<pf::prefill_kernel<0, false, 128, true>>(pf::PfL<128>::kSmem);
     pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, omap, p);

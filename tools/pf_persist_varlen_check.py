@@ -46,14 +46,35 @@ for name, reqs in later:
 print("RESULT " + json.dumps(res))
 '''
 
-def run(persist):
+def run(persist, headpair=None):
     env = dict(os.environ, VATTN_PF_PERSIST=str(persist))
+    if headpair is not None:
+        env["VATTN_PF_HEADPAIR"] = str(headpair)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
     for line in r.stdout.splitlines():
         if line.startswith("RESULT "):
             return json.loads(line[7:])
     print(r.stdout[-2000:], r.stderr[-3000:])
     return None
+
+if "--headpair" in sys.argv:
+    # 2 x 2: grid / persistent x row tiles / head pairs (Params::head_pair); all bit-equal to grid+rows
+    sets = {(pe, hp): run(pe, hp) for pe in (0, 1) for hp in (0, 1)}
+    base = sets[(0, 0)]
+    ok = all(r is not None for r in sets.values())
+    print(f"{'case':10s}" + "".join(f"{'persist' if pe else 'grid'}+{'heads' if hp else 'rows':6s} us   " for pe, hp in sets))
+    for k in base:
+        row = f"{k:10s}"
+        for key, r in sets.items():
+            same = r[k]["sha"] == base[k]["sha"]
+            oe = r[k].get("oracle_err")
+            ok &= same and r[k]["finite"] and (oe is None or oe <= 2e-2)
+            row += f"{r[k]['us']:11.1f}{'' if same else '!'}     "
+        best = min(sets, key=lambda kk: sets[kk][k]["us"])
+        row += f"best {best}  x{base[k]['us'] / sets[best][k]['us']:.2f} vs grid+rows"
+        print(row)
+    print("ALL BIT-EQUAL" if ok else "MISMATCH")
+    sys.exit(0 if ok else 1)
 
 quick = "--quick" in sys.argv
 a, b = run(0), run(1)
