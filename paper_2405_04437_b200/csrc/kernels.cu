@@ -922,7 +922,37 @@ static void run_decode(const CUtensorMap& km, const CUtensorMap& vm, DecodeParam
   // clusters of up to 8 splits (portable size).  16-CTA non-portable clusters were measured much
   // slower (B 1 x 32K, 16 splits: 49 vs 28 us with the combine kernel): the scheduler has to find
   // 16 free SMs of one GPC for each cluster.
-  const bool cl = cl_env && p.num_splits >= 2 && p.num_splits <= 8 && p.sink.n_ranks == 0;
+  bool cl = cl_env && p.num_splits >= 2 && p.num_splits <= 8 && p.sink.n_ranks == 0;
+  if (cl) {
+    // Every unit's splits must be co-resident as one cluster: when the GPU cannot hold all the
+    // units' clusters at once, the leftover clusters run as a second wave (B 2 x 64K with 8
+    // splits: 125.6 vs 80.3 us; B 3 x 32K with 6 splits: 92.4 vs 62.6 us, tools/split_fill_probe.py).
+    // Then the partials go through the combine kernel instead, whose CTAs need no co-scheduling.
+    static std::map<int, int> max_clusters;   // per cluster size, for this kernel variant
+    static std::mutex mc_mu;
+    std::lock_guard<std::mutex> lk(mc_mu);
+    auto it = max_clusters.find(p.num_splits);
+    if (it == max_clusters.end()) {
+      cudaLaunchConfig_t oc{};
+      oc.gridDim = dim3(p.num_splits, 1, 1);
+      oc.blockDim = dim3(decode_threads(CW));
+      oc.dynamicSmemBytes = L::kBytes;
+      cudaLaunchAttribute ca{};
+      ca.id = cudaLaunchAttributeClusterDimension;
+      ca.val.clusterDim.x = p.num_splits;
+      ca.val.clusterDim.y = 1;
+      ca.val.clusterDim.z = 1;
+      oc.attrs = &ca;
+      oc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &oc) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = 0;
+      }
+      it = max_clusters.emplace(p.num_splits, n).first;
+    }
+    if ((int64_t)batch * hkv > it->second) cl = false;
+  }
   p.cluster_combine = cl ? 1 : 0;
   {
     cudaLaunchConfig_t cfg{};

@@ -216,3 +216,28 @@ def test_fused_decode_rotary_matches_oracle(d, rd, inter, splits):
     for b, n in enumerate(lens):      # the cached row is the rotated k (one bf16 rounding of fp32 math)
         assert torch.allclose(got[b, n].float(), kr[b].float(), rtol=1e-2, atol=1e-2)
         assert torch.equal(vd.cpu()[b, n], vn[b])
+
+
+@pytest.mark.parametrize("batch,ctx,splits", [(2, 65536, 8), (3, 32768, 6), (8, 4096, 2)])
+def test_split_decode_where_unit_clusters_cannot_all_coreside(batch, ctx, splits):
+    """Split counts whose per-unit clusters (one cluster of `splits` CTAs per (row, KV head))
+    would not all fit on the GPU at once fall back to the combine kernel (B 2 x 64K at 8 splits
+    ran as two waves, 1.56x slower); every split count agrees with the oracle and with the
+    unsplit kernel, ragged lengths included."""
+    from paper_2405_04437_b200.attention import decode_attention_raw
+
+    dev = _cuda()
+    hq, hkv, d = 32, 8, 128
+    gen = torch.Generator(device=dev).manual_seed(batch * 131 + ctx)
+    k = torch.randn(batch, ctx, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    v = torch.randn(batch, ctx, hkv, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    q = torch.randn(batch, hq, d, device=dev, generator=gen, dtype=torch.bfloat16)
+    seq = torch.tensor([ctx - 37 * b for b in range(batch)], dtype=torch.int32, device=dev)
+    o_split = decode_attention_raw(q, k, v, seq, num_splits=splits)
+    o_one = decode_attention_raw(q, k, v, seq, num_splits=1)
+    torch.cuda.synchronize()
+    assert torch.isfinite(o_split.float()).all()
+    assert (o_split.float() - o_one.float()).abs().max().item() <= 2e-2 * o_one.float().abs().max().item()
+    rows = [0, batch - 1]
+    ref = decode_ref(q[rows].cpu(), k[rows].cpu(), v[rows].cpu(), seq[rows].cpu())
+    assert max_rel_err(o_split[rows].cpu(), ref) <= TOL
