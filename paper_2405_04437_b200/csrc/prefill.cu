@@ -83,6 +83,10 @@ struct Params {
   // then need the same K/V tiles (equal step counts: no lone last step on the causal diagonal)
   // and a prompt of <= 128 rows fills both tiles.  n_pairs counts 128-row tiles in this mode.
   int head_pair;
+  // early PV (prefill_kernel): the softmax releases keys 0..63 of P once stored, and the issuer
+  // starts their PV MMAs while keys 64..127 are exponentiated.  1 always, 0 never, -1 in CTAs
+  // that run a single tile (tools/pf_earlypv_ab.py)
+  int early_pv;
 };
 
 static int head_fast_order() {
@@ -312,7 +316,8 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
                                              uint64_t* o_final, uint64_t* q_full, uint64_t* q_ready, uint32_t tmem,
                                              int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
                                              int nB, int n_kv, const CUtensorMap& omap, uint32_t s_base = 0,
-                                             uint32_t o_par = 0, uint64_t* o_free = nullptr, int headB = -1) {
+                                             uint32_t o_par = 0, uint64_t* o_free = nullptr, int headB = -1,
+                                             uint64_t* p_lo = nullptr, uint64_t* pv_lo = nullptr) {
   const int x = warp / 4;
   const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
   const int q0 = x == 0 ? q0A : q0B;
@@ -374,6 +379,11 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
       if (!__any_sync(0xffffffffu, m_lo * p.scale_log2 > m_run + kRescaleThreshold)) {
         TMEM_ST16(tS + 0, pk);
         TMEM_ST16(tS + 16, (pk + 16));
+        if (p_lo) {   // early PV: keys 0..63 of P go to the tensor core while keys 64..127 run
+          tmem_wait_st();
+          fence_before();
+          arrive_lead<PAIR>(&p_lo[x]);
+        }
         float m_hi = -INFINITY;
         float2 acc_hi = make_float2(0.f, 0.f);
         softmax_half<POLY>(tS + 64, sc2f, nm2f, pk, m_hi, acc_hi);
@@ -387,7 +397,13 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
           // 0..63 in place, recompute keys 64..127 from S (intact) against the new max.
           const float m_new = fmaxf(m_run, fmaxf(mx_hi, m_lo * p.scale_log2));
           const float f = ptx::fast_exp2(m_run - m_new);
-          if (j > 0) {
+          if (p_lo) {
+            // P_lo was released at the old max and may already be in O: let that PV retire,
+            // then O (which holds it) is rescaled below like every earlier contribution
+            ptx::mbar_wait(&pv_lo[x], (s_base + j) & 1);
+            fence_after();
+          }
+          if (j > 0 || p_lo) {
 #pragma unroll 1
             for (int c0 = 0; c0 < D; c0 += 32) {
               uint32_t o[32];
@@ -398,7 +414,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
               TMEM_ST32(tO + c0, o);
             }
           }
-          {
+          if (!p_lo) {
             uint32_t pl[32];
             TMEM_LD32(tS + 0, pl);
             tmem_wait_ld();
@@ -483,6 +499,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     l_run += lsum;
     tmem_wait_st();
     fence_before();
+    if (p_lo) arrive_lead<PAIR>(&p_lo[x]);   // both halves at once on this path
     arrive_lead<PAIR>(&p_full[x]);
     if (lane == 0 && (warp % 4) == 0) PF_TRACE(x, j, 2);
   }
@@ -567,6 +584,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   uint64_t* p_full = bars + 15;           // [2]
   uint64_t* o_final = bars + 17;          // [2]
   uint64_t* q_ready = bars + 19;          // rotary: both Q tiles rotated in shared memory
+  uint64_t* p_lo = bars + 20;             // [2] early PV: keys 0..63 of P stored
+  uint64_t* pv_lo = bars + 22;            // [2] early PV: the PV MMAs of keys 0..63 retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -599,6 +618,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   const int q0A = hp ? pair * kBM : pair * 2 * kBM, q0B = hp ? q0A : q0A + kBM;
   const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
   const int n_kv = max(nA, nB);
+  // early PV pays only where a CTA runs one tile (no ping-pong partner to fill the tensor core
+  // during the softmax): 128-row chunks over a 16K prefix 1.067x; with two tiles 0.98-1.00x
+  const bool early = !PAGED && (p.early_pv > 0 || (p.early_pv < 0 && min(nA, nB) == 0));
 
 #ifdef VATTN_PF_TRACE
   const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
@@ -626,6 +648,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
       ptx::mbar_init(&o_final[x], 1);
     }
     ptx::mbar_init(q_ready, 2 * kBM);
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&p_lo[x], kBM);
+      ptx::mbar_init(&pv_lo[x], 1);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 9) {
@@ -725,11 +751,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
         mma_commit(&s_full[x]);
       };
-      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j
+      auto issue_pv = [&](int x, int j, int k_lo, int k_hi) {  // O_x += P_x(j) V_j, keys [16 k_lo, 16 k_hi)
         const int s = j % kStages;
         const uint32_t vb = sbase + L::kVOff + s * L::kTile;
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
+        for (int kk = k_lo; kk < k_hi; ++kk)
           mma_ts(tO[x], tS[x] + kk * 8, sdesc(vb + kk * 2048, kHalf, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
       };
       ptx::mbar_wait(q_full, 0);
@@ -748,11 +774,23 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         for (int x = 0; x < 2; ++x) {
           if (j >= nX[x]) continue;
           PF_TRACE(2 + x, j, 0);
-          // polled without a suspend hint: the issuer wakes sooner (measured 1229 vs 1220 TF)
-          ptx::mbar_wait_poll(&p_full[x], j & 1);
-          PF_TRACE(2 + x, j, 1);
-          fence_after();
-          issue_pv(x, j);
+          if (early) {
+            // keys 0..63 of P as soon as the softmax stored them, the rest when it is done
+            ptx::mbar_wait_poll(&p_lo[x], j & 1);
+            fence_after();
+            issue_pv(x, j, 0, kBN / 32);
+            mma_commit(&pv_lo[x]);
+            ptx::mbar_wait_poll(&p_full[x], j & 1);
+            PF_TRACE(2 + x, j, 1);
+            fence_after();
+            issue_pv(x, j, kBN / 32, kBN / 16);
+          } else {
+            // polled without a suspend hint: the issuer wakes sooner (measured 1229 vs 1220 TF)
+            ptx::mbar_wait_poll(&p_full[x], j & 1);
+            PF_TRACE(2 + x, j, 1);
+            fence_after();
+            issue_pv(x, j, 0, kBN / 16);
+          }
           PF_TRACE(2 + x, j, 2);
           if (j + 1 == nX[x]) {
             mma_commit(&o_final[x]);
@@ -776,7 +814,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   } else {
     softmax_role<POLY, D, VARLEN, false, L>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane,
                                             head, q_row0, q0A, q0B, nA, nB, n_kv, omap, 0, 0, nullptr,
-                                            hp ? headB : -1);
+                                            hp ? headB : -1, early ? p_lo : nullptr, early ? pv_lo : nullptr);
   }
 #ifdef VATTN_PF_TRACE
   __syncthreads();
@@ -1344,6 +1382,15 @@ static CUtensorMap make_map(void* base, int rank, const cuuint64_t* dims, const 
 // 1.096x, 16K 1.006x, bit-identical).  At <= 128 rows the row tiling launches twice as many
 // CTAs (one per head, tile B empty) on a grid far below the SM count, which is faster there
 // (0.86-0.94x with pairs).
+static int early_pv_mode() {
+  static int v = -1;   // 2 = automatic
+  if (v < 0) {
+    const char* e = getenv("VATTN_PF_EARLYPV");
+    v = e ? (atoi(e) != 0 ? 1 : 0) : 2;
+  }
+  return v == 2 ? -1 : v;
+}
+
 static int num_sms_cached();
 // rows_items / pair_items: CTAs (work items) of the launch under each tiling.  Pairs never have
 // more; they are taken when they keep the count or still fill every SM.
@@ -1406,6 +1453,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
                                (int64_t)(hq / 2) * ((n_q + pf::kBM - 1) / pf::kBM), hq, p.group) ? 1 : 0;
   p.n_pairs = p.head_pair ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
   const dim3 grid = pf::pf_grid(p, p.n_pairs, p.head_pair ? hq / 2 : hq);
+  p.early_pv = early_pv_mode();
   if (D == 64) {
     ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
     pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
@@ -1587,6 +1635,7 @@ void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq,
     return;
   }
   const dim3 grid = pf::pf_grid(p, (unsigned)work.size(), heads_per_item);
+  p.early_pv = early_pv_mode();
   if (D == 128) {
     ensure_smem_attr<pf::prefill_kernel<0, false, 128, true>>(pf::PfL<128>::kSmem);
     pf::prefill_kernel<0, false, 128, true><<<grid, pf::kThreads, pf::PfL<128>::kSmem, st>>>(qmap, qmap, qmap, omap, p);
