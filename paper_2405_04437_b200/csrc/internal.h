@@ -151,6 +151,10 @@ void launch_decode(KernelState* ks, int cache_key, const CacheView& v, const voi
 void launch_prefill_varlen(const CacheView& v, const void* q, void* out, int hq, int n_req,
                            const int32_t* q_start, const int32_t* n_q, const int32_t* slots,
                            const int32_t* kv_len, float scale, bool causal, cudaStream_t st);
+// merge split partials (fp32 O / l, log2-domain LSE; layout of decode_combine_kernel) into bf16
+// rows of `out` [rows, D] (split-KV prefill)
+void launch_split_combine(const float* part_o, const float* part_lse, void* out, int rows, int splits, int hq,
+                          int d, cudaStream_t st);
 void launch_prefill(KernelState* ks, int cache_key, const CacheView& v, const void* q, void* out,
                     int n_q, int hq, int slot, int kv_len, float scale, bool causal,
                     cudaStream_t st, const Rotary* rot = nullptr);

@@ -1126,6 +1126,24 @@ static void decode_common(const CUtensorMap& km, const CUtensorMap& vm, int d, i
   }
 }
 
+void launch_split_combine(const float* part_o, const float* part_lse, void* out, int rows, int splits, int hq,
+                          int d, cudaStream_t st) {
+  if (rows <= 0) return;
+  GatherSink none{};
+  if (d == 128) {
+    const int per_block = 128 / (128 / 4);
+    decode_combine_kernel<128><<<(rows + per_block - 1) / per_block, 128, 0, st>>>(
+        part_o, part_lse, reinterpret_cast<__nv_bfloat16*>(out), rows, splits, hq, none);
+  } else if (d == 64) {
+    const int per_block = 128 / (64 / 4);
+    decode_combine_kernel<64><<<(rows + per_block - 1) / per_block, 128, 0, st>>>(
+        part_o, part_lse, reinterpret_cast<__nv_bfloat16*>(out), rows, splits, hq, none);
+  } else {
+    throw Fail(VATTN_UNSUPPORTED, "split combine is built for head_dim 64 and 128");
+  }
+  check_rt(cudaGetLastError(), "split combine launch");
+}
+
 void launch_decode(KernelState* ks, int, const CacheView& v, const void* q, void* out, int batch,
                    int hq, const int32_t* seqlens, const int32_t* batch_idx, float scale,
                    int num_splits, void* ws, int64_t ws_bytes, cudaStream_t st, const void* k_new,

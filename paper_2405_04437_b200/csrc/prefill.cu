@@ -87,6 +87,13 @@ struct Params {
   // starts their PV MMAs while keys 64..127 are exponentiated.  1 always, 0 never, -1 in CTAs
   // that run a single tile (tools/pf_earlypv_ab.py)
   int early_pv;
+  // split-KV (single-request kernel, small grids): blockIdx.z = split; each CTA runs its tiles'
+  // KV range [j0, j0 + T) and writes fp32 O / l and lse = m + log2(l) (log2 domain) per row and
+  // split into part_o [n_q * hq][splits][D] / part_lse [n_q * hq][splits]; the decode combine
+  // kernel merges them (kv_splits <= 1: plain bf16 output)
+  int kv_splits;
+  float* part_o;
+  float* part_lse;
 };
 
 static int head_fast_order() {
@@ -317,7 +324,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
                                              int warp, int lane, int head, int q_row0, int q0A, int q0B, int nA,
                                              int nB, int n_kv, const CUtensorMap& omap, uint32_t s_base = 0,
                                              uint32_t o_par = 0, uint64_t* o_free = nullptr, int headB = -1,
-                                             uint64_t* p_lo = nullptr, uint64_t* pv_lo = nullptr) {
+                                             uint64_t* p_lo = nullptr, uint64_t* pv_lo = nullptr, int j0 = 0) {
   const int x = warp / 4;
   const int row = (warp % 4) * 32 + lane;          // TMEM lane == row of the query tile
   const int q0 = x == 0 ? q0A : q0B;
@@ -361,7 +368,7 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     fence_after();
     // pass 1: row max (chunks of 32 columns keep register pressure low; TMEM reads are cheap).
     // Only diagonal / tail tiles need the per-element mask; the others take the plain path.
-    const int k0 = j * kBN;
+    const int k0 = (j0 + j) * kBN;
     const bool need_mask = (k0 + kBN > p.kv_len) || (p.causal && k0 + kBN - 1 > qpos + p.q_off);
     const int lim = need_mask ? min(p.kv_len, p.causal ? qpos + p.q_off + 1 : p.kv_len) - k0 : kBN;
     const bool warp_mask = __any_sync(0xffffffffu, need_mask);
@@ -509,6 +516,34 @@ __device__ __forceinline__ void softmax_role(const Params& p, uint8_t* smem, uin
     fence_after();
   }
   const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+  if (!VARLEN && o_free == nullptr && p.kv_splits > 1) {
+    // split-KV partial of this row: O / l in fp32 and its log2-domain LSE (-inf: no keys here)
+    // (tcgen05.ld is warp-collective: every lane loads, only rows < n_q store)
+    const int hd = (x == 1 && headB >= 0) ? headB : head;
+    const bool live_row = qpos < p.n_q;
+    const int64_t prow = ((int64_t)(live_row ? qpos : 0) * p.hq + hd) * p.kv_splits + blockIdx.z;
+    float* po = p.part_o + prow * D;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t o[32];
+      if (n > 0) {
+        TMEM_LD32(tO + c0, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0u;
+      }
+      if (live_row) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)
+          *reinterpret_cast<float4*>(po + c0 + c) =
+              make_float4(__uint_as_float(o[c]) * inv, __uint_as_float(o[c + 1]) * inv,
+                          __uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
+      }
+    }
+    if (live_row) p.part_lse[prow] = l_run > 0.f ? m_run + __log2f(l_run) : -INFINITY;
+    return;
+  }
   // Full tiles (and any tile of a single-request launch: the map clips rows >= n_q) go out
   // through shared memory and one TMA store: the tile's Q buffer is free once o_final landed
   // (every MMA reading it has retired), and whole 128-byte rows reach L2 instead of the
@@ -616,7 +651,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   const int headB = hp ? head + 1 : head;  // tile B's head (same GQA group: group is even)
   const int kvh = head / p.group;
   const int q0A = hp ? pair * kBM : pair * 2 * kBM, q0B = hp ? q0A : q0A + kBM;
-  const int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
+  int nA = kv_tiles_for(p, q0A), nB = kv_tiles_for(p, q0B);
+  int j0 = 0;                              // split-KV: first KV tile of this CTA's range
+  if (!VARLEN && !PAGED && p.kv_splits > 1) {
+    const int per = (max(nA, nB) + p.kv_splits - 1) / p.kv_splits;
+    j0 = blockIdx.z * per;
+    nA = max(0, min(nA - j0, per));
+    nB = max(0, min(nB - j0, per));
+  }
   const int n_kv = max(nA, nB);
   // early PV pays only where a CTA runs one tile (no ping-pong partner to fill the tensor core
   // during the softmax): 128-row chunks over a 16K prefix 1.067x; with two tiles 0.98-1.00x
@@ -690,7 +732,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             ptx::mbar_arrive_expect_tx(&k_full[s], L::kTile);
 #pragma unroll
             for (int h = 0; h < D / 64; ++h)
-              ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh, j * kBN);
+              ptx::tma_load_3d(smem + L::kKOff + s * L::kTile + h * kHalf, kmp, &k_full[s], h * 64, kvh, (j0 + j) * kBN);
           }
           const int jv = j - ahead;
           if (jv >= 0) {
@@ -699,7 +741,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             ptx::mbar_arrive_expect_tx(&v_full[s], L::kTile);
 #pragma unroll
             for (int h = 0; h < D / 64; ++h)
-              ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh, jv * kBN);
+              ptx::tma_load_3d(smem + L::kVOff + s * L::kTile + h * kHalf, vmp, &v_full[s], h * 64, kvh, (j0 + jv) * kBN);
           }
         }
       }
@@ -814,7 +856,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
   } else {
     softmax_role<POLY, D, VARLEN, false, L>(p, smem, s_full, p_full, o_final, q_full, q_ready, tmem, warp, lane,
                                             head, q_row0, q0A, q0B, nA, nB, n_kv, omap, 0, 0, nullptr,
-                                            hp ? headB : -1, early ? p_lo : nullptr, early ? pv_lo : nullptr);
+                                            hp ? headB : -1, early ? p_lo : nullptr, early ? pv_lo : nullptr, j0);
   }
 #ifdef VATTN_PF_TRACE
   __syncthreads();
@@ -1391,15 +1433,29 @@ static int early_pv_mode() {
   return v == 2 ? -1 : v;
 }
 
-static int num_sms_cached();
-// rows_items / pair_items: CTAs (work items) of the launch under each tiling.  Pairs never have
-// more; they are taken when they keep the count or still fill every SM.
-static bool use_head_pairs(int64_t rows_items, int64_t pair_items, int hq, int group) {
+static int head_pair_env() {   // -1 automatic, 0 / 1 forced (VATTN_PF_HEADPAIR)
   static int mode = -2;
   if (mode == -2) {
     const char* e = getenv("VATTN_PF_HEADPAIR");
     mode = e ? atoi(e) : -1;
   }
+  return mode;
+}
+
+static int split_kv_mode() {   // VATTN_PF_SPLITKV: 0 off, 1 automatic (default), N > 1 forced
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("VATTN_PF_SPLITKV");
+    mode = e ? std::max(0, atoi(e)) : 1;
+  }
+  return mode;
+}
+
+static int num_sms_cached();
+// rows_items / pair_items: CTAs (work items) of the launch under each tiling.  Pairs never have
+// more; they are taken when they keep the count or still fill every SM.
+static bool use_head_pairs(int64_t rows_items, int64_t pair_items, int hq, int group) {
+  const int mode = head_pair_env();
   if (group % 2 || hq % 2 || mode == 0) return false;
   if (mode > 0) return true;
   return pair_items >= rows_items || pair_items >= num_sms_cached();
@@ -1451,21 +1507,56 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
   p.scale_log2 = scale * 1.4426950408889634f;
   p.head_pair = use_head_pairs((int64_t)hq * ((n_q + 2 * pf::kBM - 1) / (2 * pf::kBM)),
                                (int64_t)(hq / 2) * ((n_q + pf::kBM - 1) / pf::kBM), hq, p.group) ? 1 : 0;
-  p.n_pairs = p.head_pair ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
-  const dim3 grid = pf::pf_grid(p, p.n_pairs, p.head_pair ? hq / 2 : hq);
-  p.early_pv = early_pv_mode();
-  if (D == 64) {
-    ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
-    pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
-    check_rt(cudaGetLastError(), "prefill launch");
-    return;
-  }
   static int pair_mode = -1;
   if (pair_mode < 0) {
     const char* e = getenv("VATTN_PF_PAIR");   // 1: CTA-pair kernel (cta_group::2) where it applies
     pair_mode = e ? (atoi(e) != 0) : 0;
   }
-  if (pair_mode && !(rot && rot->cos) && p.group % 2 == 0 && hq % 2 == 0) {
+  const bool use_pair_kernel = D == 128 && pair_mode && !(rot && rot->cos) && p.group % 2 == 0 && hq % 2 == 0;
+  // Split-KV for grids far below the SM count with long KV ranges (e.g. a 128-row chunk over a
+  // long prefix: 32 CTAs of one tile each): head pairs first (two tiles per CTA), then the KV
+  // range of every CTA is split so the grid fills the SMs; partials merge in the combine kernel.
+  auto n_ctas = [&](bool hp_) {
+    return (int64_t)(hp_ ? hq / 2 : hq) * (hp_ ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM));
+  };
+  const int nkv_max = (std::max(kv_len, 1) + pf::kBN - 1) / pf::kBN;
+  const int split_env = split_kv_mode();
+  int splits = 1;
+  if (!use_pair_kernel && split_env != 0) {
+    if (split_env > 1) {
+      splits = split_env;
+    } else if (n_ctas(p.head_pair != 0) * 2 <= num_sms_cached() && nkv_max >= 16) {
+      if (p.group % 2 == 0 && hq % 2 == 0 && head_pair_env() != 0) p.head_pair = 1;
+      splits = (int)std::min<int64_t>(std::min<int64_t>(16, num_sms_cached() / n_ctas(p.head_pair != 0)), nkv_max / 8);
+    }
+    splits = std::max(1, std::min(splits, nkv_max));
+  }
+  p.n_pairs = p.head_pair ? (n_q + pf::kBM - 1) / pf::kBM : (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
+  dim3 grid = pf::pf_grid(p, p.n_pairs, p.head_pair ? hq / 2 : hq);
+  p.early_pv = early_pv_mode();
+  void* ws = nullptr;
+  if (splits > 1) {
+    const int64_t rows = (int64_t)n_q * hq;
+    check_rt(cudaMallocAsync(&ws, (size_t)rows * splits * (D + 1) * sizeof(float), st), "cudaMallocAsync(split prefill)");
+    p.kv_splits = splits;
+    p.part_o = static_cast<float*>(ws);
+    p.part_lse = p.part_o + rows * splits * D;
+    grid.z = splits;
+  }
+  auto finish = [&]() {
+    if (splits > 1) {
+      launch_split_combine(p.part_o, p.part_lse, out, n_q * hq, splits, hq, D, st);
+      check_rt(cudaFreeAsync(ws, st), "cudaFreeAsync(split prefill)");
+    }
+  };
+  if (D == 64) {
+    ensure_smem_attr<pf::prefill_kernel<0, false, 64>>(pf::PfL<64>::kSmem);
+    pf::prefill_kernel<0, false, 64><<<grid, pf::kThreads, pf::PfL<64>::kSmem, st>>>(qmap, kmap, vmap, omap, p);
+    check_rt(cudaGetLastError(), "prefill launch");
+    finish();
+    return;
+  }
+  if (use_pair_kernel) {
     p.head_pair = 0;   // the CTA-pair kernel tiles rows (two consecutive 128-row tiles)
     p.n_pairs = (n_q + 2 * pf::kBM - 1) / (2 * pf::kBM);
     // the pair kernel's K half-tiles: boxes of 64 keys
@@ -1497,6 +1588,7 @@ void launch_prefill(KernelState*, int, const CacheView& v, const void* q, void* 
     pf::prefill_kernel<3><<<grid, pf::kThreads, kS, st>>>(qmap, kmap, vmap, omap, p);
   }
   check_rt(cudaGetLastError(), "prefill launch");
+  finish();
 }
 
 static int num_sms_cached() {

@@ -291,7 +291,13 @@ def test_varlen_prefill_equals_per_request_prefill(d):
         if m:
             one = prefill_attention_raw(qd[o:o + m].contiguous(), kd, vd, sl, kl)
             torch.cuda.synchronize()
-            assert torch.equal(out[o:o + m].cpu(), one.cpu())
+            # a lone launch on a grid below half the SMs with >= 16 KV tiles splits its KV range
+            # (split-KV, a different fp32 summation); every other launch is bit-identical
+            split = (kl + 127) // 128 >= 16 and hq * ((m + 255) // 256) * 2 <= torch.cuda.get_device_properties(dev).multi_processor_count
+            if split:
+                assert max_rel_err(one.cpu(), out[o:o + m].float().cpu()) <= 1e-2
+            else:
+                assert torch.equal(out[o:o + m].cpu(), one.cpu())
             ref = prefill_ref(q[o:o + m], k[sl, :kl], v[sl, :kl])
             assert max_rel_err(out[o:o + m].cpu(), ref) <= TOL
         o += m
@@ -412,6 +418,52 @@ def test_prefill_early_pv_matches_oracle():
     root = Path(__file__).resolve().parents[1]
     r = subprocess.run([sys.executable, "-c", _EARLYPV_CHILD], cwd=root, capture_output=True, text=True,
                        timeout=600, env=dict(os.environ, VATTN_PF_EARLYPV="1"))
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
+    assert line, r.stderr[-2000:]
+    for key, (err, finite) in json.loads(line[0][7:]).items():
+        assert finite and err <= TOL, (key, err)
+
+
+_SPLITKV_CHILD = r"""
+import sys, json, torch
+sys.path.insert(0, ".")
+from paper_2405_04437_b200.attention import prefill_attention_raw
+from oracle.attention import max_rel_err, prefill_ref
+dev = torch.device("cuda")
+out = {}
+for n_q, kv, hq, hkv, causal, d in ((128, 4000, 32, 8, True, 128), (1, 3000, 8, 2, True, 128),
+                                    (200, 2500, 16, 4, False, 128), (300, 100, 8, 2, True, 128),
+                                    (128, 16384, 32, 4, True, 128), (96, 2100, 8, 4, True, 64)):
+    g = torch.Generator().manual_seed(n_q * 3 + kv)
+    k = torch.randn(1, kv + 128, hkv, d, generator=g).to(torch.bfloat16)
+    v = torch.randn(1, kv + 128, hkv, d, generator=g).to(torch.bfloat16)
+    k[:, kv:] = float("nan")
+    v[:, kv:] = float("nan")
+    q = torch.randn(n_q, hq, d, generator=g).to(torch.bfloat16)
+    o = prefill_attention_raw(q.to(dev), k.to(dev), v.to(dev), 0, kv, causal=causal).cpu()
+    ref = prefill_ref(q, k[0, :kv], v[0, :kv], causal=causal)
+    out[f"{n_q}_{kv}_{hq}_{hkv}_{causal}_{d}"] = [max_rel_err(o, ref), bool(torch.isfinite(o.float()).all())]
+print("RESULT " + json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "3", "7"])
+def test_prefill_split_kv_matches_oracle(mode):
+    """Split-KV prefill (VATTN_PF_SPLITKV: 0 off, 1 automatic - on for grids below half the SMs
+    with >= 16 KV tiles -, N forced): each CTA runs a slice of the KV tiles, writes fp32 partials
+    and a log2-domain LSE, and the combine kernel merges them.  Within the oracle tolerance for
+    chunks over long prefixes, a single query row, non-causal, rows that see no key (their
+    splits are all empty) and D 64; NaN rows past kv_len are never read."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    _cuda()
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", _SPLITKV_CHILD], cwd=root, capture_output=True, text=True,
+                       timeout=600, env=dict(os.environ, VATTN_PF_SPLITKV=mode))
     line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
     assert line, r.stderr[-2000:]
     for key, (err, finite) in json.loads(line[0][7:]).items():
