@@ -900,6 +900,11 @@ static int auto_splits(int units, int max_len) {
   // split only below that; keep >= 4 tiles (256 tokens) per split.
   const int tiles = std::max(1, (max_len + kTile - 1) / kTile);
   int s = (128 + units - 1) / units;
+  // Rounding up past one CTA per SM drops the grid into the 2-CTA / 3-stage variant; when one
+  // fewer split still keeps >= 100 CTAs the single-wave deep-ring variant is faster (B 5 x 32K:
+  // 3 splits 98.6 vs 4 splits 101.3 us; B 7 x 16K: 2 vs 3, 71.2 vs 72.9; tools/split_fill_probe.py)
+  const int sms = num_sms();
+  if (s > 1 && units * s > sms && (sms / units) * units >= 100) s = sms / units;
   s = std::min(s, std::max(1, tiles / 4));
   return std::max(1, std::min(s, kMaxSplits));
 }
